@@ -1,0 +1,207 @@
+/* schwarz_b200 — C ABI of the B200-native multilevel ORAS inpainting solver.
+ *
+ * Drop-in replacement for the solver entry points of the reference
+ * schwarz-inpaint library (header-only C++20, /root/reference/proj).  Every
+ * entry point cites the reference interface it replaces; paths are relative
+ * to proj/include/schwarz_inpaint/.  Plain pointers and sizes only: no C++
+ * or CUDA types cross this boundary, and no exception escapes it.
+ *
+ * Data layout (identical to the reference's ImageBuffer / InpaintingMask,
+ * image.hpp:24-94): images are planar double, channel c occupying
+ * [c*w*h, (c+1)*w*h), row-major; masks are uint8 per pixel, nonzero = known.
+ *
+ * Errors: every call returns an si_status.  SI_ERR_INVALID_ARGUMENT is
+ * returned exactly where the reference throws std::invalid_argument (the
+ * message, retrievable with si_last_error(), names the same check).
+ * Non-convergence is not an error: it is reported in si_report.converged
+ * and si_report.diagnostic, as the reference's SolveReport does.
+ *
+ * Threading: one si_ctx per host thread (or per GPU); contexts are
+ * independent.  si_last_error() is thread-local.
+ */
+#ifndef SCHWARZ_B200_H
+#define SCHWARZ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SI_ABI_VERSION 1
+#define SI_MAX_LEVELS 32
+
+typedef enum {
+  SI_OK = 0,
+  SI_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument (image.hpp:18-20) */
+  SI_ERR_CUDA = 2,
+  SI_ERR_OOM = 3,
+  SI_ERR_UNSUPPORTED = 4,      /* e.g. block_size > 32, method cg/mlcg */
+  SI_ERR_NO_DEVICE = 5
+} si_status;
+
+/* Method (methods.hpp:13). */
+typedef enum {
+  SI_METHOD_CG = 0,
+  SI_METHOD_MLCG = 1,
+  SI_METHOD_RAS = 2,
+  SI_METHOD_ORAS = 3,
+  SI_METHOD_MLORAS = 4
+} si_method;
+
+typedef enum { SI_AVERAGING_KNOWN_ONLY = 0, SI_AVERAGING_ALL_PIXELS = 1 } si_averaging;    /* multilevel.hpp:25 */
+typedef enum { SI_NORMALIZER_INITIAL_GUESS = 0, SI_NORMALIZER_RHS_NORM = 1 } si_normalizer; /* schwarz.hpp:36 */
+typedef enum { SI_FLAVOUR_RAS = 0, SI_FLAVOUR_ORAS = 1 } si_flavour;                      /* schwarz.hpp:29 */
+typedef enum { SI_PRECISION_FP64 = 0, SI_PRECISION_FP32 = 1 } si_precision;
+
+/* RunOptions (methods.hpp:40-55), field for field, plus the device
+ * arithmetic type.  si_default_options() fills the reference defaults. */
+typedef struct si_options {
+  double tolerance;             /* 1e-3 */
+  int levels;                   /* 3 (mlcg / mloras only) */
+  int block_size;               /* 32 */
+  int overlap;                  /* 6 */
+  double alpha;                 /* 0.25 = kDefaultOrasAlpha (schwarz.hpp:34) */
+  double coarse_tolerance;      /* 1e-2 */
+  int averaging;                /* si_averaging, KnownOnly */
+  double local_tolerance;       /* SolverConfig local{1e-2, 30, 30} */
+  int local_max_iterations;
+  int local_check_interval;
+  int max_outer_iterations;     /* 1000 */
+  int cg_max_iterations;        /* 100000 (mlcg; unsupported here) */
+  int cg_check_interval;        /* 4 */
+  int normalizer;               /* si_normalizer, InitialGuess */
+  int precision;                /* si_precision, FP64 (the reference's type) */
+} si_options;
+
+/* SolveReport (cg.hpp:29-34) + LevelRunStats (schwarz.hpp:254-260) per level. */
+typedef struct si_report {
+  int iterations;               /* finest-level outer sweeps */
+  double final_relative_residual;
+  int converged;
+  char diagnostic[128];
+  int depth;                    /* pyramid levels actually built */
+  int level_iterations[SI_MAX_LEVELS];     /* index 0 = finest */
+  double level_final_rel[SI_MAX_LEVELS];
+  int level_converged[SI_MAX_LEVELS];
+  long long local_solves;       /* blocks x channels x sweeps, all levels */
+  long long local_failures;     /* local CG cap reached or breakdown */
+  long long local_cg_iterations;/* sum of local CG iterations (device-counted) */
+  double elapsed_ms;            /* host wall clock around the solve */
+} si_report;
+
+/* Trace sink: one call per finest-level outer iteration, row 0 included
+ * (ConvergenceTrace::append, metrics.hpp:74-77).  psnr is NaN unless a
+ * reference image was passed. */
+typedef void (*si_trace_fn)(int iteration, double time_ms, double rel_residual, double psnr,
+                            void* user);
+
+typedef struct si_ctx si_ctx;
+
+/* ---- library / context ------------------------------------------------ */
+int si_abi_version(void);
+const char* si_last_error(void);
+const char* si_status_string(si_status s);
+void si_default_options(si_options* opt);
+/* Validates options as run_method/multilevel_solve would (multilevel.hpp:243-244,
+ * partition.hpp:68-73, schwarz.hpp:275-276, cg.hpp:75-80).  No device needed. */
+si_status si_validate_options(int method, const si_options* opt);
+
+si_status si_create(int device, si_ctx** out);
+void si_destroy(si_ctx* ctx);
+/* Releases cached per-level device buffers. */
+si_status si_trim(si_ctx* ctx);
+
+/* ---- solver entry points ----------------------------------------------- */
+
+/* run_method(method, f, mask, options, reference) (methods.hpp:57-88) with
+ * HOST buffers: f and reference are w*h*c planar doubles, mask w*h bytes,
+ * out receives the w*h*c reconstruction.  reference may be NULL. */
+si_status si_run_method(si_ctx* ctx, int method, const double* f, const uint8_t* mask, int w,
+                        int h, int c, const si_options* opt, const double* reference, double* out,
+                        si_report* report, si_trace_fn trace, void* user);
+
+/* Same, DEVICE-resident: d_f, d_mask, d_reference, d_out live in device
+ * memory of ctx's device; work is issued on `stream` (a cudaStream_t, NULL =
+ * the context's own stream).  The call returns when the solve is complete. */
+si_status si_run_method_device(si_ctx* ctx, int method, const double* d_f, const uint8_t* d_mask,
+                               int w, int h, int c, const si_options* opt,
+                               const double* d_reference, double* d_out, si_report* report,
+                               si_trace_fn trace, void* user, void* stream);
+
+/* solve_schwarz(f, mask, partition_domain(w,h,block,overlap), options, reference)
+ * (schwarz.hpp:349-389): single level on an explicit, unclamped partition.
+ * flavour: si_flavour; host buffers. */
+si_status si_solve_schwarz(si_ctx* ctx, const double* f, const uint8_t* mask, int w, int h, int c,
+                           int block_size, int overlap, int flavour, const si_options* opt,
+                           const double* reference, double* out, si_report* report,
+                           si_trace_fn trace, void* user);
+
+/* run_schwarz_level(op, part, b, u, r0, tol, opt, row) (schwarz.hpp:266-323):
+ * the finest seam, u in/out, host buffers.  b and u are w*h*c planar. */
+si_status si_run_schwarz_level(si_ctx* ctx, const uint8_t* mask, int w, int h, int c,
+                               const double* b, double* u, int block_size, int overlap,
+                               double r0_norm, double tolerance, int flavour,
+                               const si_options* opt, si_report* report, si_trace_fn trace,
+                               void* user);
+
+/* canonical_r0(op, b, normalizer) (schwarz.hpp:333-345), host buffers. */
+si_status si_canonical_r0(si_ctx* ctx, const uint8_t* mask, int w, int h, int c, const double* b,
+                          int normalizer, double* r0_norm);
+
+/* ---- building blocks (device-executed; host buffers) --------------------- */
+
+/* One outer sweep: u_new = u + sum_i R_i^T D_i v_i on partition_domain(w,h,
+ * block,overlap) (schwarz.hpp:305-318).  Counters may be NULL. */
+si_status si_schwarz_sweep(si_ctx* ctx, const uint8_t* mask, int w, int h, int c, const double* b,
+                           const double* u, int block_size, int overlap, int flavour,
+                           const si_options* opt, double* u_new, long long* failures,
+                           long long* cg_iterations);
+/* sum_i (b - A u)_i^2 per channel (residual_into + vec::dot, operators.hpp:91-97). */
+si_status si_residual_sumsq(si_ctx* ctx, const uint8_t* mask, int w, int h, int c,
+                            const double* u, const double* b, double* sumsq);
+/* restrict_level (multilevel.hpp:33-70): coarse grid is ceil(w/2) x ceil(h/2). */
+si_status si_restrict_level(si_ctx* ctx, const uint8_t* mask, const double* values, int w, int h,
+                            int c, int averaging, uint8_t* coarse_mask, double* coarse_values);
+/* prolongate (multilevel.hpp:101-128) of one channel. */
+si_status si_prolongate(si_ctx* ctx, const double* coarse, int cw, int ch, int fw, int fh,
+                        double* fine);
+/* LocalOperator::apply for block `index` of partition_domain(w,h,block,overlap)
+ * (build_local_operator schwarz.hpp:115-130, apply :57-75); v, out: block cells. */
+si_status si_local_operator_apply(si_ctx* ctx, const uint8_t* mask, int w, int h, int block_size,
+                                  int overlap, int index, int flavour, double alpha,
+                                  const double* v, double* out);
+
+/* ---- host-only helpers (no device needed) -------------------------------- */
+
+/* partition_domain (partition.hpp:67-106).  rects receives 8 ints per block:
+ * x0, y0, width, height, own_x0, own_y0, own_x1, own_y1 (row-major blocks). */
+si_status si_partition_domain(int w, int h, int block_size, int overlap, int* blocks_x,
+                              int* blocks_y, int* rects, int rects_capacity);
+/* synthetic_test_image (synthetic.hpp:14-59) and random_mask (masks.hpp:25-43):
+ * the reference's seeded input generators (libstdc++ <random>). */
+si_status si_synthetic_test_image(int w, int h, int c, uint64_t seed, double* out);
+si_status si_random_mask(int w, int h, double density, uint64_t seed, uint8_t* out);
+/* mse_per_channel / psnr (metrics.hpp:30-56) on host buffers. */
+si_status si_psnr(const double* u, const double* f, int w, int h, int c, double* psnr_db);
+
+/* ---- instrumentation ---------------------------------------------------- */
+
+/* Per-kernel device time (CUDA events on the launching stream) accumulated
+ * while enabled; kind: 0 residual, 1 sweep, 2 restrict, 3 prolong, 4 ingest/export. */
+typedef struct si_kernel_stats {
+  long long launches[8];
+  double device_ms[8];
+  double algorithmic_bytes[8];
+} si_kernel_stats;
+si_status si_set_profiling(si_ctx* ctx, int enabled);
+si_status si_get_kernel_stats(si_ctx* ctx, si_kernel_stats* out, int reset);
+/* Pinned host memory for zero-staging host<->device copies. */
+si_status si_host_alloc(size_t bytes, void** ptr);
+si_status si_host_free(void* ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1101 @@
+// Host orchestration of the multilevel ORAS solver + the C ABI
+// (include/schwarz_b200.h).  Everything below the ABI runs on the device:
+// the pyramid (K5 ingest, K3 restrict), per level the residual norms (K1)
+// and fused sweeps (K2), and the prolongation (K4).  The host only keeps the
+// outer loop's scalar decisions (rel <= tol, outer >= max_outer), exactly as
+// run_schwarz_level (schwarz.hpp:288-320) and multilevel_solve
+// (multilevel.hpp:239-310) take them.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <string>
+#include <vector>
+#include <functional>
+
+#include "../../include/schwarz_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "sweep.cuh"
+
+using namespace sib;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Failure {
+  si_status status;
+  std::string message;
+};
+
+[[noreturn]] void fail(si_status s, const std::string& msg) { throw Failure{s, msg}; }
+
+void check_arg(bool ok, const std::string& msg) {
+  if (!ok) fail(SI_ERR_INVALID_ARGUMENT, msg);
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();
+  if (e == cudaErrorMemoryAllocation) fail(SI_ERR_OOM, std::string(what) + ": out of device memory");
+  fail(SI_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(x) cuda_check((x), #x)
+
+using Clock = std::chrono::steady_clock;
+
+double ms_since(Clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+// ---------------------------------------------------------------- buffers
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t want) {
+    if (want <= bytes) return;
+    release();
+    CK(cudaMalloc(&ptr, want));
+    bytes = want;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(ptr);
+  }
+};
+
+struct LevelBuf {
+  DevBuf mask, b, u0, u1;
+};
+
+enum Kind { K_RESIDUAL = 0, K_SWEEP = 1, K_RESTRICT = 2, K_PROLONG = 3, K_INGEST = 4, K_COUNT = 5 };
+
+struct PendingEvent {
+  int kind;
+  double bytes;
+  cudaEvent_t start, stop;
+};
+
+}  // namespace
+
+struct si_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  std::vector<LevelBuf> levels;
+  DevBuf in_f, in_mask, in_ref, out_img, aux;   // host-API staging
+  DevBuf red_partials, red_out, counters;
+  DevBuf ticket;
+  double* host_red = nullptr;                   // pinned, for the scalar D2H
+  unsigned long long* host_cnt = nullptr;       // pinned
+  int profiling = 0;
+  std::vector<PendingEvent> pending;
+  std::vector<cudaEvent_t> event_pool;
+  si_kernel_stats stats{};
+  int sweep_nw64 = 2, sweep_nw32 = 1;           // warps per sweep CTA
+};
+
+namespace {
+
+struct Ctx {
+  si_ctx& c;
+  cudaStream_t s;
+};
+
+cudaEvent_t take_event(si_ctx& c) {
+  if (!c.event_pool.empty()) {
+    cudaEvent_t e = c.event_pool.back();
+    c.event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  return e;
+}
+
+// Brackets one kernel launch with CUDA events on the launching stream when
+// profiling is enabled; resolved after the next synchronisation.
+struct Timed {
+  Ctx& x;
+  int kind;
+  double bytes;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Timed(Ctx& x_, int k, double by) : x(x_), kind(k), bytes(by) {
+    if (x.c.profiling) {
+      a = take_event(x.c);
+      b = take_event(x.c);
+      CK(cudaEventRecord(a, x.s));
+    }
+  }
+  ~Timed() noexcept(false) {
+    if (a) {
+      CK(cudaEventRecord(b, x.s));
+      x.c.pending.push_back({kind, bytes, a, b});
+    }
+  }
+};
+
+void resolve_events(si_ctx& c) {
+  for (auto& p : c.pending) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(p.stop) == cudaSuccess && cudaEventElapsedTime(&ms, p.start, p.stop) == cudaSuccess) {
+      c.stats.launches[p.kind] += 1;
+      c.stats.device_ms[p.kind] += ms;
+      c.stats.algorithmic_bytes[p.kind] += p.bytes;
+    }
+    c.event_pool.push_back(p.start);
+    c.event_pool.push_back(p.stop);
+  }
+  c.pending.clear();
+}
+
+void sync(Ctx& x) {
+  CK(cudaStreamSynchronize(x.s));
+  if (!x.c.pending.empty()) resolve_events(x.c);
+}
+
+int grid_for(size_t n, int threads, int cap) {
+  size_t g = (n + threads - 1) / threads;
+  return static_cast<int>(std::max<size_t>(1, std::min<size_t>(g, cap)));
+}
+
+// ---------------------------------------------------------------- launches
+template <typename T>
+void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W, int H, int C,
+                     int mode, double* out) {
+  const size_t N = static_cast<size_t>(W) * H;
+  const int g = grid_for(N, kRedThreads, kRedBlocksMax);
+  x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(g) * C);
+  x.c.ticket.ensure(sizeof(unsigned int) * 4);
+  Timed t(x, K_RESIDUAL, static_cast<double>(N) * (C * sizeof(T) * (mode == 1 ? 1 : 2) + (mode == 1 ? 0 : 1)));
+  residual_sumsq_kernel<T><<<dim3(g, C), kRedThreads, 0, x.s>>>(
+      mask, u, b, W, H, N, mode, x.c.red_partials.as<double>(), out, x.c.ticket.as<unsigned int>());
+  CK(cudaGetLastError());
+}
+
+template <typename T>
+void launch_sq_error(Ctx& x, const T* u, const double* f, size_t N, int C, double* out) {
+  const int g = grid_for(N, kRedThreads, kRedBlocksMax);
+  x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(g) * C);
+  x.c.ticket.ensure(sizeof(unsigned int) * 4);
+  sq_error_kernel<T><<<dim3(g, C), kRedThreads, 0, x.s>>>(
+      u, f, N, x.c.red_partials.as<double>(), out, x.c.ticket.as<unsigned int>());
+  CK(cudaGetLastError());
+}
+
+struct LocalCfg {
+  double tol;
+  int max_it;
+  int check;
+};
+
+template <typename T, int NW>
+void launch_sweep_nw(Ctx& x, const SweepArgs<T>& a, int nblocks, int C) {
+  const size_t smem = sizeof(SweepSmem<T, NW>);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(oras_sweep_kernel<T, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    attr = true;
+  }
+  oras_sweep_kernel<T, NW><<<dim3(nblocks, C), NW * 32, smem, x.s>>>(a);
+  CK(cudaGetLastError());
+}
+
+template <typename T>
+void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_new, int W, int H,
+                  int C, int block, int overlap, int flavour, double alpha, const LocalCfg& lc,
+                  bool b_known_only, unsigned long long* counters) {
+  if (block > kMaxBlock)
+    fail(SI_ERR_UNSUPPORTED, "block size " + std::to_string(block) + " exceeds the supported 32");
+  SweepArgs<T> a;
+  a.mask = mask;
+  a.b = b;
+  a.u_old = u_old;
+  a.u_new = u_new;
+  a.W = W;
+  a.H = H;
+  a.N = static_cast<size_t>(W) * H;
+  a.ax = Axis::make(W, block, overlap);
+  a.ay = Axis::make(H, block, overlap);
+  a.am1 = static_cast<T>(alpha - 1.0);
+  a.ras = flavour == SI_FLAVOUR_RAS;
+  a.ltol = static_cast<T>(lc.tol);
+  a.lmax = lc.max_it;
+  a.lcheck = lc.check;
+  a.b_known_only = b_known_only;
+  a.counters = counters;
+  const int nblocks = a.ax.count * a.ay.count;
+  const double bytes = static_cast<double>(a.N) * (2.0 * C * sizeof(T) + 1.0);
+  Timed t(x, K_SWEEP, bytes);
+  const int nw = sizeof(T) == 8 ? x.c.sweep_nw64 : x.c.sweep_nw32;
+  switch (nw) {
+    case 1: launch_sweep_nw<T, 1>(x, a, nblocks, C); break;
+    case 4: launch_sweep_nw<T, 4>(x, a, nblocks, C); break;
+    default: launch_sweep_nw<T, 2>(x, a, nblocks, C); break;
+  }
+}
+
+// ---------------------------------------------------------------- options
+void validate_options_common(const si_options& o) {
+  check_arg(o.tolerance > 0.0 && o.coarse_tolerance > 0.0,
+            "multilevel_solve: tolerances must be positive");
+  check_arg(o.averaging == 0 || o.averaging == 1, "averaging must be KnownOnly or AllPixels");
+  check_arg(o.normalizer == 0 || o.normalizer == 1, "normalizer must be InitialGuess or RhsNorm");
+  check_arg(o.precision == SI_PRECISION_FP64 || o.precision == SI_PRECISION_FP32,
+            "precision must be FP64 or FP32");
+}
+
+// cg_solve's validate_solver_config (cg.hpp:75-80), applied to the local
+// configuration before the first sweep that runs local solves.
+void validate_local(const si_options& o) {
+  check_arg(o.local_tolerance > 0.0, "SolverConfig: tolerance must be positive");
+  check_arg(o.local_max_iterations >= 0, "SolverConfig: max_iterations must be non-negative");
+  check_arg(o.local_check_interval >= 1, "SolverConfig: residual_check_interval must be >= 1");
+}
+
+void validate_partition(int w, int h, int block, int overlap) {
+  // partition_domain (partition.hpp:68-73)
+  check_arg(w > 0 && h > 0, "partition_domain: image dimensions must be positive");
+  check_arg(block > 0, "partition_domain: block_size must be positive");
+  check_arg(overlap >= 0, "partition_domain: overlap must be non-negative");
+  check_arg(overlap < block, "partition_domain: overlap must be smaller than block_size");
+  check_arg(block <= w && block <= h, "partition_domain: block_size exceeds image dimensions");
+}
+
+struct Clamped {
+  int block, overlap;
+};
+
+// clamped_partition (multilevel.hpp:146-150)
+Clamped clamp_partition(int w, int h, int block, int overlap) {
+  const int be = std::min(block, std::min(w, h));
+  const int oe = std::max(0, std::min(overlap, be - 1));
+  validate_partition(w, h, be, oe);
+  return {be, oe};
+}
+
+double psnr_from_sq(const std::vector<double>& sq, size_t N) {
+  // psnr (metrics.hpp:51-57): mean of per-channel MSE, +inf when identical
+  double mean = 0.0;
+  for (double s : sq) mean += s / static_cast<double>(N);
+  mean /= static_cast<double>(sq.size());
+  if (mean == 0.0) return std::numeric_limits<double>::infinity();
+  return 10.0 * std::log10(255.0 * 255.0 / mean);
+}
+
+// ---------------------------------------------------------------- the solve
+struct Trace {
+  si_trace_fn fn;
+  void* user;
+  Clock::time_point t0;
+};
+
+struct LevelOutcome {
+  int iterations = 0;
+  double final_rel = 0.0;
+  bool converged = false;
+};
+
+template <typename T>
+struct LevelView {
+  int w, h;
+  const uint8_t* mask;
+  const T* b;
+  T* u[2];
+  int cur;
+};
+
+// Per-channel sums -> joint norm with the reference's sqrt-then-square
+// (schwarz.hpp:290-295; the accumulate is an fma in the gcc build).
+double joint_norm(const double* sums, int C) {
+  double joint = 0.0;
+  for (int k = 0; k < C; ++k) {
+    const double nrm = std::sqrt(sums[k]);
+    joint = std::fma(nrm, nrm, joint);
+  }
+  return std::sqrt(joint);
+}
+
+// run_schwarz_level (schwarz.hpp:266-323) on device buffers.  When
+// r0_slot_pending, the r0 reduction was already launched into host_red[C..2C)
+// and is read at the first synchronisation.
+template <typename T>
+LevelOutcome run_level(Ctx& x, LevelView<T>& L, int C, int block, int overlap, double* r0,
+                       bool r0_pending, double tol, int flavour, const si_options& o,
+                       bool b_known_only, bool sink, const Trace& tr, const double* d_ref,
+                       si_report* rep) {
+  LevelOutcome out;
+  const size_t N = static_cast<size_t>(L.w) * L.h;
+  double* d_out = x.c.red_out.as<double>();
+  unsigned long long* d_cnt = x.c.counters.as<unsigned long long>();
+  bool local_checked = false;
+  const Axis ax = Axis::make(L.w, block, overlap), ay = Axis::make(L.h, block, overlap);
+  const long long nblocks = static_cast<long long>(ax.count) * ay.count;
+  for (int outer = 0;; ++outer) {
+    launch_residual<T>(x, L.mask, L.u[L.cur], L.b, L.w, L.h, C, 0, d_out);
+    if (sink && d_ref) launch_sq_error<T>(x, L.u[L.cur], d_ref, N, C, d_out + 2 * C);
+    CK(cudaMemcpyAsync(x.c.host_red, d_out, sizeof(double) * 3 * C, cudaMemcpyDeviceToHost, x.s));
+    sync(x);
+    if (r0_pending) {
+      *r0 = joint_norm(x.c.host_red + C, C);
+      r0_pending = false;
+    }
+    const double rel = *r0 > 0.0 ? joint_norm(x.c.host_red, C) / *r0 : 0.0;
+    if (sink && tr.fn) {
+      double q = std::numeric_limits<double>::quiet_NaN();
+      if (d_ref) q = psnr_from_sq(std::vector<double>(x.c.host_red + 2 * C, x.c.host_red + 3 * C), N);
+      tr.fn(outer, ms_since(tr.t0), rel, q, tr.user);
+    }
+    out.iterations = outer;
+    out.final_rel = rel;
+    if (rel <= tol) {
+      out.converged = true;
+      break;
+    }
+    if (outer >= o.max_outer_iterations) break;
+    if (!local_checked) {
+      validate_local(o);
+      local_checked = true;
+    }
+    const LocalCfg lc{o.local_tolerance, o.local_max_iterations, o.local_check_interval};
+    launch_sweep<T>(x, L.mask, L.b, L.u[L.cur], L.u[L.cur ^ 1], L.w, L.h, C, block, overlap,
+                    flavour, o.alpha, lc, b_known_only, d_cnt);
+    L.cur ^= 1;
+    rep->local_solves += nblocks * C;
+  }
+  return out;
+}
+
+template <typename T>
+void launch_r0(Ctx& x, const LevelView<T>& L, int C, int normalizer) {
+  // canonical_r0 (schwarz.hpp:333-345): residual of u0 = b, or ||b||.
+  double* d_out = x.c.red_out.as<double>();
+  launch_residual<T>(x, L.mask, L.b, L.b, L.w, L.h, C, normalizer == 1 ? 1 : 0, d_out + C);
+}
+
+void begin_counters(Ctx& x) {
+  x.c.counters.ensure(sizeof(unsigned long long) * 4);
+  CK(cudaMemsetAsync(x.c.counters.ptr, 0, sizeof(unsigned long long) * 4, x.s));
+}
+
+void end_counters(Ctx& x, si_report* rep) {
+  CK(cudaMemcpyAsync(x.c.host_cnt, x.c.counters.ptr, sizeof(unsigned long long) * 2,
+                     cudaMemcpyDeviceToHost, x.s));
+  sync(x);
+  rep->local_failures += static_cast<long long>(x.c.host_cnt[0]);
+  rep->local_cg_iterations += static_cast<long long>(x.c.host_cnt[1]);
+}
+
+void prepare_red(Ctx& x, int C) {
+  x.c.red_out.ensure(sizeof(double) * 4 * C);
+  if (!x.c.host_red || C > 64) {
+    // pinned staging sized for up to 64 channels
+  }
+  if (C > 64) fail(SI_ERR_UNSUPPORTED, "more than 64 channels");
+}
+
+// multilevel_solve (multilevel.hpp:239-310) for the Schwarz level solvers.
+// fixed_block >= 0 selects solve_schwarz's explicit, unclamped partition
+// (schwarz.hpp:349-389) instead of clamped_partition per level.
+template <typename T>
+void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
+                       const uint8_t* d_mask, int w, int h, int C, const si_options& o,
+                       const double* d_ref, double* d_out, si_report* rep, const Trace& tr,
+                       int fixed_block = -1, int fixed_overlap = 0) {
+  prepare_red(x, C);
+  check_arg(levels_req >= 1, "build_pyramid: levels must be >= 1");
+  // Level geometry: halve (ceil) until the requested depth or a level that
+  // cannot be halved again (multilevel.hpp:90-93).
+  std::vector<int> lw{w}, lh{h};
+  while (static_cast<int>(lw.size()) < levels_req && static_cast<int>(lw.size()) < SI_MAX_LEVELS) {
+    if (lw.back() < 2 || lh.back() < 2) break;
+    lw.push_back((lw.back() + 1) / 2);
+    lh.push_back((lh.back() + 1) / 2);
+  }
+  const int depth = static_cast<int>(lw.size());
+  rep->depth = depth;
+  if (static_cast<int>(x.c.levels.size()) < depth) x.c.levels.resize(depth);
+  std::vector<LevelView<T>> L(depth);
+  for (int l = 0; l < depth; ++l) {
+    const size_t n = static_cast<size_t>(lw[l]) * lh[l];
+    auto& lb = x.c.levels[l];
+    lb.mask.ensure(n);
+    lb.b.ensure(n * C * sizeof(T));
+    lb.u0.ensure(n * C * sizeof(T));
+    lb.u1.ensure(n * C * sizeof(T));
+    L[l] = {lw[l], lh[l], l == 0 ? d_mask : lb.mask.as<uint8_t>(), lb.b.as<T>(),
+            {lb.u0.as<T>(), lb.u1.as<T>()}, 0};
+  }
+  // K5 ingest: level-0 values, known count for build_rhs's check.
+  const size_t n0 = static_cast<size_t>(w) * h;
+  {
+    Timed t(x, K_INGEST, static_cast<double>(n0) * (C * (8.0 + sizeof(T)) + 1.0));
+    ingest_kernel<T><<<grid_for(n0, 256, 148 * 16), 256, 0, x.s>>>(
+        d_f, d_mask, n0, C, x.c.levels[0].b.as<T>(), x.c.counters.as<unsigned long long>() + 2);
+    CK(cudaGetLastError());
+  }
+  // K3: restrict level by level.
+  for (int l = 1; l < depth; ++l) {
+    const size_t cn = static_cast<size_t>(lw[l]) * lh[l];
+    Timed t(x, K_RESTRICT, static_cast<double>(cn) * 4.0 * (C * sizeof(T) + 1) + cn * (C * sizeof(T) + 1));
+    restrict_kernel<T><<<grid_for(cn, 256, 148 * 16), 256, 0, x.s>>>(
+        L[l - 1].mask, L[l - 1].b, lw[l - 1], lh[l - 1], C, o.averaging,
+        x.c.levels[l].mask.as<uint8_t>(), x.c.levels[l].b.as<T>());
+    CK(cudaGetLastError());
+  }
+  bool known_checked = false;
+  for (int level = depth - 1; level >= 0; --level) {
+    LevelView<T>& V = L[level];
+    const size_t n = static_cast<size_t>(V.w) * V.h;
+    if (level == depth - 1) {
+      // canonical start u0 = b on the coarsest level (multilevel.hpp:267-273)
+      CK(cudaMemcpyAsync(V.u[0], V.b, n * C * sizeof(T), cudaMemcpyDeviceToDevice, x.s));
+      V.cur = 0;
+    }
+    const bool finest = level == 0;
+    const double tol = finest ? o.tolerance : o.coarse_tolerance;
+    Clamped cp{fixed_block, fixed_overlap};
+    if (fixed_block < 0) cp = clamp_partition(V.w, V.h, o.block_size, o.overlap);
+    if (flavour == SI_FLAVOUR_ORAS)
+      check_arg(std::isfinite(o.alpha), "run_schwarz_level: alpha must be finite");
+    if (!known_checked) {
+      // build_rhs rejects an empty mask (operators.hpp:83): read the count
+      // taken by the ingest kernel.
+      CK(cudaMemcpyAsync(x.c.host_cnt + 2, x.c.counters.as<unsigned long long>() + 2,
+                         sizeof(unsigned long long), cudaMemcpyDeviceToHost, x.s));
+      sync(x);
+      check_arg(x.c.host_cnt[2] > 0, "build_rhs: mask has no known pixels");
+      known_checked = true;
+    }
+    double r0 = 0.0;
+    launch_r0<T>(x, V, C, o.normalizer);
+    const LevelOutcome oc = run_level<T>(x, V, C, cp.block, cp.overlap, &r0, true, tol, flavour, o,
+                                         true, finest, tr, finest ? d_ref : nullptr, rep);
+    rep->level_iterations[level] = oc.iterations;
+    rep->level_final_rel[level] = oc.final_rel;
+    rep->level_converged[level] = oc.converged;
+    if (finest) {
+      rep->iterations = oc.iterations;
+      rep->final_relative_residual = oc.final_rel;
+      rep->converged = oc.converged;
+    } else {
+      // K4: prolongate + snap into the next finer level's u.
+      LevelView<T>& F = L[level - 1];
+      const size_t fn = static_cast<size_t>(F.w) * F.h;
+      Timed t(x, K_PROLONG, static_cast<double>(fn) * (2.0 * C * sizeof(T) + 1.0) + n * C * sizeof(T));
+      prolong_snap_kernel<T><<<grid_for(fn, 256, 148 * 16), 256, 0, x.s>>>(
+          V.u[V.cur], V.w, V.h, F.w, F.h, C, F.mask, F.b, F.u[0]);
+      CK(cudaGetLastError());
+      F.cur = 0;
+    }
+  }
+  // Diagnostics as multilevel_solve writes them (multilevel.hpp:284-293).
+  bool coarse_capped = false;
+  for (int l = 1; l < depth; ++l) coarse_capped |= !rep->level_converged[l];
+  if (!rep->converged)
+    std::snprintf(rep->diagnostic, sizeof rep->diagnostic, "%s",
+                  fixed_block >= 0 ? "schwarz: outer iteration cap reached"
+                                   : "multilevel: finest level did not converge");
+  else if (coarse_capped)
+    std::snprintf(rep->diagnostic, sizeof rep->diagnostic, "%s",
+                  "multilevel: a coarse level hit its iteration cap");
+  // Export the finest u (T -> double).
+  {
+    Timed t(x, K_INGEST, static_cast<double>(n0) * C * (8.0 + sizeof(T)));
+    convert_kernel<T, double><<<grid_for(n0 * C, 256, 148 * 16), 256, 0, x.s>>>(
+        L[0].u[L[0].cur], d_out, n0 * C);
+    CK(cudaGetLastError());
+  }
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+#include <functional>
+
+namespace {
+si_status guard(const std::function<void()>& fn) {
+  try {
+    fn();
+    return SI_OK;
+  } catch (const Failure& f) {
+    g_last_error = f.message;
+    return f.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host out of memory";
+    return SI_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SI_ERR_CUDA;
+  }
+}
+
+void set_device(si_ctx* c) { CK(cudaSetDevice(c->device)); }
+
+cudaStream_t pick_stream(si_ctx* c, void* stream) {
+  return stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+}
+
+void clear_report(si_report* rep) {
+  std::memset(rep, 0, sizeof(*rep));
+}
+
+int levels_for(int method, const si_options& o) {
+  return (method == SI_METHOD_MLORAS || method == SI_METHOD_MLCG) ? o.levels : 1;
+}
+
+int flavour_for(int method) { return method == SI_METHOD_RAS ? SI_FLAVOUR_RAS : SI_FLAVOUR_ORAS; }
+
+void check_method(int method) {
+  check_arg(method >= SI_METHOD_CG && method <= SI_METHOD_MLORAS,
+            "unknown method (expected cg, mlcg, ras, oras or mloras)");
+  if (method == SI_METHOD_CG || method == SI_METHOD_MLCG)
+    fail(SI_ERR_UNSUPPORTED, "method cg/mlcg is not provided by the B200 build (ORAS path only)");
+}
+
+void check_dims(int w, int h, int c) {
+  check_arg(w > 0 && h > 0 && c > 0, "ImageBuffer: dimensions must be positive");
+}
+
+void run_device(si_ctx* ctx, int method, const double* d_f, const uint8_t* d_mask, int w, int h,
+                int c, const si_options& o, const double* d_ref, double* d_out, si_report* rep,
+                si_trace_fn trace, void* user, cudaStream_t s, Clock::time_point t0) {
+  check_method(method);
+  check_dims(w, h, c);
+  validate_options_common(o);
+  Ctx x{*ctx, s};
+  begin_counters(x);
+  Trace tr{trace, user, t0};
+  if (o.precision == SI_PRECISION_FP32)
+    multilevel_device<float>(x, levels_for(method, o), flavour_for(method), d_f, d_mask, w, h, c,
+                             o, d_ref, d_out, rep, tr);
+  else
+    multilevel_device<double>(x, levels_for(method, o), flavour_for(method), d_f, d_mask, w, h, c,
+                              o, d_ref, d_out, rep, tr);
+  end_counters(x, rep);
+}
+
+}  // namespace
+
+extern "C" {
+
+int si_abi_version(void) { return SI_ABI_VERSION; }
+
+const char* si_last_error(void) { return g_last_error.c_str(); }
+
+const char* si_status_string(si_status s) {
+  switch (s) {
+    case SI_OK: return "ok";
+    case SI_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case SI_ERR_CUDA: return "cuda error";
+    case SI_ERR_OOM: return "out of memory";
+    case SI_ERR_UNSUPPORTED: return "unsupported";
+    case SI_ERR_NO_DEVICE: return "no device";
+  }
+  return "unknown";
+}
+
+void si_default_options(si_options* o) {
+  o->tolerance = 1e-3;
+  o->levels = 3;
+  o->block_size = 32;
+  o->overlap = 6;
+  o->alpha = 0.25;
+  o->coarse_tolerance = 1e-2;
+  o->averaging = SI_AVERAGING_KNOWN_ONLY;
+  o->local_tolerance = 1e-2;
+  o->local_max_iterations = 30;
+  o->local_check_interval = 30;
+  o->max_outer_iterations = 1000;
+  o->cg_max_iterations = 100000;
+  o->cg_check_interval = 4;
+  o->normalizer = SI_NORMALIZER_INITIAL_GUESS;
+  o->precision = SI_PRECISION_FP64;
+}
+
+si_status si_validate_options(int method, const si_options* opt) {
+  return guard([&] {
+    check_arg(opt != nullptr, "options must not be null");
+    check_method(method);
+    validate_options_common(*opt);
+    check_arg(levels_for(method, *opt) >= 1, "build_pyramid: levels must be >= 1");
+    check_arg(opt->block_size > 0, "partition_domain: block_size must be positive");
+    if (method != SI_METHOD_RAS)
+      check_arg(std::isfinite(opt->alpha), "run_schwarz_level: alpha must be finite");
+    validate_local(*opt);
+  });
+}
+
+si_status si_create(int device, si_ctx** out) {
+  return guard([&] {
+    check_arg(out != nullptr, "si_create: out must not be null");
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      fail(SI_ERR_NO_DEVICE, "no CUDA device available");
+    }
+    check_arg(device >= 0 && device < n, "si_create: device index out of range");
+    auto* c = new si_ctx();
+    c->device = device;
+    try {
+      CK(cudaSetDevice(device));
+      CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+      CK(cudaMallocHost(&c->host_red, sizeof(double) * 256));
+      CK(cudaMallocHost(&c->host_cnt, sizeof(unsigned long long) * 8));
+      if (const char* e = std::getenv("SI_SWEEP_WARPS64")) c->sweep_nw64 = std::atoi(e);
+      if (const char* e = std::getenv("SI_SWEEP_WARPS32")) c->sweep_nw32 = std::atoi(e);
+    } catch (...) {
+      si_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void si_destroy(si_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+  for (auto& l : c->levels) {
+    l.mask.release();
+    l.b.release();
+    l.u0.release();
+    l.u1.release();
+  }
+  for (DevBuf* b : {&c->in_f, &c->in_mask, &c->in_ref, &c->out_img, &c->aux, &c->red_partials,
+                    &c->red_out, &c->counters, &c->ticket})
+    b->release();
+  for (auto& p : c->pending) {
+    cudaEventDestroy(p.start);
+    cudaEventDestroy(p.stop);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->host_red) cudaFreeHost(c->host_red);
+  if (c->host_cnt) cudaFreeHost(c->host_cnt);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+}
+
+si_status si_trim(si_ctx* c) {
+  return guard([&] {
+    check_arg(c != nullptr, "null context");
+    set_device(c);
+    CK(cudaStreamSynchronize(c->own_stream));
+    for (auto& l : c->levels) {
+      l.mask.release();
+      l.b.release();
+      l.u0.release();
+      l.u1.release();
+    }
+    for (DevBuf* b : {&c->in_f, &c->in_mask, &c->in_ref, &c->out_img, &c->aux}) b->release();
+  });
+}
+
+si_status si_run_method_device(si_ctx* ctx, int method, const double* d_f, const uint8_t* d_mask,
+                               int w, int h, int c, const si_options* opt,
+                               const double* d_reference, double* d_out, si_report* report,
+                               si_trace_fn trace, void* user, void* stream) {
+  si_report local;
+  si_report* rep = report ? report : &local;
+  clear_report(rep);
+  const auto t0 = Clock::now();
+  si_status st = guard([&] {
+    check_arg(ctx && d_f && d_mask && d_out, "null argument");
+    si_options o;
+    if (opt) o = *opt; else si_default_options(&o);
+    set_device(ctx);
+    run_device(ctx, method, d_f, d_mask, w, h, c, o, d_reference, d_out, rep, trace, user,
+               pick_stream(ctx, stream), t0);
+  });
+  rep->elapsed_ms = ms_since(t0);
+  return st;
+}
+
+si_status si_run_method(si_ctx* ctx, int method, const double* f, const uint8_t* mask, int w,
+                        int h, int c, const si_options* opt, const double* reference, double* out,
+                        si_report* report, si_trace_fn trace, void* user) {
+  si_report local;
+  si_report* rep = report ? report : &local;
+  clear_report(rep);
+  const auto t0 = Clock::now();
+  si_status st = guard([&] {
+    check_arg(ctx && f && mask && out, "null argument");
+    check_dims(w, h, c);
+    si_options o;
+    if (opt) o = *opt; else si_default_options(&o);
+    set_device(ctx);
+    const size_t n = static_cast<size_t>(w) * h;
+    Ctx x{*ctx, ctx->own_stream};
+    ctx->in_f.ensure(n * c * sizeof(double));
+    ctx->in_mask.ensure(n);
+    ctx->out_img.ensure(n * c * sizeof(double));
+    CK(cudaMemcpyAsync(ctx->in_f.ptr, f, n * c * sizeof(double), cudaMemcpyHostToDevice, x.s));
+    CK(cudaMemcpyAsync(ctx->in_mask.ptr, mask, n, cudaMemcpyHostToDevice, x.s));
+    const double* d_ref = nullptr;
+    if (reference) {
+      ctx->in_ref.ensure(n * c * sizeof(double));
+      CK(cudaMemcpyAsync(ctx->in_ref.ptr, reference, n * c * sizeof(double),
+                         cudaMemcpyHostToDevice, x.s));
+      d_ref = ctx->in_ref.as<double>();
+    }
+    run_device(ctx, method, ctx->in_f.as<double>(), ctx->in_mask.as<uint8_t>(), w, h, c, o, d_ref,
+               ctx->out_img.as<double>(), rep, trace, user, x.s, t0);
+    CK(cudaMemcpyAsync(out, ctx->out_img.ptr, n * c * sizeof(double), cudaMemcpyDeviceToHost, x.s));
+    sync(x);
+  });
+  rep->elapsed_ms = ms_since(t0);
+  return st;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- building blocks
+namespace {
+
+// LocalOperator::apply on one block (schwarz.hpp:57-75) with the diagonal of
+// build_local_operator (schwarz.hpp:115-130); one thread per block cell.
+__global__ void local_operator_kernel(const uint8_t* mask, int W, int H, int x0, int y0, int B,
+                                      int ras, double am1, const double* v, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B * B) return;
+  const int ly = i / B, lx = i % B;
+  const int gx = x0 + lx, gy = y0 + ly;
+  if (mask[static_cast<size_t>(gy) * W + gx]) {
+    out[i] = v[i];
+    return;
+  }
+  double acc = robin_diag<double>(gx, gy, lx, ly, B, W, H, am1, ras) * v[i];
+  if (lx > 0) acc -= v[i - 1];
+  if (lx + 1 < B) acc -= v[i + 1];
+  if (ly > 0) acc -= v[i - B];
+  if (ly + 1 < B) acc -= v[i + B];
+  out[i] = acc;
+}
+
+template <typename T>
+T* upload(Ctx& x, DevBuf& buf, const T* host, size_t count) {
+  buf.ensure(count * sizeof(T) + 16);
+  CK(cudaMemcpyAsync(buf.ptr, host, count * sizeof(T), cudaMemcpyHostToDevice, x.s));
+  return buf.as<T>();
+}
+
+template <typename T>
+void download(Ctx& x, T* host, const void* dev, size_t count) {
+  CK(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, x.s));
+  sync(x);
+}
+
+si_options opts_or_default(const si_options* opt) {
+  si_options o;
+  if (opt) o = *opt; else si_default_options(&o);
+  return o;
+}
+
+}  // namespace
+
+extern "C" {
+
+si_status si_solve_schwarz(si_ctx* ctx, const double* f, const uint8_t* mask, int w, int h, int c,
+                           int block_size, int overlap, int flavour, const si_options* opt,
+                           const double* reference, double* out, si_report* report,
+                           si_trace_fn trace, void* user) {
+  si_report local;
+  si_report* rep = report ? report : &local;
+  clear_report(rep);
+  const auto t0 = Clock::now();
+  si_status st = guard([&] {
+    check_arg(ctx && f && mask && out, "null argument");
+    check_dims(w, h, c);
+    const si_options o = opts_or_default(opt);
+    check_arg(o.tolerance > 0.0, "solve_schwarz: tolerance must be positive");
+    check_arg(flavour == SI_FLAVOUR_RAS || flavour == SI_FLAVOUR_ORAS, "unknown flavour");
+    validate_partition(w, h, block_size, overlap);
+    si_options oo = o;
+    oo.coarse_tolerance = 1.0;  // single level: unused
+    validate_options_common(oo);
+    set_device(ctx);
+    Ctx x{*ctx, ctx->own_stream};
+    const size_t n = static_cast<size_t>(w) * h;
+    const double* d_f = upload(x, ctx->in_f, f, n * c);
+    const uint8_t* d_m = upload(x, ctx->in_mask, mask, n);
+    const double* d_ref = reference ? upload(x, ctx->in_ref, reference, n * c) : nullptr;
+    ctx->out_img.ensure(n * c * sizeof(double));
+    begin_counters(x);
+    Trace tr{trace, user, t0};
+    if (oo.precision == SI_PRECISION_FP32)
+      multilevel_device<float>(x, 1, flavour, d_f, d_m, w, h, c, oo, d_ref,
+                               ctx->out_img.as<double>(), rep, tr, block_size, overlap);
+    else
+      multilevel_device<double>(x, 1, flavour, d_f, d_m, w, h, c, oo, d_ref,
+                                ctx->out_img.as<double>(), rep, tr, block_size, overlap);
+    end_counters(x, rep);
+    download(x, out, ctx->out_img.ptr, n * c);
+  });
+  rep->elapsed_ms = ms_since(t0);
+  return st;
+}
+
+si_status si_run_schwarz_level(si_ctx* ctx, const uint8_t* mask, int w, int h, int c,
+                               const double* b, double* u, int block_size, int overlap,
+                               double r0_norm, double tolerance, int flavour,
+                               const si_options* opt, si_report* report, si_trace_fn trace,
+                               void* user) {
+  si_report local;
+  si_report* rep = report ? report : &local;
+  clear_report(rep);
+  const auto t0 = Clock::now();
+  si_status st = guard([&] {
+    check_arg(ctx && mask && b && u, "null argument");
+    check_arg(c > 0, "run_schwarz_level: channel count mismatch");
+    validate_partition(w, h, block_size, overlap);
+    check_arg(flavour == SI_FLAVOUR_RAS || std::isfinite(opt ? opt->alpha : 0.25),
+              "run_schwarz_level: alpha must be finite");
+    const si_options o = opts_or_default(opt);
+    set_device(ctx);
+    Ctx x{*ctx, ctx->own_stream};
+    prepare_red(x, c);
+    const size_t n = static_cast<size_t>(w) * h;
+    if (ctx->levels.empty()) ctx->levels.resize(1);
+    auto& lb = ctx->levels[0];
+    lb.u0.ensure(n * c * sizeof(double));
+    lb.u1.ensure(n * c * sizeof(double));
+    const uint8_t* d_m = upload(x, ctx->in_mask, mask, n);
+    const double* d_b = upload(x, ctx->in_f, b, n * c);
+    CK(cudaMemcpyAsync(lb.u0.ptr, u, n * c * sizeof(double), cudaMemcpyHostToDevice, x.s));
+    LevelView<double> V{w, h, d_m, d_b, {lb.u0.as<double>(), lb.u1.as<double>()}, 0};
+    begin_counters(x);
+    Trace tr{trace, user, t0};
+    double r0 = r0_norm;
+    const LevelOutcome oc = run_level<double>(x, V, c, block_size, overlap, &r0, false, tolerance,
+                                              flavour, o, false, true, tr, nullptr, rep);
+    end_counters(x, rep);
+    download(x, u, V.u[V.cur], n * c);
+    rep->depth = 1;
+    rep->iterations = rep->level_iterations[0] = oc.iterations;
+    rep->final_relative_residual = rep->level_final_rel[0] = oc.final_rel;
+    rep->converged = rep->level_converged[0] = oc.converged;
+  });
+  rep->elapsed_ms = ms_since(t0);
+  return st;
+}
+
+si_status si_canonical_r0(si_ctx* ctx, const uint8_t* mask, int w, int h, int c, const double* b,
+                          int normalizer, double* r0_norm) {
+  return guard([&] {
+    check_arg(ctx && mask && b && r0_norm, "null argument");
+    check_dims(w, h, c);
+    set_device(ctx);
+    Ctx x{*ctx, ctx->own_stream};
+    prepare_red(x, c);
+    const size_t n = static_cast<size_t>(w) * h;
+    const uint8_t* d_m = upload(x, ctx->in_mask, mask, n);
+    const double* d_b = upload(x, ctx->in_f, b, n * c);
+    launch_residual<double>(x, d_m, d_b, d_b, w, h, c, normalizer == 1 ? 1 : 0,
+                            ctx->red_out.as<double>());
+    download(x, ctx->host_red, ctx->red_out.ptr, c);
+    *r0_norm = joint_norm(ctx->host_red, c);
+  });
+}
+
+si_status si_schwarz_sweep(si_ctx* ctx, const uint8_t* mask, int w, int h, int c, const double* b,
+                           const double* u, int block_size, int overlap, int flavour,
+                           const si_options* opt, double* u_new, long long* failures,
+                           long long* cg_iterations) {
+  return guard([&] {
+    check_arg(ctx && mask && b && u && u_new, "null argument");
+    check_dims(w, h, c);
+    validate_partition(w, h, block_size, overlap);
+    const si_options o = opts_or_default(opt);
+    validate_local(o);
+    set_device(ctx);
+    Ctx x{*ctx, ctx->own_stream};
+    const size_t n = static_cast<size_t>(w) * h;
+    if (ctx->levels.empty()) ctx->levels.resize(1);
+    auto& lb = ctx->levels[0];
+    lb.u0.ensure(n * c * sizeof(double));
+    lb.u1.ensure(n * c * sizeof(double));
+    const uint8_t* d_m = upload(x, ctx->in_mask, mask, n);
+    const double* d_b = upload(x, ctx->in_f, b, n * c);
+    CK(cudaMemcpyAsync(lb.u0.ptr, u, n * c * sizeof(double), cudaMemcpyHostToDevice, x.s));
+    begin_counters(x);
+    const LocalCfg lc{o.local_tolerance, o.local_max_iterations, o.local_check_interval};
+    launch_sweep<double>(x, d_m, d_b, lb.u0.as<double>(), lb.u1.as<double>(), w, h, c, block_size,
+                         overlap, flavour, o.alpha, lc, false,
+                         ctx->counters.as<unsigned long long>());
+    download(x, u_new, lb.u1.ptr, n * c);
+    download(x, ctx->host_cnt, ctx->counters.ptr, 2);
+    if (failures) *failures = static_cast<long long>(ctx->host_cnt[0]);
+    if (cg_iterations) *cg_iterations = static_cast<long long>(ctx->host_cnt[1]);
+  });
+}
+
+si_status si_residual_sumsq(si_ctx* ctx, const uint8_t* mask, int w, int h, int c,
+                            const double* u, const double* b, double* sumsq) {
+  return guard([&] {
+    check_arg(ctx && mask && u && b && sumsq, "null argument");
+    check_dims(w, h, c);
+    set_device(ctx);
+    Ctx x{*ctx, ctx->own_stream};
+    prepare_red(x, c);
+    const size_t n = static_cast<size_t>(w) * h;
+    const uint8_t* d_m = upload(x, ctx->in_mask, mask, n);
+    const double* d_b = upload(x, ctx->in_f, b, n * c);
+    const double* d_u = upload(x, ctx->aux, u, n * c);
+    launch_residual<double>(x, d_m, d_u, d_b, w, h, c, 0, ctx->red_out.as<double>());
+    download(x, sumsq, ctx->red_out.ptr, c);
+  });
+}
+
+si_status si_restrict_level(si_ctx* ctx, const uint8_t* mask, const double* values, int w, int h,
+                            int c, int averaging, uint8_t* coarse_mask, double* coarse_values) {
+  return guard([&] {
+    check_arg(ctx && mask && values && coarse_mask && coarse_values, "null argument");
+    check_dims(w, h, c);
+    check_arg(w >= 2 && h >= 2, "restrict_level: fine grid must be at least 2x2");
+    set_device(ctx);
+    Ctx x{*ctx, ctx->own_stream};
+    const size_t n = static_cast<size_t>(w) * h;
+    const int cw = (w + 1) / 2, ch = (h + 1) / 2;
+    const size_t cn = static_cast<size_t>(cw) * ch;
+    const uint8_t* d_m = upload(x, ctx->in_mask, mask, n);
+    const double* d_v = upload(x, ctx->in_f, values, n * c);
+    ctx->out_img.ensure(cn * c * sizeof(double));
+    ctx->aux.ensure(cn + 16);
+    restrict_kernel<double><<<grid_for(cn, 256, 148 * 16), 256, 0, x.s>>>(
+        d_m, d_v, w, h, c, averaging, ctx->aux.as<uint8_t>(), ctx->out_img.as<double>());
+    CK(cudaGetLastError());
+    download(x, coarse_mask, ctx->aux.ptr, cn);
+    download(x, coarse_values, ctx->out_img.ptr, cn * c);
+  });
+}
+
+si_status si_prolongate(si_ctx* ctx, const double* coarse, int cw, int ch, int fw, int fh,
+                        double* fine) {
+  return guard([&] {
+    check_arg(ctx && coarse && fine, "null argument");
+    check_arg(cw == (fw + 1) / 2 && ch == (fh + 1) / 2,
+              "prolongate: coarse grid is not the dyadic parent of the fine grid");
+    check_arg(cw > 0 && ch > 0, "prolongate: coarse vector length mismatch");
+    set_device(ctx);
+    Ctx x{*ctx, ctx->own_stream};
+    const size_t fn = static_cast<size_t>(fw) * fh;
+    const double* d_c = upload(x, ctx->in_f, coarse, static_cast<size_t>(cw) * ch);
+    ctx->out_img.ensure(fn * sizeof(double));
+    prolong_snap_kernel<double><<<grid_for(fn, 256, 148 * 16), 256, 0, x.s>>>(
+        d_c, cw, ch, fw, fh, 1, nullptr, nullptr, ctx->out_img.as<double>());
+    CK(cudaGetLastError());
+    download(x, fine, ctx->out_img.ptr, fn);
+  });
+}
+
+si_status si_local_operator_apply(si_ctx* ctx, const uint8_t* mask, int w, int h, int block_size,
+                                  int overlap, int index, int flavour, double alpha,
+                                  const double* v, double* out) {
+  return guard([&] {
+    check_arg(ctx && mask && v && out, "null argument");
+    validate_partition(w, h, block_size, overlap);
+    const Axis ax = Axis::make(w, block_size, overlap), ay = Axis::make(h, block_size, overlap);
+    check_arg(index >= 0 && index < ax.count * ay.count,
+              "build_local_operator: subdomain index out of range");
+    set_device(ctx);
+    Ctx x{*ctx, ctx->own_stream};
+    const int B = block_size;
+    const size_t cells = static_cast<size_t>(B) * B;
+    const uint8_t* d_m = upload(x, ctx->in_mask, mask, static_cast<size_t>(w) * h);
+    const double* d_v = upload(x, ctx->in_f, v, cells);
+    ctx->out_img.ensure(cells * sizeof(double));
+    const int bx = index % ax.count, by = index / ax.count;
+    local_operator_kernel<<<grid_for(cells, 256, 1 << 20), 256, 0, x.s>>>(
+        d_m, w, h, ax.anchor(bx), ay.anchor(by), B, flavour == SI_FLAVOUR_RAS, alpha - 1.0, d_v,
+        ctx->out_img.as<double>());
+    CK(cudaGetLastError());
+    download(x, out, ctx->out_img.ptr, cells);
+  });
+}
+
+si_status si_partition_domain(int w, int h, int block_size, int overlap, int* blocks_x,
+                              int* blocks_y, int* rects, int rects_capacity) {
+  return guard([&] {
+    validate_partition(w, h, block_size, overlap);
+    const Axis ax = Axis::make(w, block_size, overlap), ay = Axis::make(h, block_size, overlap);
+    if (blocks_x) *blocks_x = ax.count;
+    if (blocks_y) *blocks_y = ay.count;
+    if (!rects) return;
+    int k = 0;
+    for (int by = 0; by < ay.count; ++by)
+      for (int bx = 0; bx < ax.count; ++bx, ++k) {
+        if (k >= rects_capacity) return;
+        int* r = rects + 8 * k;
+        r[0] = ax.anchor(bx);
+        r[1] = ay.anchor(by);
+        r[2] = block_size;
+        r[3] = block_size;
+        r[4] = ax.owned_begin(bx);
+        r[5] = ay.owned_begin(by);
+        r[6] = ax.owned_end(bx);
+        r[7] = ay.owned_end(by);
+      }
+  });
+}
+
+si_status si_psnr(const double* u, const double* f, int w, int h, int c, double* psnr_db) {
+  return guard([&] {
+    check_arg(u && f && psnr_db, "null argument");
+    check_dims(w, h, c);
+    const size_t n = static_cast<size_t>(w) * h;
+    std::vector<double> mse(c);
+    for (int k = 0; k < c; ++k) {
+      double acc = 0.0;
+      for (size_t i = 0; i < n; ++i) {
+        const double d = 255.0 * (u[k * n + i] - f[k * n + i]);
+        acc += d * d;
+      }
+      mse[k] = acc;
+    }
+    *psnr_db = psnr_from_sq(mse, n);
+  });
+}
+
+si_status si_set_profiling(si_ctx* ctx, int enabled) {
+  return guard([&] {
+    check_arg(ctx != nullptr, "null context");
+    ctx->profiling = enabled != 0;
+  });
+}
+
+si_status si_get_kernel_stats(si_ctx* ctx, si_kernel_stats* out, int reset) {
+  return guard([&] {
+    check_arg(ctx && out, "null argument");
+    set_device(ctx);
+    if (!ctx->pending.empty()) resolve_events(*ctx);
+    *out = ctx->stats;
+    if (reset) ctx->stats = si_kernel_stats{};
+  });
+}
+
+si_status si_host_alloc(size_t bytes, void** ptr) {
+  return guard([&] {
+    check_arg(ptr != nullptr, "null argument");
+    CK(cudaMallocHost(ptr, bytes));
+  });
+}
+
+si_status si_host_free(void* ptr) {
+  return guard([&] { CK(cudaFreeHost(ptr)); });
+}
+
+}  // extern "C"

@@ -1,0 +1,291 @@
+"""End-to-end GPU parity of run_method / solve_schwarz / multilevel_solve.
+
+Bar (stated per assertion):
+  fp64: equal outer-iteration counts on every level; every trace row within
+        1e-9 relative; output max-abs <= 1e-9 and MSE <= 1e-18.
+  fp32: equal counts; trace rows within 1e-4 relative; output max-abs <= 5e-4
+        and MSE <= 1e-10.
+Behavioural tests port schwarz_test.cpp / multilevel_test.cpp /
+acceptance_test.cpp properties to the GPU path.
+"""
+import numpy as np
+import pytest
+
+import paper_2110_03946_b200 as si
+from instances import C1, C2, config_instance, random_instance
+
+pytestmark = pytest.mark.gpu
+
+FP64 = dict(trace=1e-9, maxabs=1e-9, mse=1e-18)
+FP32 = dict(trace=1e-4, maxabs=5e-4, mse=1e-10)
+
+
+def compare(res, ora, bar, levels=True):
+    rep = res.report
+    if levels:
+        assert rep.level_iterations == ora.level_iterations, (rep.level_iterations,
+                                                              ora.level_iterations)
+    assert rep.iterations == ora.iterations
+    got = np.array([r.rel_residual for r in res.trace.rows])
+    assert got.shape == ora.trace.shape
+    rel = np.abs(got - ora.trace) / np.maximum(np.abs(ora.trace), 1e-300)
+    assert rel.max() <= bar["trace"], rel
+    diff = res.image.data - ora.image
+    assert np.abs(diff).max() <= bar["maxabs"]
+    assert np.mean(diff * diff) <= bar["mse"]
+    assert rep.converged == ora.converged
+
+
+def opts_dict(o: si.RunOptions, method):
+    return dict(tolerance=o.tolerance, levels=o.levels if si.is_multilevel(method) else 1,
+                block_size=o.block_size, overlap=o.overlap, alpha=o.alpha,
+                coarse_tolerance=o.coarse_tolerance, averaging=int(o.averaging),
+                local_tolerance=o.local.tolerance, local_max_iterations=o.local.max_iterations,
+                local_check_interval=o.local.residual_check_interval,
+                max_outer_iterations=o.max_outer_iterations, normalizer=int(o.normalizer),
+                flavour=0 if method == si.Method.Ras else 1)
+
+
+@pytest.mark.parametrize("precision,bar", [(si.Precision.FP64, FP64), (si.Precision.FP32, FP32)])
+def test_c1_mloras_matches_oracle(solver, oracle, precision, bar):
+    """BASELINE config 1: 256x256 grey, 5%, 2 levels (the CPU reference case)."""
+    f, m = config_instance(C1)
+    o = si.RunOptions(levels=2, precision=precision)
+    res = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    ora = oracle.oracle_solve(f.data, m.known, **opts_dict(o, si.Method.MultilevelOras))
+    assert ora.level_iterations == [2, 2]
+    compare(res, ora, bar)
+    assert res.report.local_cg_iterations == ora.local_cg_iterations or precision == si.Precision.FP32
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("precision,bar", [(si.Precision.FP64, FP64), (si.Precision.FP32, FP32)])
+def test_c2_mloras_matches_oracle(solver, oracle, precision, bar):
+    """BASELINE config 2: 1920x1080 RGB, 4%, 2 levels."""
+    f, m = config_instance(C2)
+    o = si.RunOptions(levels=2, precision=precision)
+    res = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    ora = oracle.oracle_solve(f.data, m.known, **opts_dict(o, si.Method.MultilevelOras))
+    assert ora.level_iterations == [1, 2]
+    compare(res, ora, bar)
+
+
+RANDOM_CASES = [
+    # (w, h, c, density, method, options)
+    (64, 64, 1, 0.1, si.Method.Oras, dict(tolerance=1e-6, block_size=16, overlap=4)),
+    (64, 48, 3, 0.07, si.Method.Oras, dict(tolerance=1e-6, block_size=16, overlap=4)),
+    (40, 40, 3, 0.1, si.Method.Ras, dict(tolerance=1e-6, block_size=16, overlap=4)),
+    (96, 96, 1, 0.05, si.Method.MultilevelOras, dict(block_size=16, overlap=3)),
+    (48, 48, 1, 0.08, si.Method.MultilevelOras, dict(tolerance=1e-8, block_size=16, overlap=4)),
+    (512, 512, 1, 0.05, si.Method.MultilevelOras, dict()),
+    (123, 77, 3, 0.04, si.Method.MultilevelOras, dict(levels=4)),
+    (9, 3, 1, 0.5, si.Method.MultilevelOras, dict(levels=5)),
+    (33, 17, 2, 0.3, si.Method.MultilevelOras, dict(averaging=si.CoarseAveraging.AllPixels,
+                                                    normalizer=si.ResidualNormalizer.RhsNorm)),
+    (300, 170, 3, 0.02, si.Method.MultilevelOras, dict(alpha=0.5, block_size=24, overlap=5)),
+]
+
+
+@pytest.mark.parametrize("w,h,c,d,method,kw", RANDOM_CASES)
+def test_random_instances_match_oracle(solver, oracle, w, h, c, d, method, kw):
+    f, m = random_instance(w, h, d, c, 1000 + w + h)
+    o = si.RunOptions(**kw)
+    res = solver.run_method(method, f, m, o)
+    ora = oracle.oracle_solve(f.data, m.known, **opts_dict(o, method))
+    compare(res, ora, FP64)
+
+
+def test_acceptance_oracle_equivalence_dense(solver):
+    """acceptance_test.cpp:39-67: mloras at tol 1e-8 agrees with a dense direct solve."""
+    rng = np.random.default_rng(101)
+    worst = 0.0
+    for inst in range(12):
+        w, h = rng.integers(8, 33, 2)
+        c = 1 if inst % 2 == 0 else 3
+        f = si.synthetic_test_image(int(w), int(h), c, 1000 + inst)
+        m = si.random_mask(int(w), int(h), float(rng.uniform(0.05, 0.5)), 77 + inst)
+        res = solver.run_method(si.Method.MultilevelOras, f, m,
+                                si.RunOptions(tolerance=1e-8, max_outer_iterations=5000))
+        assert res.report.converged
+        exact = dense_inpaint(m.known, f.data)
+        worst = max(worst, np.abs(res.image.data - exact).max())
+    assert worst <= 1e-6
+
+
+def dense_inpaint(mask, f):
+    """tests/support/oracle.hpp:15-51 with numpy in place of Eigen's LU."""
+    h, w = mask.shape
+    n = w * h
+    A = np.zeros((n, n))
+    for y in range(h):
+        for x in range(w):
+            i = y * w + x
+            if mask[y, x]:
+                A[i, i] = 1.0
+                continue
+            deg = 0
+            for xx, yy in ((x - 1, y), (x + 1, y), (x, y - 1), (x, y + 1)):
+                if 0 <= xx < w and 0 <= yy < h:
+                    A[i, yy * w + xx] -= 1.0
+                    deg += 1
+            A[i, i] = deg
+    out = np.empty_like(f)
+    for c in range(f.shape[0]):
+        b = np.where(mask.reshape(-1) != 0, f[c].reshape(-1), 0.0)
+        out[c] = np.linalg.solve(A, b).reshape(h, w)
+    return out
+
+
+# ---------------------------------------------------------------- behaviour
+def tight(flavour=si.SchwarzFlavour.Oras, tol=1e-6, alpha=0.25, **kw):
+    return si.SchwarzSolveOptions(si.SchwarzOptions(flavour, alpha, max_outer_iterations=5000,
+                                                    **kw), tol)
+
+
+def test_alpha_one_reproduces_ras_bitwise(solver):
+    """schwarz_test.cpp:109-122."""
+    f, m = random_instance(40, 40, 0.1, 3, 17)
+    part = si.partition_domain(40, 40, 16, 4)
+    ras = solver.solve_schwarz(f, m, part, tight(si.SchwarzFlavour.Ras))
+    oras = solver.solve_schwarz(f, m, part, tight(si.SchwarzFlavour.Oras, alpha=1.0))
+    assert ras.report.iterations == oras.report.iterations
+    assert np.array_equal(ras.image.data, oras.image.data)
+
+
+def test_single_block_exact_local_solve_one_iteration(solver):
+    """schwarz_test.cpp:124-133."""
+    f, m = random_instance(24, 24, 0.2, 1, 19)
+    part = si.partition_domain(24, 24, 24, 4)
+    assert part.size() == 1
+    opt = tight(tol=1e-8, local=si.SolverConfig(1e-12, 100000, 50))
+    res = solver.solve_schwarz(f, m, part, opt)
+    assert res.report.converged and res.report.iterations == 1
+
+
+def test_fixed_point_of_exact_solution(solver):
+    """schwarz_test.cpp:135-150: run_schwarz_level from the dense solution."""
+    f, m = random_instance(16, 16, 0.25, 1, 23)
+    u = dense_inpaint(m.known, f.data)
+    b = np.where(m.known[None] != 0, f.data, 0.0)
+    r0 = solver.canonical_r0(m, b)
+    part = si.partition_domain(16, 16, 8, 2)
+    rep = solver.run_schwarz_level(m, part, b, u, r0, 1e-8, si.SchwarzOptions())
+    assert rep.converged and rep.iterations == 0
+
+
+def test_partition_independence(solver):
+    """schwarz_test.cpp:152-166 / acceptance criterion 4."""
+    f, m = random_instance(64, 64, 0.08, 1, 29)
+    a = solver.solve_schwarz(f, m, si.partition_domain(64, 64, 16, 4), tight(tol=1e-8))
+    b = solver.solve_schwarz(f, m, si.partition_domain(64, 64, 32, 6), tight(tol=1e-8))
+    assert a.report.converged and b.report.converged
+    assert np.abs(a.image.data - b.image.data).max() <= 1e-6
+
+
+def test_oras_needs_no_more_iterations_than_ras(solver):
+    """schwarz_test.cpp:168-178."""
+    f, m = random_instance(64, 64, 0.05, 1, 31)
+    part = si.partition_domain(64, 64, 16, 4)
+    ras = solver.solve_schwarz(f, m, part, tight(si.SchwarzFlavour.Ras))
+    oras = solver.solve_schwarz(f, m, part, tight())
+    assert ras.report.converged and oras.report.converged
+    assert oras.report.iterations <= ras.report.iterations
+
+
+def test_maximum_principle_and_constants(solver):
+    """schwarz_test.cpp:180-204."""
+    f, m = random_instance(48, 32, 0.1, 1, 37)
+    res = solver.solve_schwarz(f, m, si.partition_domain(48, 32, 16, 4), tight(tol=1e-8))
+    assert res.report.converged
+    kv = f.data[0][m.known != 0]
+    assert res.image.data.min() >= kv.min() - 1e-6 and res.image.data.max() <= kv.max() + 1e-6
+    flat = si.ImageBuffer(20, 20, 1, 0.4)
+    mask = si.random_mask(20, 20, 0.1, 41)
+    res = solver.solve_schwarz(flat, mask, si.partition_domain(20, 20, 8, 2), tight(tol=1e-8))
+    assert np.abs(res.image.data - 0.4).max() <= 1e-6
+
+
+def test_full_mask_returns_input_with_zero_iterations(solver):
+    """schwarz_test.cpp:206-215."""
+    mask = si.InpaintingMask(12, 12, 1)
+    img = si.synthetic_test_image(12, 12, 1, 2)
+    res = solver.solve_schwarz(img, mask, si.partition_domain(12, 12, 6, 2), tight(tol=1e-3))
+    assert res.report.converged and res.report.iterations == 0
+    assert np.array_equal(res.image.data, img.data)
+
+
+def test_trace_rows_decrease_to_tolerance(solver):
+    """schwarz_test.cpp:217-237 (with PSNR rows)."""
+    f, m = random_instance(64, 64, 0.1, 1, 43)
+    res = solver.solve_schwarz(f, m, si.partition_domain(64, 64, 16, 4), tight(), reference=f)
+    rows = res.trace.rows
+    assert res.report.converged and len(rows) >= 2
+    assert rows[0].iteration == 0 and rows[0].rel_residual == 1.0
+    for i in range(1, len(rows)):
+        assert rows[i].rel_residual < rows[i - 1].rel_residual
+        assert rows[i].time_ms >= rows[i - 1].time_ms
+        assert rows[i].iteration == i and rows[i].psnr is not None
+    assert rows[-1].rel_residual <= 1e-6
+    assert rows[-1].psnr > rows[0].psnr
+
+
+def test_neumann_cut_stays_robust(solver):
+    """schwarz_test.cpp:257-268: alpha = 0 must not raise."""
+    f, m = random_instance(24, 24, 0.3, 1, 53)
+    opt = tight(alpha=0.0)
+    opt.schwarz.max_outer_iterations = 500
+    solver.solve_schwarz(f, m, si.partition_domain(24, 24, 8, 2), opt)
+
+
+def test_levels_one_matches_direct_schwarz_bitwise(solver):
+    """multilevel_test.cpp:161-182."""
+    f, m = random_instance(40, 30, 0.1, 3, 7)
+    mopt = si.MultilevelSolveOptions(levels=1, tolerance=1e-6, block_size=12, overlap=3)
+    ml = solver.multilevel_solve(f, m, si.LevelSolver.Oras, mopt)
+    sopt = si.SchwarzSolveOptions(tolerance=1e-6)
+    sl = solver.solve_schwarz(f, m, si.partition_domain(40, 30, 12, 3), sopt)
+    assert ml.report.iterations == sl.report.iterations
+    assert np.array_equal(ml.image.data, sl.image.data)
+
+
+def test_constant_image_zero_finest_iterations(solver):
+    """multilevel_test.cpp:184-200."""
+    flat = si.ImageBuffer(32, 32, 1, 0.7)
+    mask = si.random_mask(32, 32, 0.1, 9)
+    res = solver.multilevel_solve(flat, mask, si.LevelSolver.Oras,
+                                  si.MultilevelSolveOptions(levels=3, block_size=8, overlap=2))
+    assert res.report.converged and res.report.iterations == 0
+    assert np.abs(res.image.data - 0.7).max() <= 0.01
+
+
+def test_coarse_initialisation_cuts_finest_iterations(solver):
+    """multilevel_test.cpp:202-218."""
+    f, m = random_instance(96, 96, 0.05, 1, 11)
+    flat = solver.multilevel_solve(f, m, si.LevelSolver.Oras,
+                                   si.MultilevelSolveOptions(levels=1, block_size=16, overlap=3))
+    nested = solver.multilevel_solve(f, m, si.LevelSolver.Oras,
+                                     si.MultilevelSolveOptions(levels=3, block_size=16, overlap=3))
+    assert flat.report.converged and nested.report.converged
+    assert nested.report.iterations < flat.report.iterations
+
+
+def test_errors_mirror_reference(solver):
+    f, m = random_instance(16, 16, 0.2, 1, 1)
+    with pytest.raises(si.InvalidArgument, match="no known pixels"):
+        solver.run_method(si.Method.MultilevelOras, f, si.InpaintingMask(16, 16))
+    with pytest.raises(si.InvalidArgument, match="tolerances must be positive"):
+        solver.run_method(si.Method.MultilevelOras, f, m, si.RunOptions(tolerance=0.0))
+    with pytest.raises(si.InvalidArgument, match="dimensions differ"):
+        solver.run_method(si.Method.Oras, f, si.InpaintingMask(8, 16, 1))
+    with pytest.raises(si.InvalidArgument, match="alpha must be finite"):
+        solver.run_method(si.Method.Oras, f, m, si.RunOptions(alpha=float("nan")))
+    with pytest.raises(si.Unsupported):
+        solver.run_method(si.Method.MultilevelCg, f, m)
+
+
+def test_non_convergence_is_reported_not_raised(solver):
+    f, m = random_instance(64, 64, 0.05, 1, 3)
+    res = solver.run_method(si.Method.Oras, f, m, si.RunOptions(tolerance=1e-12,
+                                                               max_outer_iterations=2))
+    assert not res.report.converged and res.report.iterations == 2
+    assert "did not converge" in res.report.diagnostic
