@@ -189,11 +189,14 @@ si_status si_psnr(const double* u, const double* f, int w, int h, int c, double*
 /* ---- instrumentation ---------------------------------------------------- */
 
 /* Per-kernel device time (CUDA events on the launching stream) accumulated
- * while enabled; kind: 0 residual, 1 sweep, 2 restrict, 3 prolong, 4 ingest/export. */
+ * while profiling is enabled; kind: 0 residual (K1), 1 sweep (K2), 2 restrict
+ * (K3), 3 prolong (K4), 4 ingest/export (K5), 5 metrics (K6).
+ * total_launches counts every kernel launched by the context, always. */
 typedef struct si_kernel_stats {
   long long launches[8];
   double device_ms[8];
   double algorithmic_bytes[8];
+  long long total_launches;
 } si_kernel_stats;
 si_status si_set_profiling(si_ctx* ctx, int enabled);
 si_status si_get_kernel_stats(si_ctx* ctx, si_kernel_stats* out, int reset);

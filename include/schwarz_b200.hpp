@@ -1,0 +1,250 @@
+// schwarz_b200.hpp — C++ drop-in for the reference's solver front door.
+//
+// Header-only wrapper over the C ABI (schwarz_b200.h).  It reproduces the
+// reference's types and entry points (namespace schwarz_inpaint ->
+// schwarz_b200) so a caller of
+//     schwarz_inpaint::run_method(Method::MultilevelOras, f, mask, options)
+// (methods.hpp:57-88) switches by changing the include and the namespace:
+//   * ImageBuffer / InpaintingMask      image.hpp:24-94 (same planar layout)
+//   * RunOptions / SolverConfig / Method methods.hpp:13-55, cg.hpp:23-27
+//   * SolveResult / ConvergenceTrace    metrics.hpp:58-105
+//   * SubdomainPartition                partition.hpp:21-106
+// Errors: SI_ERR_INVALID_ARGUMENT -> std::invalid_argument (same message the
+// reference throws); other failures -> std::runtime_error.  Non-convergence
+// is reported in SolveReport, never thrown.
+// Link with libschwarz_b200.so.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "schwarz_b200.h"
+
+namespace schwarz_b200 {
+
+namespace detail {
+inline void throw_status(si_status s) {
+  if (s == SI_OK) return;
+  const std::string msg = si_last_error();
+  if (s == SI_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  throw std::runtime_error(std::string(si_status_string(s)) + ": " + msg);
+}
+inline void check_arg(bool ok, const std::string& msg) {
+  if (!ok) throw std::invalid_argument(msg);
+}
+}  // namespace detail
+
+struct ImageBuffer {
+  int width = 0, height = 0, channels = 1;
+  std::vector<double> data;
+  ImageBuffer() = default;
+  ImageBuffer(int w, int h, int ch, double fill = 0.0) : width(w), height(h), channels(ch) {
+    detail::check_arg(w > 0 && h > 0 && ch > 0, "ImageBuffer: dimensions must be positive");
+    data.assign(static_cast<size_t>(w) * h * ch, fill);
+  }
+  size_t pixel_count() const { return static_cast<size_t>(width) * height; }
+  double& at(int x, int y, int c = 0) { return data[c * pixel_count() + static_cast<size_t>(y) * width + x]; }
+  double at(int x, int y, int c = 0) const { return data[c * pixel_count() + static_cast<size_t>(y) * width + x]; }
+};
+
+struct InpaintingMask {
+  int width = 0, height = 0;
+  std::vector<uint8_t> known;
+  InpaintingMask() = default;
+  InpaintingMask(int w, int h, uint8_t fill = 0) : width(w), height(h) {
+    detail::check_arg(w > 0 && h > 0, "InpaintingMask: dimensions must be positive");
+    known.assign(static_cast<size_t>(w) * h, fill);
+  }
+  size_t size() const { return static_cast<size_t>(width) * height; }
+  bool is_known(int x, int y) const { return known[static_cast<size_t>(y) * width + x] != 0; }
+};
+
+enum class Method { Cg = 0, MultilevelCg = 1, Ras = 2, Oras = 3, MultilevelOras = 4 };
+enum class CoarseAveraging { KnownOnly = 0, AllPixels = 1 };
+enum class ResidualNormalizer { InitialGuess = 0, RhsNorm = 1 };
+enum class Precision { FP64 = 0, FP32 = 1 };
+
+inline constexpr double kDefaultOrasAlpha = 0.25;
+
+struct SolverConfig {
+  double tolerance = 1e-6;
+  int max_iterations = 10000;
+  int residual_check_interval = 1;
+};
+
+struct RunOptions {
+  double tolerance = 1e-3;
+  int levels = 3;
+  int block_size = 32;
+  int overlap = 6;
+  double alpha = kDefaultOrasAlpha;
+  double coarse_tolerance = 1e-2;
+  CoarseAveraging averaging = CoarseAveraging::KnownOnly;
+  SolverConfig local{1e-2, 30, 30};
+  int max_outer_iterations = 1000;
+  int cg_max_iterations = 100000;
+  int cg_check_interval = 4;
+  ResidualNormalizer normalizer = ResidualNormalizer::InitialGuess;
+  Precision precision = Precision::FP64;  // device arithmetic; FP64 = the reference's
+
+  si_options to_c() const {
+    si_options o;
+    o.tolerance = tolerance;
+    o.levels = levels;
+    o.block_size = block_size;
+    o.overlap = overlap;
+    o.alpha = alpha;
+    o.coarse_tolerance = coarse_tolerance;
+    o.averaging = static_cast<int>(averaging);
+    o.local_tolerance = local.tolerance;
+    o.local_max_iterations = local.max_iterations;
+    o.local_check_interval = local.residual_check_interval;
+    o.max_outer_iterations = max_outer_iterations;
+    o.cg_max_iterations = cg_max_iterations;
+    o.cg_check_interval = cg_check_interval;
+    o.normalizer = static_cast<int>(normalizer);
+    o.precision = static_cast<int>(precision);
+    return o;
+  }
+};
+
+struct TraceRow {
+  int iteration = 0;
+  double time_ms = 0.0;
+  double rel_residual = 0.0;
+  std::optional<double> psnr;
+};
+
+struct ConvergenceTrace {
+  std::vector<TraceRow> rows;
+  void append(int it, double ms, double rel, std::optional<double> q = std::nullopt) {
+    rows.push_back({it, ms, rel, q});
+  }
+};
+
+struct SolveReport {
+  int iterations = 0;
+  double final_relative_residual = 0.0;
+  bool converged = false;
+  std::string diagnostic;
+  std::vector<int> level_iterations;  // index 0 = finest (B200 extension)
+  long long local_solves = 0, local_failures = 0, local_cg_iterations = 0;
+};
+
+struct SolveResult {
+  ImageBuffer image;
+  ConvergenceTrace trace;
+  SolveReport report;
+};
+
+struct Subdomain {
+  int x0 = 0, y0 = 0, width = 0, height = 0;
+  int own_x0 = 0, own_y0 = 0, own_x1 = 0, own_y1 = 0;
+};
+
+struct SubdomainPartition {
+  int image_width = 0, image_height = 0, block_size = 0, overlap = 0, blocks_x = 0, blocks_y = 0;
+  std::vector<Subdomain> subdomains;
+  size_t size() const { return subdomains.size(); }
+};
+
+// One device context per thread (the reference's single global thread pool
+// becomes one CUDA context per host thread / GPU).
+class Context {
+ public:
+  explicit Context(int device = 0) { detail::throw_status(si_create(device, &ctx_)); }
+  ~Context() { si_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  si_ctx* get() const { return ctx_; }
+
+  static Context& thread_default() {
+    thread_local Context ctx(0);
+    return ctx;
+  }
+
+ private:
+  si_ctx* ctx_ = nullptr;
+};
+
+namespace detail {
+inline void trace_sink(int it, double ms, double rel, double q, void* user) {
+  auto* t = static_cast<ConvergenceTrace*>(user);
+  t->append(it, ms, rel, std::isnan(q) ? std::nullopt : std::optional<double>(q));
+}
+inline SolveReport to_report(const si_report& r) {
+  SolveReport out;
+  out.iterations = r.iterations;
+  out.final_relative_residual = r.final_relative_residual;
+  out.converged = r.converged != 0;
+  out.diagnostic = r.diagnostic;
+  out.level_iterations.assign(r.level_iterations, r.level_iterations + r.depth);
+  out.local_solves = r.local_solves;
+  out.local_failures = r.local_failures;
+  out.local_cg_iterations = r.local_cg_iterations;
+  return out;
+}
+}  // namespace detail
+
+// run_method (methods.hpp:57-88).
+inline SolveResult run_method(Method method, const ImageBuffer& f, const InpaintingMask& mask,
+                              const RunOptions& options, const ImageBuffer* reference = nullptr,
+                              Context& ctx = Context::thread_default()) {
+  detail::check_arg(f.width == mask.width && f.height == mask.height,
+                    "image and mask dimensions differ");
+  SolveResult res;
+  res.image = ImageBuffer(f.width, f.height, f.channels);
+  si_report rep;
+  const si_options o = options.to_c();
+  detail::throw_status(si_run_method(ctx.get(), static_cast<int>(method), f.data.data(),
+                                     mask.known.data(), f.width, f.height, f.channels, &o,
+                                     reference ? reference->data.data() : nullptr,
+                                     res.image.data.data(), &rep, &detail::trace_sink,
+                                     &res.trace));
+  res.report = detail::to_report(rep);
+  return res;
+}
+
+// partition_domain (partition.hpp:67-106).
+inline SubdomainPartition partition_domain(int w, int h, int block, int overlap) {
+  SubdomainPartition p;
+  detail::throw_status(si_partition_domain(w, h, block, overlap, &p.blocks_x, &p.blocks_y,
+                                           nullptr, 0));
+  std::vector<int> r(8 * static_cast<size_t>(p.blocks_x) * p.blocks_y);
+  detail::throw_status(si_partition_domain(w, h, block, overlap, &p.blocks_x, &p.blocks_y,
+                                           r.data(), p.blocks_x * p.blocks_y));
+  p.image_width = w;
+  p.image_height = h;
+  p.block_size = block;
+  p.overlap = overlap;
+  for (size_t i = 0; i < r.size(); i += 8)
+    p.subdomains.push_back({r[i], r[i + 1], r[i + 2], r[i + 3], r[i + 4], r[i + 5], r[i + 6], r[i + 7]});
+  return p;
+}
+
+inline ImageBuffer synthetic_test_image(int w, int h, int c, uint64_t seed) {
+  ImageBuffer img(w, h, c);
+  detail::throw_status(si_synthetic_test_image(w, h, c, seed, img.data.data()));
+  return img;
+}
+
+inline InpaintingMask random_mask(int w, int h, double density, uint64_t seed) {
+  InpaintingMask m(w, h);
+  const si_status s = si_random_mask(w, h, density, seed, m.known.data());
+  if (s != SI_OK) throw std::invalid_argument("random_mask: invalid dimensions or density");
+  return m;
+}
+
+inline double psnr(const ImageBuffer& u, const ImageBuffer& f) {
+  detail::check_arg(u.width == f.width && u.height == f.height && u.channels == f.channels,
+                    "mse_per_channel: image dimensions differ");
+  double q = 0.0;
+  detail::throw_status(si_psnr(u.data.data(), f.data.data(), u.width, u.height, u.channels, &q));
+  return q;
+}
+
+}  // namespace schwarz_b200

@@ -63,6 +63,7 @@ class si_kernel_stats(C.Structure):
         ("launches", C.c_longlong * 8),
         ("device_ms", C.c_double * 8),
         ("algorithmic_bytes", C.c_double * 8),
+        ("total_launches", C.c_longlong),
     ]
 
 

@@ -546,9 +546,11 @@ class Solver:
     def kernel_stats(self, reset: bool = False) -> dict:
         s = L.si_kernel_stats()
         _check(self._lib.si_get_kernel_stats(self._h, C.byref(s), int(reset)))
-        names = ["residual", "sweep", "restrict", "prolong", "ingest_export"]
-        return {n: {"launches": s.launches[i], "device_ms": s.device_ms[i],
-                    "algorithmic_bytes": s.algorithmic_bytes[i]} for i, n in enumerate(names)}
+        names = ["residual", "sweep", "restrict", "prolong", "ingest_export", "metrics"]
+        out = {n: {"launches": s.launches[i], "device_ms": s.device_ms[i],
+                   "algorithmic_bytes": s.algorithmic_bytes[i]} for i, n in enumerate(names)}
+        out["total_launches"] = s.total_launches
+        return out
 
 
 def _require_same_grid(f: ImageBuffer, mask: InpaintingMask):

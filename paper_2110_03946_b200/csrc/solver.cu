@@ -81,7 +81,7 @@ struct LevelBuf {
   DevBuf mask, b, u0, u1;
 };
 
-enum Kind { K_RESIDUAL = 0, K_SWEEP = 1, K_RESTRICT = 2, K_PROLONG = 3, K_INGEST = 4, K_COUNT = 5 };
+enum Kind { K_RESIDUAL = 0, K_SWEEP = 1, K_RESTRICT = 2, K_PROLONG = 3, K_INGEST = 4, K_METRIC = 5 };
 
 struct PendingEvent {
   int kind;
@@ -105,6 +105,7 @@ struct si_ctx {
   std::vector<cudaEvent_t> event_pool;
   si_kernel_stats stats{};
   int sweep_nw64 = 2, sweep_nw32 = 1;           // warps per sweep CTA
+  long long launch_count = 0;                   // kernels launched (always counted)
 };
 
 namespace {
@@ -133,6 +134,7 @@ struct Timed {
   double bytes;
   cudaEvent_t a = nullptr, b = nullptr;
   Timed(Ctx& x_, int k, double by) : x(x_), kind(k), bytes(by) {
+    x.c.launch_count += 1;
     if (x.c.profiling) {
       a = take_event(x.c);
       b = take_event(x.c);
@@ -190,6 +192,7 @@ void launch_sq_error(Ctx& x, const T* u, const double* f, size_t N, int C, doubl
   const int g = grid_for(N, kRedThreads, kRedBlocksMax);
   x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(g) * C);
   x.c.ticket.ensure(sizeof(unsigned int) * 4);
+  Timed t(x, K_METRIC, static_cast<double>(N) * C * (sizeof(T) + 8.0));
   sq_error_kernel<T><<<dim3(g, C), kRedThreads, 0, x.s>>>(
       u, f, N, x.c.red_partials.as<double>(), out, x.c.ticket.as<unsigned int>());
   CK(cudaGetLastError());
@@ -1083,7 +1086,11 @@ si_status si_get_kernel_stats(si_ctx* ctx, si_kernel_stats* out, int reset) {
     set_device(ctx);
     if (!ctx->pending.empty()) resolve_events(*ctx);
     *out = ctx->stats;
-    if (reset) ctx->stats = si_kernel_stats{};
+    out->total_launches = ctx->launch_count;
+    if (reset) {
+      ctx->stats = si_kernel_stats{};
+      ctx->launch_count = 0;
+    }
   });
 }
 

@@ -1,0 +1,124 @@
+"""Generate tests/golden/ fixtures from the UNMODIFIED reference.
+
+Runs only where the reference was compiled (oracle/_ref/libref.so, built by
+oracle/Makefile from /root/reference/proj/include).  Every fixture records
+the reference's own outputs on seeded inputs from its own generators:
+
+  inputs.json   sha256 of synthetic_test_image / random_mask bytes per config
+  c1.npz        256x256 grey, 5%, 2 levels: full output, trace, level counts
+  c2.npz/c3.npz 1080p / 4K RGB: trace, level counts, local-solve statistics,
+                per-channel sums and 4096 sampled output pixels
+  small.npz     12 small instances over the option space, full outputs
+  kernels.npz   restriction / prolongation / local-operator probes
+
+Usage: python tests/golden/make_golden.py
+"""
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import pyoracle as P  # noqa: E402
+
+CONFIGS = {
+    "c1": dict(w=256, h=256, c=1, d=0.05, levels=2),
+    "c2": dict(w=1920, h=1080, c=3, d=0.04, levels=2),
+    "c3": dict(w=3840, h=2160, c=3, d=0.04, levels=3),
+}
+
+SMALL = [
+    # w, h, c, density, seed, options
+    (64, 64, 1, 0.1, 1, dict(levels=1, tolerance=1e-6, block_size=16, overlap=4)),
+    (64, 48, 3, 0.07, 2, dict(levels=1, tolerance=1e-6, block_size=16, overlap=4)),
+    (40, 40, 3, 0.1, 3, dict(levels=1, tolerance=1e-6, block_size=16, overlap=4, flavour=0)),
+    (96, 96, 1, 0.05, 4, dict(levels=3, block_size=16, overlap=3)),
+    (48, 48, 1, 0.08, 5, dict(levels=3, tolerance=1e-8, block_size=16, overlap=4)),
+    (123, 77, 3, 0.04, 6, dict(levels=4)),
+    (9, 3, 1, 0.5, 7, dict(levels=5)),
+    (33, 17, 2, 0.3, 8, dict(levels=3, averaging=1, normalizer=1)),
+    (150, 90, 3, 0.02, 9, dict(levels=3, alpha=0.5, block_size=24, overlap=5)),
+    (50, 40, 2, 0.2, 10, dict(levels=2, block_size=32, overlap=6)),
+    (77, 31, 1, 0.15, 11, dict(levels=2, block_size=8, overlap=3, alpha=2.0)),
+    (128, 128, 3, 0.05, 12, dict(levels=3, local_max_iterations=10, local_check_interval=4)),
+]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def instance(w, h, c, d, seed_img, seed_mask):
+    return P.ref_synthetic_test_image(w, h, c, seed_img), P.ref_random_mask(w, h, d, seed_mask)
+
+
+def main():
+    if not P.ref_available():
+        sys.exit("oracle/_ref/libref.so missing: run `make -C oracle` where /root/reference exists")
+    P.ref().ref_set_threads(0)
+    hashes = {}
+    for name, cfg in CONFIGS.items():
+        f, m = instance(cfg["w"], cfg["h"], cfg["c"], cfg["d"], 7, 11)
+        hashes[name] = {"image": sha(f), "mask": sha(m), **cfg}
+        run = P.ref_run_method("mloras", f, m, levels=cfg["levels"])
+        lv = P.ref_solve_levels(f, m, levels=cfg["levels"])
+        assert np.array_equal(run.image, lv.image) and np.array_equal(run.trace, lv.trace)
+        rng = np.random.default_rng(1234)
+        idx = rng.choice(f.size, size=min(4096, f.size), replace=False)
+        fields = dict(trace=run.trace, level_iterations=np.array(lv.level_iterations),
+                      iterations=run.iterations, final_rel=run.final_rel,
+                      converged=run.converged, local_solves=lv.local_solves,
+                      local_failures=lv.local_failures, channel_sum=run.image.sum(axis=(1, 2)),
+                      channel_sumsq=(run.image ** 2).sum(axis=(1, 2)), sample_index=idx,
+                      sample_value=run.image.reshape(-1)[idx])
+        if name == "c1":
+            fields["image"] = run.image
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **fields)
+        print(name, lv.level_iterations, run.trace)
+
+    small = {}
+    for i, (w, h, c, d, seed, opts) in enumerate(SMALL):
+        f, m = instance(w, h, c, max(d, 1.5 / (w * h)), 1000 + seed, 77 + seed)
+        lv = P.ref_solve_levels(f, m, **opts)
+        small[f"case{i}_image"] = lv.image
+        small[f"case{i}_trace"] = lv.trace
+        small[f"case{i}_levels"] = np.array(lv.level_iterations)
+        small[f"case{i}_stats"] = np.array([lv.local_solves, lv.local_failures, int(lv.converged)])
+        hashes[f"small{i}"] = {"image": sha(f), "mask": sha(m), "w": w, "h": h, "c": c,
+                               "d": max(d, 1.5 / (w * h)), "seed_image": 1000 + seed,
+                               "seed_mask": 77 + seed, "options": opts}
+    np.savez_compressed(os.path.join(HERE, "small.npz"), **small)
+
+    # kernel probes: restriction (both averagings), prolongation, local operator
+    k = {}
+    f, m = instance(29, 23, 2, 0.3, 5, 6)
+    vals = np.where(m[None] != 0, f, 0.0)
+    for avg in (0, 1):
+        cm = np.empty((12, 15), np.uint8)
+        cv = np.empty((2, 12, 15))
+        assert P.ref().ref_restrict_level(m.ravel(), vals.ravel(), 29, 23, 2, avg, cm.ravel(),
+                                          cv.ravel()) == 0
+        k[f"restrict{avg}_mask"], k[f"restrict{avg}_values"] = cm, cv
+    k["restrict_in_mask"], k["restrict_in_values"] = m, vals
+    coarse = np.random.default_rng(5).uniform(0, 1, (23, 37))
+    fine = np.empty((45, 73))
+    assert P.ref().ref_prolongate(coarse.ravel(), 37, 23, 73, 45, fine.ravel()) == 0
+    k["prolong_in"], k["prolong_out"] = coarse, fine
+    v = np.random.default_rng(9).uniform(-1, 1, 64)
+    out = np.empty(64)
+    assert P.ref().ref_local_operator_apply(m.ravel(), 29, 23, 8, 2, 5, 1, 0.25, v, out) == 0
+    k["localop_mask"], k["localop_in"], k["localop_out"] = m, v, out
+    np.savez_compressed(os.path.join(HERE, "kernels.npz"), **k)
+
+    with open(os.path.join(HERE, "inputs.json"), "w") as fh:
+        json.dump(hashes, fh, indent=1, sort_keys=True)
+    print("wrote fixtures to", HERE)
+
+
+if __name__ == "__main__":
+    main()
