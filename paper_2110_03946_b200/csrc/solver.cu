@@ -104,7 +104,7 @@ struct si_ctx {
   std::vector<PendingEvent> pending;
   std::vector<cudaEvent_t> event_pool;
   si_kernel_stats stats{};
-  int sweep_nw64 = 2, sweep_nw32 = 1;           // warps per sweep CTA
+  int sweep_nw64 = 4, sweep_nw32 = 2;           // warps per sweep CTA
   long long launch_count = 0;                   // kernels launched (always counted)
 };
 
@@ -206,14 +206,10 @@ struct LocalCfg {
 
 template <typename T, int NW>
 void launch_sweep_nw(Ctx& x, const SweepArgs<T>& a, int nblocks, int C) {
-  const size_t smem = sizeof(SweepSmem<T, NW>);
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(oras_sweep_kernel<T, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(smem)));
-    attr = true;
-  }
-  oras_sweep_kernel<T, NW><<<dim3(nblocks, C), NW * 32, smem, x.s>>>(a);
+  if (a.ax.block == kMaxBlock)
+    oras_sweep_kernel<T, NW, true><<<dim3(nblocks, C), NW * 32, 0, x.s>>>(a);
+  else
+    oras_sweep_kernel<T, NW, false><<<dim3(nblocks, C), NW * 32, 0, x.s>>>(a);
   CK(cudaGetLastError());
 }
 
@@ -244,10 +240,13 @@ void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_
   const double bytes = static_cast<double>(a.N) * (2.0 * C * sizeof(T) + 1.0);
   Timed t(x, K_SWEEP, bytes);
   const int nw = sizeof(T) == 8 ? x.c.sweep_nw64 : x.c.sweep_nw32;
-  switch (nw) {
-    case 1: launch_sweep_nw<T, 1>(x, a, nblocks, C); break;
-    case 4: launch_sweep_nw<T, 4>(x, a, nblocks, C); break;
-    default: launch_sweep_nw<T, 2>(x, a, nblocks, C); break;
+  if constexpr (sizeof(T) == 8) {
+    if (nw == 2) launch_sweep_nw<T, 2>(x, a, nblocks, C);
+    else launch_sweep_nw<T, 4>(x, a, nblocks, C);
+  } else {
+    if (nw == 1) launch_sweep_nw<T, 1>(x, a, nblocks, C);
+    else if (nw == 2) launch_sweep_nw<T, 2>(x, a, nblocks, C);
+    else launch_sweep_nw<T, 4>(x, a, nblocks, C);
   }
 }
 

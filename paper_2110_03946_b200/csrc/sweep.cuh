@@ -6,24 +6,26 @@
 //   solve_local_block + cg_solve (schwarz.hpp:202-250, cg.hpp:90-154),
 //   accumulate_owned (partition.hpp:148-156).
 //
-// One CTA = one (subdomain, channel).  The residual slice is computed on chip
-// from the (B+2)^2 window of u_old (so no global residual image is ever
-// written), and the local CG runs entirely in registers:
-//   * lane = block column, each warp owns R = 32/NW consecutive rows, so
-//     horizontal stencil neighbours come from __shfl_up/down and vertical
-//     ones from the thread's own registers;
-//   * rows at warp boundaries are exchanged through shared memory, but never
-//     with a dedicated barrier: before each reduction barrier every warp
-//     publishes the *components* of its boundary rows (r, old p, x), and its
-//     neighbours rebuild p_new = r + beta*p with the identical fma after the
-//     barrier.  A CG iteration therefore costs exactly 2 CTA barriers (3 on
-//     a true-residual check), and 0 when NW == 1;
+// One CTA = one (subdomain, channel), NW warps.  Layout: lane = block column,
+// warp w owns rows [w*R, (w+1)*R), R = 32/NW, so every CG vector lives in
+// registers (R values per thread per vector):
+//   * horizontal stencil neighbours come from __shfl_up/down, vertical ones
+//     from the thread's own registers;
+//   * the rows at warp boundaries are exchanged through shared memory with no
+//     dedicated barrier: before each reduction barrier every warp publishes
+//     the *components* of its boundary rows (r, old p, x) and its neighbours
+//     rebuild p_new = r + beta*p with the identical fma afterwards.  One CG
+//     iteration costs 2 CTA barriers (3 on a true-residual check);
 //   * dot products: warp butterfly + fixed-order cross-warp sum, so every
-//     thread holds the same value and all control flow stays CTA-uniform.
-// The result u_new = u_old + v is written only on the block's owned
-// rectangle into a separate buffer (ping-pong): owned rectangles tile the
-// image, so every pixel is written exactly once and no CTA reads what
-// another writes.
+//     thread holds the same value and all control flow is CTA-uniform.
+// Nothing is staged in shared memory besides those boundary rows: the
+// residual slice and the local right-hand side are rebuilt from global memory
+// (u_old, mask, b are read-only during the sweep) whenever they are needed —
+// at setup, at the rare true-residual checks and at write-back — which keeps
+// shared memory at ~4 KB per CTA and occupancy register-bound.
+// u_new = u_old + v is written only on the block's owned rectangle into a
+// separate buffer (ping-pong): owned rectangles tile the image, so every
+// pixel is written exactly once and no CTA reads what another writes.
 #pragma once
 
 #include "common.cuh"
@@ -53,23 +55,6 @@ __device__ __forceinline__ T fmaT(T a, T b, T c) {
   return fma(a, b, c);
 }
 
-// Residual of the global operator at an interior-of-window cell whose u
-// neighbours sit in the shared tile (operators.hpp:38-66, 91-97):
-//   known:   r = b - u
-//   unknown: r = b - (deg*u - (((W + E) + N) + S)) over in-image neighbours.
-template <typename T>
-__device__ __forceinline__ T residual_cell(T u, T uW, T uE, T uN, T uS, bool known, T bv, int gx,
-                                           int gy, int W, int H) {
-  if (known) return bv - u;
-  T sum = T(0);
-  int deg = 0;
-  if (gx > 0) { sum += uW; ++deg; }
-  if (gx + 1 < W) { sum += uE; ++deg; }
-  if (gy > 0) { sum += uN; ++deg; }
-  if (gy + 1 < H) { sum += uS; ++deg; }
-  return bv - fmaT(T(deg), u, -sum);
-}
-
 // Robin diagonal of an unknown cell (fill_local_structure, schwarz.hpp:100-108):
 //   diag = deg_global + (alpha - 1) * cut, cut = in-image neighbours outside the block.
 template <typename T>
@@ -84,12 +69,10 @@ __device__ __forceinline__ T robin_diag(int gx, int gy, int lx, int ly, int B, i
 
 template <typename T, int NW>
 struct SweepSmem {
-  T us[kTile][kTile];          // u_old window, rows/cols -1..B
-  T rs[kTile][kTile];          // residual slice with a zero ghost ring
-  T bs[kMaxBlock][kMaxBlock];  // local right-hand side (for true residuals)
-  uint8_t ms[kTile][kTile + 2];
-  T pub[NW > 1 ? NW : 1][2][3][32];   // [warp][top/bottom][r,p,x][col]
-  T pubt[NW > 1 ? NW : 1][2][32];     // true-residual boundary rows
+  T pt[kMaxBlock][kMaxBlock + 2];  // stencil operand rows, zero ghost columns 0 and B+1
+  T bt[kMaxBlock][kMaxBlock];      // local right-hand side (true-residual checks)
+  T pub[NW][2][3][32];             // [warp][top/bottom][r,p,x][col]
+  T pubt[NW][2][32];               // true-residual boundary rows
   T red[3][NW];
 };
 
@@ -107,102 +90,188 @@ __device__ __forceinline__ T cta_sum(T v, T (*red)[NW], int slot, int warp, int 
   return s;
 }
 
+// Per-thread view of the block: column lx, rows row0 .. row0+R-1.
+template <typename T, int R>
+struct Cell {
+  int lx, gx, row0, x0, y0, B, W, H;
+  bool col_ok;
+  const uint8_t* __restrict__ mask;
+  const T* __restrict__ u;
+  const T* __restrict__ b;
+  int b_known_only;
+};
+
+// Residual r = b - A u (operators.hpp:38-66, 91-97) of block rows
+// row0-1 .. row0+R (index j = 0..R+1; rows outside the block are ghosts = 0),
+// together with the in-block known bits of the same rows and u of own rows.
+//   known:   r = b - u
+//   unknown: r = b - (deg*u - (((W + E) + N) + S)) over in-image neighbours.
+template <typename T, int R>
+__device__ __forceinline__ void residual_rows(const Cell<T, R>& c, T (&r)[R + 2], uint64_t& kbits,
+                                              T (&u_own)[R]) {
+  const int lane = threadIdx.x & 31;
+  // u of rows row0-2 .. row0+R+1 at my column (k = 0..R+3); the ring columns
+  // x0-1 (lane 0) and x0+B (lane B-1) are fetched on demand below.
+  T uc[R + 4];
+  const bool edge_w = lane == 0, edge_e = lane == c.B - 1;
+#pragma unroll
+  for (int k = 0; k < R + 4; ++k) {
+    const int gy = c.y0 + c.row0 - 2 + k;
+    T v = T(0);
+    if (gy >= 0 && gy < c.H && c.gx < c.W && lane <= c.B) v = c.u[static_cast<size_t>(gy) * c.W + c.gx];
+    uc[k] = v;
+  }
+  kbits = 0;
+#pragma unroll
+  for (int j = 0; j < R + 2; ++j) {
+    const int ly = c.row0 - 1 + j;
+    const int gy = c.y0 + ly;
+    const int k = j + 1;  // index of this row in uc
+    T sW = __shfl_up_sync(0xffffffffu, uc[k], 1);
+    T sE = __shfl_down_sync(0xffffffffu, uc[k], 1);
+    if (gy >= 0 && gy < c.H) {
+      const size_t rowp = static_cast<size_t>(gy) * c.W;
+      if (edge_w) sW = c.gx > 0 ? c.u[rowp + c.gx - 1] : T(0);
+      if (edge_e) sE = c.gx + 1 < c.W ? c.u[rowp + c.gx + 1] : T(0);
+    }
+    T rv = T(0);
+    if (c.col_ok && ly >= 0 && ly < c.B) {
+      const size_t p = static_cast<size_t>(gy) * c.W + c.gx;
+      const bool known = c.mask[p] != 0;
+      if (known) kbits |= 1ull << j;
+      const T bv = (known || !c.b_known_only) ? c.b[p] : T(0);
+      if (known) {
+        rv = bv - uc[k];
+      } else {
+        T sum = T(0);
+        int deg = 0;
+        if (c.gx > 0) { sum += sW; ++deg; }
+        if (c.gx + 1 < c.W) { sum += sE; ++deg; }
+        if (gy > 0) { sum += uc[k - 1]; ++deg; }
+        if (gy + 1 < c.H) { sum += uc[k + 1]; ++deg; }
+        rv = bv - fmaT(T(deg), uc[k], -sum);
+      }
+    }
+    r[j] = rv;
+    if (j >= 1 && j <= R) u_own[j - 1] = uc[k];
+  }
+}
+
+// Local right-hand side of my rows (solve_local_block, schwarz.hpp:219-230):
+//   rhs = unk * (pv + knw_W pv_W + knw_E pv_E + knw_N pv_N + knw_S pv_S),
+// knw counting only in-block neighbours (ghost ring = 0).  Returns unk bits.
+template <typename T, int R>
+__device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, T (&rhs)[R], T (&u_own)[R],
+                                              uint64_t* kbits_out = nullptr) {
+  const int lane = threadIdx.x & 31;
+  T r[R + 2];
+  uint64_t kb;
+  residual_rows<T, R>(c, r, kb, u_own);
+  const uint64_t kbW = __shfl_up_sync(0xffffffffu, kb, 1);
+  const uint64_t kbE = __shfl_down_sync(0xffffffffu, kb, 1);
+  uint32_t unk = 0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int j = i + 1;
+    const int ly = c.row0 + i;
+    const T rW = __shfl_up_sync(0xffffffffu, r[j], 1);
+    const T rE = __shfl_down_sync(0xffffffffu, r[j], 1);
+    T t = T(0);
+    if (c.col_ok && ly < c.B && !((kb >> j) & 1ull)) {
+      unk |= 1u << i;
+      t = r[j];
+      if (lane > 0 && ((kbW >> j) & 1ull)) t += rW;
+      if (lane + 1 < c.B && ((kbE >> j) & 1ull)) t += rE;
+      if (ly > 0 && ((kb >> (j - 1)) & 1ull)) t += r[j - 1];
+      if (ly + 1 < c.B && ((kb >> (j + 1)) & 1ull)) t += r[j + 1];
+    }
+    rhs[i] = t;
+  }
+  if (kbits_out) *kbits_out = kb;
+  return unk;
+}
+
+// Resident CTAs per SM requested from ptxas (caps registers per thread):
+// the CG vectors need 4*R values of T per thread.
 template <typename T, int NW>
-__global__ void __launch_bounds__(NW * 32) oras_sweep_kernel(SweepArgs<T> a) {
+struct SweepOcc {
+  static constexpr int value = sizeof(T) == 8 ? (NW == 4 ? 4 : (NW == 2 ? 3 : 1))
+                                              : (NW == 4 ? 6 : (NW == 2 ? 4 : 2));
+};
+
+// FULL: the block is exactly 32x32 (every level of any image >= 32 pixels
+// wide and high with the default block size), so the Robin rows are
+// compile-time positions.
+template <typename T, int NW, bool FULL>
+__global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_kernel(SweepArgs<T> a) {
   constexpr int R = 32 / NW;  // rows per thread
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  SweepSmem<T, NW>& S = *reinterpret_cast<SweepSmem<T, NW>*>(smem_raw);
+  __shared__ SweepSmem<T, NW> S;
 
   const int bx = blockIdx.x % a.ax.count;
   const int by = blockIdx.x / a.ax.count;
-  const int c = blockIdx.y;
-  const int B = a.ax.block;
-  const int x0 = a.ax.anchor(bx), y0 = a.ay.anchor(by);
-  const int W = a.W, H = a.H;
+  const int ch = blockIdx.y;
+  const int B = FULL ? kMaxBlock : a.ax.block;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const size_t plane = static_cast<size_t>(c) * a.N;
-  const T* __restrict__ uo = a.u_old + plane;
-  const T* __restrict__ bb = a.b + plane;
+  const size_t plane = static_cast<size_t>(ch) * a.N;
 
-  // ---- 1. stage the u window and mask (coalesced along rows) ----------
-  const int TW = B + 2;
-  for (int i = tid; i < TW * TW; i += NW * 32) {
-    const int ly = i / TW - 1, lx = i % TW - 1;
-    const int gy = y0 + ly, gx = x0 + lx;
-    T uv = T(0);
-    uint8_t mk = 0;
-    if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
-      const size_t p = static_cast<size_t>(gy) * W + gx;
-      uv = uo[p];
-      mk = a.mask[p];
-    }
-    S.us[ly + 1][lx + 1] = uv;
-    S.ms[ly + 1][lx + 1] = mk;
-  }
-  __syncthreads();
+  Cell<T, R> c;
+  c.lx = lane;
+  c.x0 = a.ax.anchor(bx);
+  c.y0 = a.ay.anchor(by);
+  c.gx = c.x0 + lane;
+  c.row0 = warp * R;
+  c.B = B;
+  c.W = a.W;
+  c.H = a.H;
+  c.col_ok = lane < B;
+  c.mask = a.mask;
+  c.u = a.u_old + plane;
+  c.b = a.b + plane;
+  c.b_known_only = a.b_known_only;
 
-  // ---- 2. residual slice (restrict_block_into of r = b - A u) ----------
-  int any_unknown = 0;
-  for (int i = tid; i < TW * TW; i += NW * 32) {
-    const int ly = i / TW - 1, lx = i % TW - 1;
-    T rv = T(0);
-    if (lx >= 0 && lx < B && ly >= 0 && ly < B) {
-      const int gy = y0 + ly, gx = x0 + lx;
-      const bool known = S.ms[ly + 1][lx + 1] != 0;
-      any_unknown |= !known;
-      const size_t p = static_cast<size_t>(gy) * W + gx;
-      const T bv = (known || !a.b_known_only) ? bb[p] : T(0);
-      rv = residual_cell(S.us[ly + 1][lx + 1], S.us[ly + 1][lx], S.us[ly + 1][lx + 2],
-                         S.us[ly][lx + 1], S.us[ly + 2][lx + 1], known, bv, gx, gy, W, H);
-    }
-    S.rs[ly + 1][lx + 1] = rv;
-  }
-  any_unknown = __syncthreads_or(any_unknown);
-
-  // ---- 3. local system in registers: lane = column, rows warp*R + i -----
-  const int lx = lane;
-  const int gx = x0 + lx;
-  const bool col_ok = lx < B;
-  const int row0 = warp * R;
-  uint32_t unk = 0;  // bit i: cell (row0+i, lx) is an unknown block cell
   T x[R], r[R], p[R], q[R];
-  T dI = T(0), dT = T(0), dB = T(0);  // Robin diagonals: interior / first / last row
-  if (col_ok) {
-    dI = robin_diag(gx, y0 + 1, lx, 1, B, W, H, a.am1, a.ras);
-    dT = robin_diag(gx, y0, lx, 0, B, W, H, a.am1, a.ras);
-    dB = robin_diag(gx, y0 + B - 1, lx, B - 1, B, W, H, a.am1, a.ras);
+  uint32_t unk;
+  {
+    T u_scratch[R];
+    unk = local_rhs<T, R>(c, r, u_scratch);
   }
-  const int iT = -row0;             // local row index of ly == 0 (if in range)
-  const int iB = (B - 1) - row0;    // local row index of ly == B-1
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    x[i] = T(0);
+    S.bt[c.row0 + i][lane] = r[i];
+    S.pt[c.row0 + i][lane + 1] = r[i];  // p = r initially
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) S.pt[c.row0 + i][0] = T(0);
+  }
+  if (lane == B - 1 || (!FULL && lane == 31)) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) S.pt[c.row0 + i][B + 1] = T(0);
+  }
+  const int any_unknown = __syncthreads_or(unk != 0);
+
+  // Robin diagonals of my column: interior rows, block row 0, block row B-1.
+  T dI = T(0), dT = T(0), dB = T(0);
+  if (c.col_ok) {
+    dI = robin_diag(c.gx, c.y0 + 1, lane, 1, B, c.W, c.H, a.am1, a.ras);
+    dT = robin_diag(c.gx, c.y0, lane, 0, B, c.W, c.H, a.am1, a.ras);
+    dB = robin_diag(c.gx, c.y0 + B - 1, lane, B - 1, B, c.W, c.H, a.am1, a.ras);
+  }
+  const T dFirst = (warp == 0) ? dT : dI;        // FULL: row i = 0
+  const T dLast = (warp == NW - 1) ? dB : dI;    // FULL: row i = R-1
+  const int iT = -c.row0;            // generic: local index of block row 0
+  const int iB = (B - 1) - c.row0;   // generic: local index of block row B-1
+
   int iters = 0;
   bool converged = true;
 
   if (any_unknown) {
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int ly = row0 + i;
-      T rhs = T(0);
-      if (col_ok && ly < B && !S.ms[ly + 1][lx + 1]) {
-        unk |= 1u << i;
-        // rhs = unk*(pv + sum_{in-block nbrs} knw*pv) (schwarz.hpp:219-230)
-        T t = S.rs[ly + 1][lx + 1];
-        if (lx > 0 && S.ms[ly + 1][lx]) t += S.rs[ly + 1][lx];
-        if (lx + 1 < B && S.ms[ly + 1][lx + 2]) t += S.rs[ly + 1][lx + 2];
-        if (ly > 0 && S.ms[ly][lx + 1]) t += S.rs[ly][lx + 1];
-        if (ly + 1 < B && S.ms[ly + 2][lx + 1]) t += S.rs[ly + 2][lx + 1];
-        rhs = t;
-      }
-      if (ly < kMaxBlock) S.bs[ly][lx] = rhs;
-      x[i] = T(0);
-      r[i] = rhs;  // r = b - A*0 = b exactly
-      p[i] = rhs;
-    }
-
-    // Neighbour rows of my tile (vertical boundary): p, r, x of the row
-    // above (index 0) and below (index 1).
+    for (int i = 0; i < R; ++i) p[i] = r[i];  // r = b - A*0 = b exactly
     T nb_p[2] = {T(0), T(0)}, nb_r[2] = {T(0), T(0)}, nb_x[2] = {T(0), T(0)};
 
-    auto publish = [&](void) {
+    auto publish = [&]() {
       if (NW > 1) {
         S.pub[warp][0][0][lane] = r[0];
         S.pub[warp][0][1][lane] = p[0];
@@ -212,7 +281,7 @@ __global__ void __launch_bounds__(NW * 32) oras_sweep_kernel(SweepArgs<T> a) {
         S.pub[warp][1][2][lane] = x[R - 1];
       }
     };
-    auto collect = [&](void) {
+    auto collect = [&]() {
       if (NW > 1) {
         if (warp > 0) {
           nb_r[0] = S.pub[warp - 1][1][0][lane];
@@ -226,24 +295,34 @@ __global__ void __launch_bounds__(NW * 32) oras_sweep_kernel(SweepArgs<T> a) {
         }
       }
     };
-    // q = A v on my cells (LocalStencilOperator::apply, schwarz.hpp:146-159):
-    // o = unk * (d*v - vW - vE - vN - vS); neighbours outside the block are
-    // ghost zeros, which every CG vector already holds there.
-    auto apply = [&](const T* v, T vN0, T vS1, T* o) {
+    // Stage my rows of v as stencil operand (the warp owns whole rows, so a
+    // warp barrier suffices; the ghost columns stay zero).
+    auto stage = [&](const T(&v)[R]) {
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < R; ++i) S.pt[c.row0 + i][lane + 1] = v[i];
+      __syncwarp();
+    };
+    // o = A v on my cells (LocalStencilOperator::apply, schwarz.hpp:146-159):
+    // o = unk * (d*v - vW - vE - vN - vS); block-external neighbours are
+    // ghost zeros.  v must have been staged.
+    auto apply = [&](const T(&v)[R], T vN0, T vS1, T(&o)[R]) {
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        T vW = __shfl_up_sync(0xffffffffu, v[i], 1);
-        T vE = __shfl_down_sync(0xffffffffu, v[i], 1);
-        if (lane == 0) vW = T(0);
-        if (lane == 31) vE = T(0);
+        const T vW = S.pt[c.row0 + i][lane];
+        const T vE = S.pt[c.row0 + i][lane + 2];
         const T vN = i > 0 ? v[i - 1] : vN0;
         const T vS = i + 1 < R ? v[i + 1] : vS1;
-        const T d = (i == iT) ? dT : ((i == iB) ? dB : dI);
+        T d;
+        if (FULL)
+          d = (i == 0) ? dFirst : ((i == R - 1) ? dLast : dI);
+        else
+          d = (i == iT) ? dT : ((i == iB) ? dB : dI);
         T t = fmaT(d, v[i], -vW);
         t = t - vE;
         t = t - vN;
         t = t - vS;
-        o[i] = (unk >> i) & 1u ? t : T(0);
+        o[i] = ((unk >> i) & 1u) ? t : T(0);
       }
     };
 
@@ -251,11 +330,17 @@ __global__ void __launch_bounds__(NW * 32) oras_sweep_kernel(SweepArgs<T> a) {
     T part = T(0);
 #pragma unroll
     for (int i = 0; i < R; ++i) part = fmaT(r[i], r[i], part);
-    T rr = cta_sum<T, NW>(part, S.red, 1, warp, lane);
+    T rr = cta_sum<T, NW>(part, S.red, 1, warp, lane);  // also orders the pt staging
     collect();
     nb_p[0] = nb_r[0];  // p = r initially
     nb_p[1] = nb_r[1];
     const T r0 = sqrt(rr);
+    // maybe_done = sqrt(rr_new) <= tol*r0 (cg.hpp:132); the sqrt is only
+    // evaluated inside a 1e-12 band around the threshold, outside it the
+    // squared comparison decides identically.
+    const T thr = a.ltol * r0;
+    const T thr2 = thr * thr;
+    const T thr2_lo = thr2 * T(1.0 - 1e-6), thr2_hi = thr2 * T(1.0 + 1e-6);
     converged = false;
     if (r0 == T(0)) {
       converged = true;
@@ -282,16 +367,18 @@ __global__ void __launch_bounds__(NW * 32) oras_sweep_kernel(SweepArgs<T> a) {
         T rr_new = cta_sum<T, NW>(part, S.red, 1, warp, lane);
         collect();
         const bool cadence = iter % a.lcheck == 0 || iter == a.lmax;
-        const bool maybe_done = sqrt(rr_new) <= a.ltol * r0;
+        bool maybe_done;
+        if (rr_new < thr2_lo) maybe_done = true;
+        else if (rr_new > thr2_hi) maybe_done = false;
+        else maybe_done = sqrt(rr_new) <= thr;
         if (cadence || maybe_done) {
           // True residual b - A x, then confirm or replace (cg.hpp:131-146).
+          stage(x);
           apply(x, nb_x[0], nb_x[1], q);
           part = T(0);
 #pragma unroll
           for (int i = 0; i < R; ++i) {
-            const int ly = row0 + i;
-            const T bv = (col_ok && ly < B) ? S.bs[ly][lx] : T(0);
-            q[i] = bv - q[i];
+            q[i] = S.bt[c.row0 + i][lane] - q[i];
             part = fmaT(q[i], q[i], part);
           }
           if (NW > 1) {
@@ -316,6 +403,7 @@ __global__ void __launch_bounds__(NW * 32) oras_sweep_kernel(SweepArgs<T> a) {
         const T beta = rr_new / rr;
 #pragma unroll
         for (int i = 0; i < R; ++i) p[i] = fmaT(beta, p[i], r[i]);
+        stage(p);
         nb_p[0] = fmaT(beta, nb_p[0], nb_r[0]);
         nb_p[1] = fmaT(beta, nb_p[1], nb_r[1]);
         rr = rr_new;
@@ -324,19 +412,21 @@ __global__ void __launch_bounds__(NW * 32) oras_sweep_kernel(SweepArgs<T> a) {
     }
   }
 
-  // ---- 4. accumulate_owned: u_new = u_old + v on the owned rectangle ----
+  // ---- accumulate_owned: u_new = u_old + v on the owned rectangle ----------
+  // v = CG solution at unknown cells, the residual b - u at known cells.
   const int ox0 = a.ax.owned_begin(bx), ox1 = a.ax.owned_end(bx);
   const int oy0 = a.ay.owned_begin(by), oy1 = a.ay.owned_end(by);
   T* __restrict__ un = a.u_new + plane;
-  if (col_ok && gx >= ox0 && gx < ox1) {
+  if (c.col_ok && c.gx >= ox0 && c.gx < ox1) {
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      const int ly = row0 + i;
-      const int gy = y0 + ly;
+      const int ly = c.row0 + i;
+      const int gy = c.y0 + ly;
       if (ly < B && gy >= oy0 && gy < oy1) {
-        // unknown cells take the CG solution, known cells keep the residual
-        const T v = ((unk >> i) & 1u) ? x[i] : S.rs[ly + 1][lx + 1];
-        un[static_cast<size_t>(gy) * W + gx] = S.us[ly + 1][lx + 1] + v;
+        const size_t pix = static_cast<size_t>(gy) * c.W + c.gx;
+        const T uo = c.u[pix];
+        const T v = ((unk >> i) & 1u) ? x[i] : c.b[pix] - uo;
+        un[pix] = uo + v;
       }
     }
   }

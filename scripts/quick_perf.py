@@ -15,4 +15,4 @@ for cfg, name in [(C1,'C1'),(C2,'C2'),(C3,'C3')]:
         r = s.run_method(si.Method.MultilevelOras, f, m, o)
         st = s.kernel_stats(reset=True); s.set_profiling(False)
         print(name, prec.name, 'levels', r.report.level_iterations, 'trace', [x.rel_residual for x in r.trace.rows], 'host ms', [round(t*1e3,1) for t in ts], 'cg its', r.report.local_cg_iterations, 'fails', r.report.local_failures)
-        print('   ', {k:(v['launches'], round(v['device_ms'],3)) for k,v in st.items()})
+        print('   ', {k:(v['launches'], round(v['device_ms'],3)) for k,v in st.items() if isinstance(v, dict)})
