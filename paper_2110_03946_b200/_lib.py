@@ -116,7 +116,7 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _build.LIB
+    return os.environ.get("SI_LIB_PATH") or _build.LIB
 
 
 def load(build_if_missing: bool = True):
@@ -128,10 +128,11 @@ def load(build_if_missing: bool = True):
         if build_if_missing and (not os.path.exists(_build.LIB) or
                                  os.environ.get("SI_REBUILD") == "1"):
             _build.build(force=os.environ.get("SI_REBUILD") == "1")
-        if not os.path.exists(_build.LIB):
-            raise RuntimeError(f"{_build.LIB} is missing: build it with "
+        path = lib_path()
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} is missing: build it with "
                                "`python -m paper_2110_03946_b200.build` (nvcc, sm_100a)")
-        lib = C.CDLL(_build.LIB)
+        lib = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

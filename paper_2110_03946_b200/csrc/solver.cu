@@ -104,7 +104,7 @@ struct si_ctx {
   std::vector<PendingEvent> pending;
   std::vector<cudaEvent_t> event_pool;
   si_kernel_stats stats{};
-  int sweep_nw64 = 4, sweep_nw32 = 2;           // warps per sweep CTA
+  int sweep_nw64 = 4, sweep_nw32 = 4;           // warps per sweep CTA
   long long launch_count = 0;                   // kernels launched (always counted)
 };
 

@@ -90,6 +90,26 @@ __device__ __forceinline__ T cta_sum(T v, T (*red)[NW], int slot, int warp, int 
   return s;
 }
 
+// Thread-local part of a dot product: two interleaved accumulators (even and
+// odd rows) halve the dependent-fma chain.
+template <typename T, int R>
+__device__ __forceinline__ T dot2(const T (&a)[R], const T (&b)[R]) {
+  T s0 = T(0), s1 = T(0);
+#pragma unroll
+  for (int i = 0; i < R; i += 2) {
+    s0 = fma(a[i], b[i], s0);
+    if (i + 1 < R) s1 = fma(a[i + 1], b[i + 1], s1);
+  }
+  return s0 + s1;
+}
+
+// sqrt(v) <= thr, evaluated out of line: the caller only needs it inside a
+// narrow band around thr^2, everywhere else the squared test is exact.
+template <typename T>
+__device__ __noinline__ bool band_sqrt_le(T v, T thr) {
+  return sqrt(v) <= thr;
+}
+
 // Per-thread view of the block: column lx, rows row0 .. row0+R-1.
 template <typename T, int R>
 struct Cell {
@@ -193,10 +213,16 @@ __device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, T (&rhs)[R], 
 
 // Resident CTAs per SM requested from ptxas (caps registers per thread):
 // the CG vectors need 4*R values of T per thread.
+#ifndef SI_OCC64
+#define SI_OCC64 4
+#endif
+#ifndef SI_OCC32
+#define SI_OCC32 6
+#endif
 template <typename T, int NW>
 struct SweepOcc {
-  static constexpr int value = sizeof(T) == 8 ? (NW == 4 ? 4 : (NW == 2 ? 3 : 1))
-                                              : (NW == 4 ? 6 : (NW == 2 ? 4 : 2));
+  static constexpr int value = sizeof(T) == 8 ? (NW == 4 ? SI_OCC64 : (NW == 2 ? 3 : 1))
+                                              : (NW == 4 ? SI_OCC32 : (NW == 2 ? 4 : 2));
 };
 
 // FULL: the block is exactly 32x32 (every level of any image >= 32 pixels
@@ -327,10 +353,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
     };
 
     publish();
-    T part = T(0);
-#pragma unroll
-    for (int i = 0; i < R; ++i) part = fmaT(r[i], r[i], part);
-    T rr = cta_sum<T, NW>(part, S.red, 1, warp, lane);  // also orders the pt staging
+    T rr = cta_sum<T, NW>(dot2<T, R>(r, r), S.red, 1, warp, lane);  // also orders the pt staging
     collect();
     nb_p[0] = nb_r[0];  // p = r initially
     nb_p[1] = nb_r[1];
@@ -345,42 +368,34 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
     if (r0 == T(0)) {
       converged = true;
     } else {
+      int until_check = a.lcheck;  // iter % lcheck == 0  <=>  countdown hits 0
       for (int iter = 1; iter <= a.lmax; ++iter) {
         apply(p, nb_p[0], nb_p[1], q);
-        part = T(0);
-#pragma unroll
-        for (int i = 0; i < R; ++i) part = fmaT(p[i], q[i], part);
-        const T pAp = cta_sum<T, NW>(part, S.red, 0, warp, lane);
+        const T pAp = cta_sum<T, NW>(dot2<T, R>(p, q), S.red, 0, warp, lane);
         if (!(pAp > T(0)) || !isfinite(pAp)) {  // breakdown (cg.hpp:120-125)
           iters = iter - 1;
           break;
         }
         const T alpha = rr / pAp;
-        part = T(0);
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           x[i] = fmaT(alpha, p[i], x[i]);
           r[i] = fmaT(-alpha, q[i], r[i]);
-          part = fmaT(r[i], r[i], part);
         }
         publish();
-        T rr_new = cta_sum<T, NW>(part, S.red, 1, warp, lane);
+        T rr_new = cta_sum<T, NW>(dot2<T, R>(r, r), S.red, 1, warp, lane);
         collect();
-        const bool cadence = iter % a.lcheck == 0 || iter == a.lmax;
-        bool maybe_done;
-        if (rr_new < thr2_lo) maybe_done = true;
-        else if (rr_new > thr2_hi) maybe_done = false;
-        else maybe_done = sqrt(rr_new) <= thr;
+        if (--until_check == 0) until_check = a.lcheck;
+        const bool cadence = until_check == a.lcheck || iter == a.lmax;
+        bool maybe_done = rr_new < thr2_lo;
+        if (rr_new >= thr2_lo && rr_new <= thr2_hi) maybe_done = band_sqrt_le(rr_new, thr);
         if (cadence || maybe_done) {
           // True residual b - A x, then confirm or replace (cg.hpp:131-146).
           stage(x);
           apply(x, nb_x[0], nb_x[1], q);
-          part = T(0);
 #pragma unroll
-          for (int i = 0; i < R; ++i) {
-            q[i] = S.bt[c.row0 + i][lane] - q[i];
-            part = fmaT(q[i], q[i], part);
-          }
+          for (int i = 0; i < R; ++i) q[i] = S.bt[c.row0 + i][lane] - q[i];
+          const T part = dot2<T, R>(q, q);
           if (NW > 1) {
             S.pubt[warp][0][lane] = q[0];
             S.pubt[warp][1][lane] = q[R - 1];
