@@ -12,9 +12,9 @@ namespace sib {
 constexpr int kRedThreads = 256;
 constexpr int kRedBlocksMax = 1184;  // 148 SMs x 8
 
-template <typename Term>
+// blk: this CTA's index among the nblk CTAs of its channel chn.
 __device__ void reduce_epilogue(double v, double* partials, double* out, unsigned int* ticket,
-                                int nblk, int nch) {
+                                int blk, int nblk, int chn, int nch) {
   __shared__ double wsum[kRedThreads / 32];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -24,9 +24,9 @@ __device__ void reduce_epilogue(double v, double* partials, double* out, unsigne
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 0; w < kRedThreads / 32; ++w) s += wsum[w];
-    partials[blockIdx.y * nblk + blockIdx.x] = s;
+    partials[chn * nblk + blk] = s;
     __threadfence();
-    const unsigned int total = gridDim.x * gridDim.y;
+    const unsigned int total = gridDim.x * gridDim.y * gridDim.z;
     last = atomicAdd(ticket, 1u) == total - 1;
   }
   __syncthreads();
@@ -50,40 +50,105 @@ __device__ void reduce_epilogue(double v, double* partials, double* out, unsigne
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
-struct NoTerm {};
-
 // K1: per channel sum of (b - A u)^2 (residual_into + vec::norm^2,
-// operators.hpp:38-66/91-97, cg.hpp:46-50).  mode 1: sum of b^2 (RhsNorm).
+// operators.hpp:38-66/91-97, cg.hpp:46-50); mode 1: sum of b^2 (RhsNorm).
+// Each warp walks a vertical strip of kResRows rows that is 32*V pixels
+// wide (V consecutive pixels per lane, vector loads when rows are aligned),
+// keeping the rows above and below in registers, so u is read from memory
+// once per pixel.  known_invariant: b is zero
+// at unknown pixels (the multilevel data flow), so it is only read where the
+// mask is set.
+constexpr int kResRows = 8;
+
+template <typename T>
+struct Pair {
+  T a, b;
+};
+
+template <typename T, bool VEC>
+__device__ __forceinline__ Pair<T> load_pair(const T* __restrict__ row, int x, int W) {
+  if (VEC) {
+    if (x + 1 < W) {
+      if constexpr (sizeof(T) == 8) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(row + x));
+        return {v.x, v.y};
+      } else {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(row + x));
+        return {v.x, v.y};
+      }
+    }
+  }
+  Pair<T> r{T(0), T(0)};
+  if (x < W) r.a = row[x];
+  if (x + 1 < W) r.b = row[x + 1];
+  return r;
+}
+
+// V consecutive values of one row starting at x (zero outside [0, W)).
+template <typename T, int V, bool VEC>
+__device__ __forceinline__ void load_run(const T* __restrict__ row, int x, int W, T (&v)[V]) {
+  if (VEC && x + V <= W) {
+#pragma unroll
+    for (int k = 0; k < V; k += 2) {
+      const Pair<T> p = load_pair<T, true>(row, x + k, W);
+      v[k] = p.a;
+      v[k + 1] = p.b;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < V; ++k) v[k] = (x + k < W) ? row[x + k] : T(0);
+  }
+}
+
+// Grid (x segments of kRedThreads pixels, row groups, channel); each CTA
+// walks rows y = blockIdx.y, y += gridDim.y.  No integer division per pixel;
+// the five stencil reads of u hit L1/L2 (DRAM sees u once).
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads)
     residual_sumsq_kernel(const uint8_t* __restrict__ mask, const T* __restrict__ u,
                           const T* __restrict__ b, int W, int H, size_t N, int mode,
-                          double* partials, double* out, unsigned int* ticket) {
-  const int c = blockIdx.y;
-  const T* uc = u + c * N;
-  const T* bc = b + c * N;
+                          int known_invariant, double* partials, double* out, unsigned int* ticket) {
+  const int c = blockIdx.z;
+  const T* __restrict__ uc = u + c * N;
+  const T* __restrict__ bc = b + c * N;
+  const int x = blockIdx.x * kRedThreads + threadIdx.x;
   double acc = 0.0;
-  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < N; i += stride) {
-    T r;
-    if (mode == 1) {
-      r = bc[i];
-    } else if (mask[i]) {
-      r = bc[i] - uc[i];
-    } else {
-      const int y = static_cast<int>(i / W), x = static_cast<int>(i - static_cast<size_t>(y) * W);
-      T sum = T(0);
-      int deg = 0;
-      if (x > 0) { sum += uc[i - 1]; ++deg; }
-      if (x + 1 < W) { sum += uc[i + 1]; ++deg; }
-      if (y > 0) { sum += uc[i - W]; ++deg; }
-      if (y + 1 < H) { sum += uc[i + W]; ++deg; }
-      r = bc[i] - fma(T(deg), uc[i], -sum);
+  if (x < W) {
+    const bool hw = x > 0, he = x + 1 < W;
+#pragma unroll 2
+    for (int y = blockIdx.y; y < H; y += gridDim.y) {
+      const size_t i = static_cast<size_t>(y) * W + x;
+      T r;
+      if (mode == 1) {
+        r = __ldg(bc + i);
+      } else {
+        const uint8_t m = __ldg(mask + i);
+        const T ctr = __ldg(uc + i);
+        const T vw = hw ? __ldg(uc + i - 1) : T(0);
+        const T ve = he ? __ldg(uc + i + 1) : T(0);
+        const T vn = y > 0 ? __ldg(uc + i - W) : T(0);
+        const T vs = y + 1 < H ? __ldg(uc + i + W) : T(0);
+        if (m) {
+          // invariant (multilevel data flow): u == b at known pixels, so the
+          // reference's b - u is exactly +0 there and b need not be read.
+          r = known_invariant ? T(0) : __ldg(bc + i) - ctr;
+        } else {
+          // operators.hpp:44-58: ((W + E) + N) + S over in-image neighbours
+          T sum = T(0);
+          int deg = 0;
+          if (hw) { sum += vw; ++deg; }
+          if (he) { sum += ve; ++deg; }
+          if (y > 0) { sum += vn; ++deg; }
+          if (y + 1 < H) { sum += vs; ++deg; }
+          r = (known_invariant ? T(0) : __ldg(bc + i)) - fma(T(deg), ctr, -sum);
+        }
+      }
+      const double rd = static_cast<double>(r);
+      acc = fma(rd, rd, acc);
     }
-    const double rd = static_cast<double>(r);
-    acc = fma(rd, rd, acc);
   }
-  reduce_epilogue<NoTerm>(acc, partials, out, ticket, gridDim.x, gridDim.y);
+  reduce_epilogue(acc, partials, out, ticket, blockIdx.y * gridDim.x + blockIdx.x,
+                  gridDim.x * gridDim.y, blockIdx.z, gridDim.z);
 }
 
 // K6: per channel sum of (255 u - 255 f)^2 (mse_per_channel, metrics.hpp:30-47).
@@ -98,7 +163,7 @@ __global__ void __launch_bounds__(kRedThreads)
     const double d = 255.0 * (static_cast<double>(u[c * N + i]) - f[c * N + i]);
     acc = fma(d, d, acc);
   }
-  reduce_epilogue<NoTerm>(acc, partials, out, ticket, gridDim.x, gridDim.y);
+  reduce_epilogue(acc, partials, out, ticket, blockIdx.x, gridDim.x, blockIdx.y, gridDim.y);
 }
 
 // K5: level-0 values = f at known pixels, 0 elsewhere (build_pyramid,
@@ -108,10 +173,24 @@ __global__ void ingest_kernel(const double* __restrict__ f, const uint8_t* __res
                               size_t N, int C, T* __restrict__ b, unsigned long long* known) {
   unsigned int cnt = 0;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < N; i += stride) {
-    const bool k = mask[i] != 0;
-    cnt += k;
-    for (int c = 0; c < C; ++c) b[c * N + i] = k ? static_cast<T>(f[c * N + i]) : T(0);
+  const size_t pairs = N / 2;
+  if (N % 2 == 0) {
+    for (size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < pairs; j += stride) {
+      const uchar2 m = reinterpret_cast<const uchar2*>(mask)[j];
+      cnt += (m.x != 0) + (m.y != 0);
+      for (int c = 0; c < C; ++c) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(f + c * N) + j);
+        T* dst = b + c * N + 2 * j;
+        dst[0] = m.x ? static_cast<T>(v.x) : T(0);
+        dst[1] = m.y ? static_cast<T>(v.y) : T(0);
+      }
+    }
+  } else {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < N; i += stride) {
+      const bool k = mask[i] != 0;
+      cnt += k;
+      for (int c = 0; c < C; ++c) b[c * N + i] = k ? static_cast<T>(f[c * N + i]) : T(0);
+    }
   }
   cnt = __reduce_add_sync(0xffffffffu, cnt);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(known, static_cast<unsigned long long>(cnt));
@@ -120,75 +199,146 @@ __global__ void ingest_kernel(const double* __restrict__ f, const uint8_t* __res
 // K3: restrict_level (multilevel.hpp:33-70): coarse pixel = clipped 2x2 fine
 // cell; known = OR; value = mean of known fine values (KnownOnly) or of all
 // of them (AllPixels), accumulated in row-major order like the reference.
-template <typename T>
+// One thread per coarse pixel; the two fine rows are read as pairs.
+template <typename T, bool VEC>
 __global__ void restrict_kernel(const uint8_t* __restrict__ fmask, const T* __restrict__ fval,
                                 int fw, int fh, int C, int averaging, uint8_t* __restrict__ cmask,
                                 T* __restrict__ cval) {
   const int cw = (fw + 1) / 2, ch = (fh + 1) / 2;
   const size_t fn = static_cast<size_t>(fw) * fh, cn = static_cast<size_t>(cw) * ch;
-  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-  for (size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cn; j += stride) {
-    const int cy = static_cast<int>(j / cw), cx = static_cast<int>(j - static_cast<size_t>(cy) * cw);
-    const int fx0 = 2 * cx, fy0 = 2 * cy;
-    const int fx1 = min(fx0 + 2, fw), fy1 = min(fy0 + 2, fh);
-    int known = 0, total = 0;
-    for (int y = fy0; y < fy1; ++y)
-      for (int x = fx0; x < fx1; ++x) {
-        known += fmask[static_cast<size_t>(y) * fw + x] != 0;
-        ++total;
-      }
-    cmask[j] = known ? 1 : 0;
-    for (int c = 0; c < C; ++c) {
-      T acc = T(0);
-      if (known) {
-        for (int y = fy0; y < fy1; ++y)
-          for (int x = fx0; x < fx1; ++x) {
-            const size_t i = static_cast<size_t>(y) * fw + x;
-            if (averaging == 0 && !fmask[i]) continue;
-            acc += fval[c * fn + i];
-          }
-        acc = acc / T(averaging == 0 ? known : total);
-      }
-      cval[c * cn + j] = acc;
+  const int cx = blockIdx.x * blockDim.x + threadIdx.x, cy = blockIdx.y;
+  if (cx >= cw) return;
+  const int fx0 = 2 * cx, fy0 = 2 * cy;
+  const bool two_x = fx0 + 1 < fw, two_y = fy0 + 1 < fh;
+  const size_t r0 = static_cast<size_t>(fy0) * fw + fx0, r1 = r0 + fw;
+  const bool k00 = fmask[r0] != 0, k01 = two_x && fmask[r0 + 1] != 0;
+  const bool k10 = two_y && fmask[r1] != 0, k11 = two_x && two_y && fmask[r1 + 1] != 0;
+  const int known = k00 + k01 + k10 + k11;
+  const int total = (1 + two_x) * (1 + two_y);
+  const size_t j = static_cast<size_t>(cy) * cw + cx;
+  cmask[j] = known ? 1 : 0;
+  for (int c = 0; c < C; ++c) {
+    T acc = T(0);
+    if (known) {
+      const T* v = fval + c * fn;
+      const Pair<T> a = load_pair<T, VEC>(v + static_cast<size_t>(fy0) * fw, fx0, fw);
+      Pair<T> bb{T(0), T(0)};
+      if (two_y) bb = load_pair<T, VEC>(v + static_cast<size_t>(fy0 + 1) * fw, fx0, fw);
+      const bool all = averaging != 0;
+      if (all || k00) acc += a.a;
+      if (two_x && (all || k01)) acc += a.b;
+      if (two_y && (all || k10)) acc += bb.a;
+      if (two_x && two_y && (all || k11)) acc += bb.b;
+      acc = acc / T(all ? total : known);
     }
+    cval[c * cn + j] = acc;
   }
 }
 
 // K4: prolongate (multilevel.hpp:101-128) + snap known fine pixels to their
 // data (multilevel.hpp:294-303): cell-centred bilinear, coordinate
-// 0.5*f - 0.25 clamped to the coarse grid.
+// 0.5*f - 0.25 clamped to the coarse grid.  One thread per horizontal pair
+// of fine pixels (they share coarse samples); coarse reads hit L1/L2.
 template <typename T>
-__global__ void prolong_snap_kernel(const T* __restrict__ coarse, int cw, int ch, int fw, int fh,
-                                    int C, const uint8_t* __restrict__ fmask,
-                                    const T* __restrict__ fval, T* __restrict__ fine) {
+__device__ __forceinline__ T prolong_px_unused(const T* __restrict__ cc, int cw, int ch, int fx, int fy) {
+  const double yc = fmin(fmax(0.5 * fy - 0.25, 0.0), static_cast<double>(ch - 1));
+  const double xc = fmin(fmax(0.5 * fx - 0.25, 0.0), static_cast<double>(cw - 1));
+  const int y0 = static_cast<int>(yc), x0 = static_cast<int>(xc);
+  const int y1 = min(y0 + 1, ch - 1), x1 = min(x0 + 1, cw - 1);
+  const T ty = static_cast<T>(yc - y0), tx = static_cast<T>(xc - x0);
+  const T v00 = __ldg(cc + static_cast<size_t>(y0) * cw + x0);
+  const T v01 = __ldg(cc + static_cast<size_t>(y0) * cw + x1);
+  const T v10 = __ldg(cc + static_cast<size_t>(y1) * cw + x0);
+  const T v11 = __ldg(cc + static_cast<size_t>(y1) * cw + x1);
+  // (1-ty)*((1-tx)*v00 + tx*v01) + ty*((1-tx)*v10 + tx*v11), with the
+  // contraction gcc -O3 applies to the reference expression
+  // (p*q + r*s -> fma(p, q, r*s); checked bitwise in the tests).
+  const T a0 = fma(T(1) - tx, v00, tx * v01);
+  const T a1 = fma(T(1) - tx, v10, tx * v11);
+  return fma(T(1) - ty, a0, ty * a1);
+}
+
+// Fine tile 64 x 16 per CTA (256 threads, a 2x2 quad each); the coarse
+// window it samples (34 x 10 per channel) is staged in shared memory.
+constexpr int kProX = 64, kProY = 16, kProCX = kProX / 2 + 2, kProCY = kProY / 2 + 2;
+
+template <typename T>
+__device__ __forceinline__ void prolong_axis(int f, int cn, double& t, int& i0, int& i1) {
+  const double c = fmin(fmax(0.5 * f - 0.25, 0.0), static_cast<double>(cn - 1));
+  i0 = static_cast<int>(c);
+  i1 = min(i0 + 1, cn - 1);
+  t = c - i0;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 4)
+    prolong_snap_kernel(const T* __restrict__ coarse, int cw, int ch, int fw, int fh, int C,
+                        const uint8_t* __restrict__ fmask, const T* __restrict__ fval,
+                        T* __restrict__ fine) {
+  constexpr int kCh = 4;  // channels staged per pass
+  __shared__ T tile[kCh][kProCY][kProCX];
   const size_t fn = static_cast<size_t>(fw) * fh, cn = static_cast<size_t>(cw) * ch;
-  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < fn; i += stride) {
-    const int fy = static_cast<int>(i / fw), fx = static_cast<int>(i - static_cast<size_t>(fy) * fw);
-    const bool snap = fmask != nullptr && fmask[i] != 0;
-    double yc = fmin(fmax(0.5 * fy - 0.25, 0.0), static_cast<double>(ch - 1));
-    double xc = fmin(fmax(0.5 * fx - 0.25, 0.0), static_cast<double>(cw - 1));
-    const int y0 = static_cast<int>(yc), x0 = static_cast<int>(xc);
-    const int y1 = min(y0 + 1, ch - 1), x1 = min(x0 + 1, cw - 1);
-    const T ty = static_cast<T>(yc - y0), tx = static_cast<T>(xc - x0);
-    for (int c = 0; c < C; ++c) {
-      T v;
-      if (snap) {
-        v = fval[c * fn + i];
-      } else {
-        const T* cc = coarse + c * cn;
-        const T v00 = cc[static_cast<size_t>(y0) * cw + x0];
-        const T v01 = cc[static_cast<size_t>(y0) * cw + x1];
-        const T v10 = cc[static_cast<size_t>(y1) * cw + x0];
-        const T v11 = cc[static_cast<size_t>(y1) * cw + x1];
-        // (1-ty)*((1-tx)*v00 + tx*v01) + ty*((1-tx)*v10 + tx*v11), with the
-        // contraction gcc -O3 applies to the reference expression
-        // (p*q + r*s -> fma(p, q, r*s); checked bitwise in the tests).
-        const T a0 = fma(T(1) - tx, v00, tx * v01);
-        const T a1 = fma(T(1) - tx, v10, tx * v11);
-        v = fma(T(1) - ty, a0, ty * a1);
+  const int fx0 = blockIdx.x * kProX, fy0 = blockIdx.y * kProY;
+  const int cx0 = fx0 / 2 - 1, cy0 = fy0 / 2 - 1;  // staged window origin
+  const int qx = threadIdx.x & 31, qy = threadIdx.x >> 5;
+  const int fxq = fx0 + 2 * qx, fyq = fy0 + 2 * qy;
+  // snap bits of my quad, loaded before the staging barrier
+  unsigned snap = 0;
+  if (fmask != nullptr) {
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx)
+        if (fyq + dy < fh && fxq + dx < fw && fmask[static_cast<size_t>(fyq + dy) * fw + fxq + dx])
+          snap |= 1u << (2 * dy + dx);
+  }
+  for (int c0 = 0; c0 < C; c0 += kCh) {
+    const int nc = min(kCh, C - c0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nc * kProCY * kProCX; i += blockDim.x) {
+      const int k = i / (kProCY * kProCX), rem = i - k * (kProCY * kProCX);
+      const int ly = rem / kProCX, lx = rem - ly * kProCX;
+      const int gy = min(max(cy0 + ly, 0), ch - 1), gx = min(max(cx0 + lx, 0), cw - 1);
+      tile[k][ly][lx] = __ldg(coarse + (c0 + k) * cn + static_cast<size_t>(gy) * cw + gx);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      const int fy = fyq + dy;
+      if (fy >= fh) continue;
+      double tyd;
+      int ya, yb;
+      prolong_axis<T>(fy, ch, tyd, ya, yb);
+      const T ty = static_cast<T>(tyd);
+      const int a0 = ya - cy0, a1 = yb - cy0;
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx) {
+        const int fx = fxq + dx;
+        if (fx >= fw) continue;
+        double txd;
+        int xa, xb;
+        prolong_axis<T>(fx, cw, txd, xa, xb);
+        const T tx = static_cast<T>(txd);
+        const int b0 = xa - cx0, b1 = xb - cx0;
+        const size_t i = static_cast<size_t>(fy) * fw + fx;
+        const bool s = (snap >> (2 * dy + dx)) & 1u;
+        for (int k = 0; k < nc; ++k) {
+          T v;
+          if (s) {
+            v = fval[(c0 + k) * fn + i];
+          } else {
+            const T v00 = tile[k][a0][b0], v01 = tile[k][a0][b1];
+            const T v10 = tile[k][a1][b0], v11 = tile[k][a1][b1];
+            // (1-ty)*((1-tx)*v00 + tx*v01) + ty*((1-tx)*v10 + tx*v11), with the
+            // contraction gcc -O3 applies to the reference expression
+            // (p*q + r*s -> fma(p, q, r*s); checked bitwise in the tests).
+            const T p0 = fma(T(1) - tx, v00, tx * v01);
+            const T p1 = fma(T(1) - tx, v10, tx * v11);
+            v = fma(T(1) - ty, p0, ty * p1);
+          }
+          fine[(c0 + k) * fn + i] = v;
+        }
       }
-      fine[c * fn + i] = v;
     }
   }
 }

@@ -176,14 +176,17 @@ int grid_for(size_t n, int threads, int cap) {
 // ---------------------------------------------------------------- launches
 template <typename T>
 void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W, int H, int C,
-                     int mode, double* out) {
+                     int mode, double* out, bool known_invariant = true) {
   const size_t N = static_cast<size_t>(W) * H;
-  const int g = grid_for(N, kRedThreads, kRedBlocksMax);
-  x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(g) * C);
+  const int gx = (W + kRedThreads - 1) / kRedThreads;
+  const int gy = std::max(1, std::min(H, (2 * kRedBlocksMax + gx * C - 1) / (gx * C)));
+  x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(gx) * gy * C);
   x.c.ticket.ensure(sizeof(unsigned int) * 4);
-  Timed t(x, K_RESIDUAL, static_cast<double>(N) * (C * sizeof(T) * (mode == 1 ? 1 : 2) + (mode == 1 ? 0 : 1)));
-  residual_sumsq_kernel<T><<<dim3(g, C), kRedThreads, 0, x.s>>>(
-      mask, u, b, W, H, N, mode, x.c.red_partials.as<double>(), out, x.c.ticket.as<unsigned int>());
+  // algorithmic bytes: u (or b) once per pixel per channel + the mask
+  Timed t(x, K_RESIDUAL, static_cast<double>(N) * (C * sizeof(T) + (mode == 1 ? 0 : 1)));
+  residual_sumsq_kernel<T><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
+      mask, u, b, W, H, N, mode, known_invariant ? 1 : 0, x.c.red_partials.as<double>(), out,
+      x.c.ticket.as<unsigned int>());
   CK(cudaGetLastError());
 }
 
@@ -195,6 +198,26 @@ void launch_sq_error(Ctx& x, const T* u, const double* f, size_t N, int C, doubl
   Timed t(x, K_METRIC, static_cast<double>(N) * C * (sizeof(T) + 8.0));
   sq_error_kernel<T><<<dim3(g, C), kRedThreads, 0, x.s>>>(
       u, f, N, x.c.red_partials.as<double>(), out, x.c.ticket.as<unsigned int>());
+  CK(cudaGetLastError());
+}
+
+template <typename T>
+void launch_restrict(Ctx& x, const uint8_t* fmask, const T* fval, int fw, int fh, int C,
+                     int averaging, uint8_t* cmask, T* cval) {
+  const int cw = (fw + 1) / 2, ch = (fh + 1) / 2;
+  const dim3 grid((cw + 127) / 128, ch);
+  if (fw % 2 == 0 && reinterpret_cast<uintptr_t>(fval) % 16 == 0)
+    restrict_kernel<T, true><<<grid, 128, 0, x.s>>>(fmask, fval, fw, fh, C, averaging, cmask, cval);
+  else
+    restrict_kernel<T, false><<<grid, 128, 0, x.s>>>(fmask, fval, fw, fh, C, averaging, cmask, cval);
+  CK(cudaGetLastError());
+}
+
+template <typename T>
+void launch_prolong(Ctx& x, const T* coarse, int cw, int ch, int fw, int fh, int C,
+                    const uint8_t* fmask, const T* fval, T* fine) {
+  const dim3 grid((fw + kProX - 1) / kProX, (fh + kProY - 1) / kProY);
+  prolong_snap_kernel<T><<<grid, 256, 0, x.s>>>(coarse, cw, ch, fw, fh, C, fmask, fval, fine);
   CK(cudaGetLastError());
 }
 
@@ -216,7 +239,7 @@ void launch_sweep_nw(Ctx& x, const SweepArgs<T>& a, int nblocks, int C) {
 template <typename T>
 void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_new, int W, int H,
                   int C, int block, int overlap, int flavour, double alpha, const LocalCfg& lc,
-                  bool b_known_only, unsigned long long* counters) {
+                  bool known_invariant, unsigned long long* counters) {
   if (block > kMaxBlock)
     fail(SI_ERR_UNSUPPORTED, "block size " + std::to_string(block) + " exceeds the supported 32");
   SweepArgs<T> a;
@@ -234,7 +257,7 @@ void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_
   a.ltol = static_cast<T>(lc.tol);
   a.lmax = lc.max_it;
   a.lcheck = lc.check;
-  a.b_known_only = b_known_only;
+  a.known_invariant = known_invariant;
   a.counters = counters;
   const int nblocks = a.ax.count * a.ay.count;
   const double bytes = static_cast<double>(a.N) * (2.0 * C * sizeof(T) + 1.0);
@@ -337,7 +360,7 @@ double joint_norm(const double* sums, int C) {
 template <typename T>
 LevelOutcome run_level(Ctx& x, LevelView<T>& L, int C, int block, int overlap, double* r0,
                        bool r0_pending, double tol, int flavour, const si_options& o,
-                       bool b_known_only, bool sink, const Trace& tr, const double* d_ref,
+                       bool known_invariant, bool sink, const Trace& tr, const double* d_ref,
                        si_report* rep) {
   LevelOutcome out;
   const size_t N = static_cast<size_t>(L.w) * L.h;
@@ -347,7 +370,7 @@ LevelOutcome run_level(Ctx& x, LevelView<T>& L, int C, int block, int overlap, d
   const Axis ax = Axis::make(L.w, block, overlap), ay = Axis::make(L.h, block, overlap);
   const long long nblocks = static_cast<long long>(ax.count) * ay.count;
   for (int outer = 0;; ++outer) {
-    launch_residual<T>(x, L.mask, L.u[L.cur], L.b, L.w, L.h, C, 0, d_out);
+    launch_residual<T>(x, L.mask, L.u[L.cur], L.b, L.w, L.h, C, 0, d_out, known_invariant);
     if (sink && d_ref) launch_sq_error<T>(x, L.u[L.cur], d_ref, N, C, d_out + 2 * C);
     CK(cudaMemcpyAsync(x.c.host_red, d_out, sizeof(double) * 3 * C, cudaMemcpyDeviceToHost, x.s));
     sync(x);
@@ -374,7 +397,7 @@ LevelOutcome run_level(Ctx& x, LevelView<T>& L, int C, int block, int overlap, d
     }
     const LocalCfg lc{o.local_tolerance, o.local_max_iterations, o.local_check_interval};
     launch_sweep<T>(x, L.mask, L.b, L.u[L.cur], L.u[L.cur ^ 1], L.w, L.h, C, block, overlap,
-                    flavour, o.alpha, lc, b_known_only, d_cnt);
+                    flavour, o.alpha, lc, known_invariant, d_cnt);
     L.cur ^= 1;
     rep->local_solves += nblocks * C;
   }
@@ -453,9 +476,8 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
   for (int l = 1; l < depth; ++l) {
     const size_t cn = static_cast<size_t>(lw[l]) * lh[l];
     Timed t(x, K_RESTRICT, static_cast<double>(cn) * 4.0 * (C * sizeof(T) + 1) + cn * (C * sizeof(T) + 1));
-    restrict_kernel<T><<<grid_for(cn, 256, 148 * 16), 256, 0, x.s>>>(
-        L[l - 1].mask, L[l - 1].b, lw[l - 1], lh[l - 1], C, o.averaging,
-        x.c.levels[l].mask.as<uint8_t>(), x.c.levels[l].b.as<T>());
+    launch_restrict<T>(x, L[l - 1].mask, L[l - 1].b, lw[l - 1], lh[l - 1], C, o.averaging,
+                       x.c.levels[l].mask.as<uint8_t>(), x.c.levels[l].b.as<T>());
     CK(cudaGetLastError());
   }
   bool known_checked = false;
@@ -498,8 +520,7 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
       LevelView<T>& F = L[level - 1];
       const size_t fn = static_cast<size_t>(F.w) * F.h;
       Timed t(x, K_PROLONG, static_cast<double>(fn) * (2.0 * C * sizeof(T) + 1.0) + n * C * sizeof(T));
-      prolong_snap_kernel<T><<<grid_for(fn, 256, 148 * 16), 256, 0, x.s>>>(
-          V.u[V.cur], V.w, V.h, F.w, F.h, C, F.mask, F.b, F.u[0]);
+      launch_prolong<T>(x, V.u[V.cur], V.w, V.h, F.w, F.h, C, F.mask, F.b, F.u[0]);
       CK(cudaGetLastError());
       F.cur = 0;
     }
@@ -907,7 +928,7 @@ si_status si_canonical_r0(si_ctx* ctx, const uint8_t* mask, int w, int h, int c,
     const uint8_t* d_m = upload(x, ctx->in_mask, mask, n);
     const double* d_b = upload(x, ctx->in_f, b, n * c);
     launch_residual<double>(x, d_m, d_b, d_b, w, h, c, normalizer == 1 ? 1 : 0,
-                            ctx->red_out.as<double>());
+                            ctx->red_out.as<double>(), false);
     download(x, ctx->host_red, ctx->red_out.ptr, c);
     *r0_norm = joint_norm(ctx->host_red, c);
   });
@@ -957,7 +978,7 @@ si_status si_residual_sumsq(si_ctx* ctx, const uint8_t* mask, int w, int h, int 
     const uint8_t* d_m = upload(x, ctx->in_mask, mask, n);
     const double* d_b = upload(x, ctx->in_f, b, n * c);
     const double* d_u = upload(x, ctx->aux, u, n * c);
-    launch_residual<double>(x, d_m, d_u, d_b, w, h, c, 0, ctx->red_out.as<double>());
+    launch_residual<double>(x, d_m, d_u, d_b, w, h, c, 0, ctx->red_out.as<double>(), false);
     download(x, sumsq, ctx->red_out.ptr, c);
   });
 }
@@ -977,8 +998,8 @@ si_status si_restrict_level(si_ctx* ctx, const uint8_t* mask, const double* valu
     const double* d_v = upload(x, ctx->in_f, values, n * c);
     ctx->out_img.ensure(cn * c * sizeof(double));
     ctx->aux.ensure(cn + 16);
-    restrict_kernel<double><<<grid_for(cn, 256, 148 * 16), 256, 0, x.s>>>(
-        d_m, d_v, w, h, c, averaging, ctx->aux.as<uint8_t>(), ctx->out_img.as<double>());
+    launch_restrict<double>(x, d_m, d_v, w, h, c, averaging, ctx->aux.as<uint8_t>(),
+                            ctx->out_img.as<double>());
     CK(cudaGetLastError());
     download(x, coarse_mask, ctx->aux.ptr, cn);
     download(x, coarse_values, ctx->out_img.ptr, cn * c);
@@ -997,8 +1018,7 @@ si_status si_prolongate(si_ctx* ctx, const double* coarse, int cw, int ch, int f
     const size_t fn = static_cast<size_t>(fw) * fh;
     const double* d_c = upload(x, ctx->in_f, coarse, static_cast<size_t>(cw) * ch);
     ctx->out_img.ensure(fn * sizeof(double));
-    prolong_snap_kernel<double><<<grid_for(fn, 256, 148 * 16), 256, 0, x.s>>>(
-        d_c, cw, ch, fw, fh, 1, nullptr, nullptr, ctx->out_img.as<double>());
+    launch_prolong<double>(x, d_c, cw, ch, fw, fh, 1, nullptr, nullptr, ctx->out_img.as<double>());
     CK(cudaGetLastError());
     download(x, fine, ctx->out_img.ptr, fn);
   });

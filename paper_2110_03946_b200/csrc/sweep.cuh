@@ -46,7 +46,8 @@ struct SweepArgs {
   T ltol;              // local CG tolerance
   int lmax;            // local CG max iterations
   int lcheck;          // true-residual cadence
-  int b_known_only;    // b is zero at unknown pixels: skip those loads
+  int known_invariant;    // multilevel invariant: b = 0 at unknown pixels and u = b at
+                       // known pixels (so r = 0 there); b is never read
   unsigned long long* counters;  // [0] failures, [1] CG iterations (may be null)
 };
 
@@ -118,7 +119,7 @@ struct Cell {
   const uint8_t* __restrict__ mask;
   const T* __restrict__ u;
   const T* __restrict__ b;
-  int b_known_only;
+  int known_invariant;
 };
 
 // Residual r = b - A u (operators.hpp:38-66, 91-97) of block rows
@@ -159,10 +160,10 @@ __device__ __forceinline__ void residual_rows(const Cell<T, R>& c, T (&r)[R + 2]
       const size_t p = static_cast<size_t>(gy) * c.W + c.gx;
       const bool known = c.mask[p] != 0;
       if (known) kbits |= 1ull << j;
-      const T bv = (known || !c.b_known_only) ? c.b[p] : T(0);
       if (known) {
-        rv = bv - uc[k];
+        rv = c.known_invariant ? T(0) : c.b[p] - uc[k];
       } else {
+        const T bv = c.known_invariant ? T(0) : c.b[p];
         T sum = T(0);
         int deg = 0;
         if (c.gx > 0) { sum += sW; ++deg; }
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
   c.mask = a.mask;
   c.u = a.u_old + plane;
   c.b = a.b + plane;
-  c.b_known_only = a.b_known_only;
+  c.known_invariant = a.known_invariant;
 
   T x[R], r[R], p[R], q[R];
   uint32_t unk;
@@ -440,7 +441,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
       if (ly < B && gy >= oy0 && gy < oy1) {
         const size_t pix = static_cast<size_t>(gy) * c.W + c.gx;
         const T uo = c.u[pix];
-        const T v = ((unk >> i) & 1u) ? x[i] : c.b[pix] - uo;
+        const T v = ((unk >> i) & 1u) ? x[i] : (c.known_invariant ? T(0) : c.b[pix] - uo);
         un[pix] = uo + v;
       }
     }
