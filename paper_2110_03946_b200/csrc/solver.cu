@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "sweep.cuh"
+#include "sweep_warp.cuh"
 
 using namespace sib;
 
@@ -106,6 +107,7 @@ struct si_ctx {
   si_kernel_stats stats{};
   int sweep_nw64 = 4, sweep_nw32 = 4;           // warps per sweep CTA
   long long launch_count = 0;                   // kernels launched (always counted)
+  int sweep_warp = 0;                           // 1: full blocks on the one-warp variant
 };
 
 namespace {
@@ -229,7 +231,9 @@ struct LocalCfg {
 
 template <typename T, int NW>
 void launch_sweep_nw(Ctx& x, const SweepArgs<T>& a, int nblocks, int C) {
-  if (a.ax.block == kMaxBlock)
+  if (a.ax.block == kMaxBlock && x.c.sweep_warp) {
+    oras_sweep_warp_kernel<T><<<dim3(nblocks, C), 32, 0, x.s>>>(a);
+  } else if (a.ax.block == kMaxBlock)
     oras_sweep_kernel<T, NW, true><<<dim3(nblocks, C), NW * 32, 0, x.s>>>(a);
   else
     oras_sweep_kernel<T, NW, false><<<dim3(nblocks, C), NW * 32, 0, x.s>>>(a);
@@ -681,6 +685,7 @@ si_status si_create(int device, si_ctx** out) {
       CK(cudaMallocHost(&c->host_cnt, sizeof(unsigned long long) * 8));
       if (const char* e = std::getenv("SI_SWEEP_WARPS64")) c->sweep_nw64 = std::atoi(e);
       if (const char* e = std::getenv("SI_SWEEP_WARPS32")) c->sweep_nw32 = std::atoi(e);
+      if (const char* e = std::getenv("SI_SWEEP_WARP")) c->sweep_warp = std::atoi(e);
     } catch (...) {
       si_destroy(c);
       throw;
