@@ -22,9 +22,7 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 
 import numpy as np
@@ -64,53 +62,63 @@ def frame_seeds(rank, j):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """SM clock and throttle reasons sampled through NVML during the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, period_s: float = 0.02):
         self.device = device
-        self.proc = None
-        self.path = None
+        self.period = period_s
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = None
+        self._thread = None
+        self.error = None
 
     def start(self):
-        fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.device]) if vis and vis.split(",")[0].isdigit() \
+                else self.device
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons",
+                                  getattr(pynvml, "nvmlDeviceGetCurrentClocksThrottleReasons", None))
+        except Exception as e:  # NVML unavailable: report, never fail the bench
+            self.error = str(e)[:120]
+            return
+        self._stop = threading.Event()
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    if get_reasons is not None:
+                        bits = get_reasons(h)
+                        for bit, name in self.REASONS.items():
+                            if bits & bit:
+                                self.reasons.add(name)
+                except Exception:
+                    pass
+                self._stop.wait(self.period)
+
+        self._thread = threading.Thread(target=run, daemon=True)
+        self._thread.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        os.unlink(self.path)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if self._thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None,
+                    "reasons": ["nvml unavailable: " + (self.error or "?")]}
+        self._stop.set()
+        self._thread.join()
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
 
 
 # ------------------------------------------------------------------ CPU legs
@@ -294,13 +302,14 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     achieved = (sw["algorithmic_bytes"] / (sw["device_ms"] / 1e3) / 1e9) if sw["device_ms"] else 0.0
-    traffic = None
+    traffic, traffic_alg = None, None
     tfile = os.path.join(ROOT, "profiles", "sweep_dram_traffic.json")
-    if os.path.exists(tfile):
+    if os.path.exists(tfile):  # one ncu --set full capture (scripts/summarize_profiles.py)
         try:
-            traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
+            tj = json.load(open(tfile))
+            traffic, traffic_alg = tj.get("dram_bytes_per_launch"), tj.get("algorithmic_bytes_per_launch")
         except ValueError:
-            traffic = None
+            pass
     total_dev = sum(v["device_ms"] for k, v in stats.items() if isinstance(v, dict))
     frame_bytes = sum(v["algorithmic_bytes"] for k, v in stats.items() if isinstance(v, dict))
 
@@ -317,6 +326,8 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "oras_sweep_kernel", "achieved": achieved,
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "traffic_launch": "finest-level sweep, ncu dram__bytes_read+write",
+                     "traffic_algorithmic": traffic_alg,
                      "frame_hbm_frac": (frame_bytes / args.steps) / (ms_per_step / 1e3) / 1e9 / peak,
                      "sweep_share_of_step": sw["device_ms"] / max(total_dev, 1e-9)},
         "e2e": {"value": e2e_value, "unit": "frames/s",
