@@ -130,6 +130,15 @@ si_status si_run_method_device(si_ctx* ctx, int method, const double* d_f, const
                                const double* d_reference, double* d_out, si_report* report,
                                si_trace_fn trace, void* user, void* stream);
 
+/* A batch of independent frames (BASELINE configs[3]): run_method on each of
+ * the n frames f[k]/mask[k] -> out[k] (host buffers, each w*h*c / w*h).  The
+ * host->device copy of frame k+1 and the device->host copy of frame k-1 run on
+ * their own streams while frame k is solved (pinned host buffers make them
+ * truly asynchronous).  reports: NULL or n entries. */
+si_status si_run_method_batch(si_ctx* ctx, int method, int n, const double* const* f,
+                              const uint8_t* const* mask, int w, int h, int c,
+                              const si_options* opt, double* const* out, si_report* reports);
+
 /* solve_schwarz(f, mask, partition_domain(w,h,block,overlap), options, reference)
  * (schwarz.hpp:349-389): single level on an explicit, unclamped partition.
  * flavour: si_flavour; host buffers. */

@@ -13,6 +13,6 @@ from .api import (  # noqa: F401
     SolverError, Subdomain, SubdomainPartition, TraceRow, Unsupported, canonical_r0,
     clamped_partition, default_solver, is_multilevel, kDefaultOrasAlpha, method_name,
     mse_per_channel, multilevel_solve, parse_method, partition_domain, psnr, random_mask,
-    run_method, run_schwarz_level, solve_schwarz, synthetic_test_image)
+    run_batch, run_method, run_schwarz_level, solve_schwarz, synthetic_test_image)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

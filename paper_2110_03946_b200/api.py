@@ -390,6 +390,30 @@ class Solver:
                                               C.byref(rep), cb, None, stream))
         return _report(rep)
 
+    def run_batch(self, method: Method, frames, options: Optional[RunOptions] = None,
+                  outputs=None) -> List[SolveResult]:
+        """run_method over a batch of independent frames [(ImageBuffer, InpaintingMask)]
+        with host<->device copies overlapped with the solves (si_run_method_batch).
+        outputs: optional list of preallocated (pinned) ImageBuffers."""
+        options = options or RunOptions()
+        n = len(frames)
+        if n == 0:
+            return []
+        f0 = frames[0][0]
+        for f, m in frames:
+            _require_same_grid(f, m)
+            if (f.width, f.height, f.channels) != (f0.width, f0.height, f0.channels):
+                raise InvalidArgument("run_batch: frames must share one shape")
+        outs = outputs or [ImageBuffer(f0.width, f0.height, f0.channels) for _ in range(n)]
+        fp = (C.c_void_p * n)(*[f.data.ctypes.data for f, _ in frames])
+        mp = (C.c_void_p * n)(*[m.known.ctypes.data for _, m in frames])
+        op = (C.c_void_p * n)(*[o.data.ctypes.data for o in outs])
+        reps = (L.si_report * n)()
+        o = options.to_c()
+        _check(self._lib.si_run_method_batch(self._h, int(method), n, fp, mp, f0.width, f0.height,
+                                             f0.channels, C.byref(o), op, reps))
+        return [SolveResult(outs[k], ConvergenceTrace(), _report(reps[k])) for k in range(n)]
+
     def solve_schwarz(self, f: ImageBuffer, mask: InpaintingMask, partition: SubdomainPartition,
                       options: Optional[SchwarzSolveOptions] = None,
                       reference: Optional[ImageBuffer] = None) -> SolveResult:
@@ -578,6 +602,10 @@ def run_method(method: Method, f: ImageBuffer, mask: InpaintingMask,
                options: Optional[RunOptions] = None,
                reference: Optional[ImageBuffer] = None) -> SolveResult:
     return default_solver().run_method(method, f, mask, options, reference)
+
+
+def run_batch(method: Method, frames, options: Optional[RunOptions] = None, outputs=None):
+    return default_solver().run_batch(method, frames, options, outputs)
 
 
 def multilevel_solve(f, mask, solver: LevelSolver, options=None, reference=None) -> SolveResult:

@@ -99,8 +99,13 @@ struct si_ctx {
   DevBuf in_f, in_mask, in_ref, out_img, aux;   // host-API staging
   DevBuf red_partials, red_out, counters;
   DevBuf ticket;
-  double* host_red = nullptr;                   // pinned, for the scalar D2H
-  unsigned long long* host_cnt = nullptr;       // pinned
+  // Scalars cross PCIe through mapped (zero-copy) pinned memory written by
+  // the kernels themselves: no copy-engine transfer that could queue behind a
+  // batch's 200 MB image copies on the same engine.
+  double* host_red = nullptr;                   // mapped host memory
+  double* dev_red = nullptr;                    // device alias of host_red
+  unsigned long long* host_cnt = nullptr;       // mapped host memory
+  unsigned long long* dev_cnt = nullptr;        // device alias of host_cnt
   int profiling = 0;
   std::vector<PendingEvent> pending;
   std::vector<cudaEvent_t> event_pool;
@@ -108,6 +113,11 @@ struct si_ctx {
   int sweep_nw64 = 4, sweep_nw32 = 4;           // warps per sweep CTA
   long long launch_count = 0;                   // kernels launched (always counted)
   int sweep_warp = 0;                           // 1: full blocks on the one-warp variant
+  // batch pipeline: two staging slots, one stream per copy direction
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  DevBuf slot_f[2], slot_mask[2], slot_out[2];
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_solved[2] = {nullptr, nullptr},
+              ev_d2h[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -368,7 +378,7 @@ LevelOutcome run_level(Ctx& x, LevelView<T>& L, int C, int block, int overlap, d
                        si_report* rep) {
   LevelOutcome out;
   const size_t N = static_cast<size_t>(L.w) * L.h;
-  double* d_out = x.c.red_out.as<double>();
+  double* d_out = x.c.dev_red;  // mapped: results land in host_red
   unsigned long long* d_cnt = x.c.counters.as<unsigned long long>();
   bool local_checked = false;
   const Axis ax = Axis::make(L.w, block, overlap), ay = Axis::make(L.h, block, overlap);
@@ -376,7 +386,6 @@ LevelOutcome run_level(Ctx& x, LevelView<T>& L, int C, int block, int overlap, d
   for (int outer = 0;; ++outer) {
     launch_residual<T>(x, L.mask, L.u[L.cur], L.b, L.w, L.h, C, 0, d_out, known_invariant);
     if (sink && d_ref) launch_sq_error<T>(x, L.u[L.cur], d_ref, N, C, d_out + 2 * C);
-    CK(cudaMemcpyAsync(x.c.host_red, d_out, sizeof(double) * 3 * C, cudaMemcpyDeviceToHost, x.s));
     sync(x);
     if (r0_pending) {
       *r0 = joint_norm(x.c.host_red + C, C);
@@ -411,19 +420,34 @@ LevelOutcome run_level(Ctx& x, LevelView<T>& L, int C, int block, int overlap, d
 template <typename T>
 void launch_r0(Ctx& x, const LevelView<T>& L, int C, int normalizer) {
   // canonical_r0 (schwarz.hpp:333-345): residual of u0 = b, or ||b||.
-  double* d_out = x.c.red_out.as<double>();
+  double* d_out = x.c.dev_red;
   launch_residual<T>(x, L.mask, L.b, L.b, L.w, L.h, C, normalizer == 1 ? 1 : 0, d_out + C);
+}
+
+__global__ void copy_u64_kernel(const unsigned long long* src, unsigned long long* dst, int n,
+                                bool zero_src) {
+  const int i = threadIdx.x;
+  if (i < n) {
+    if (dst) dst[i] = src[i];
+    if (zero_src) const_cast<unsigned long long*>(src)[i] = 0ull;
+  }
 }
 
 void begin_counters(Ctx& x) {
   x.c.counters.ensure(sizeof(unsigned long long) * 4);
-  CK(cudaMemsetAsync(x.c.counters.ptr, 0, sizeof(unsigned long long) * 4, x.s));
+  copy_u64_kernel<<<1, 32, 0, x.s>>>(x.c.counters.as<unsigned long long>(), nullptr, 4, true);
+  CK(cudaGetLastError());
+}
+
+// device counters -> mapped host memory, then wait
+void publish_counters(Ctx& x, int n) {
+  copy_u64_kernel<<<1, 32, 0, x.s>>>(x.c.counters.as<unsigned long long>(), x.c.dev_cnt, n, false);
+  CK(cudaGetLastError());
+  sync(x);
 }
 
 void end_counters(Ctx& x, si_report* rep) {
-  CK(cudaMemcpyAsync(x.c.host_cnt, x.c.counters.ptr, sizeof(unsigned long long) * 2,
-                     cudaMemcpyDeviceToHost, x.s));
-  sync(x);
+  publish_counters(x, 2);
   rep->local_failures += static_cast<long long>(x.c.host_cnt[0]);
   rep->local_cg_iterations += static_cast<long long>(x.c.host_cnt[1]);
 }
@@ -490,7 +514,8 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
     const size_t n = static_cast<size_t>(V.w) * V.h;
     if (level == depth - 1) {
       // canonical start u0 = b on the coarsest level (multilevel.hpp:267-273)
-      CK(cudaMemcpyAsync(V.u[0], V.b, n * C * sizeof(T), cudaMemcpyDeviceToDevice, x.s));
+      convert_kernel<T, T><<<grid_for(n * C, 256, 148 * 16), 256, 0, x.s>>>(V.b, V.u[0], n * C);
+      CK(cudaGetLastError());
       V.cur = 0;
     }
     const bool finest = level == 0;
@@ -502,9 +527,7 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
     if (!known_checked) {
       // build_rhs rejects an empty mask (operators.hpp:83): read the count
       // taken by the ingest kernel.
-      CK(cudaMemcpyAsync(x.c.host_cnt + 2, x.c.counters.as<unsigned long long>() + 2,
-                         sizeof(unsigned long long), cudaMemcpyDeviceToHost, x.s));
-      sync(x);
+      publish_counters(x, 3);
       check_arg(x.c.host_cnt[2] > 0, "build_rhs: mask has no known pixels");
       known_checked = true;
     }
@@ -681,8 +704,10 @@ si_status si_create(int device, si_ctx** out) {
     try {
       CK(cudaSetDevice(device));
       CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
-      CK(cudaMallocHost(&c->host_red, sizeof(double) * 256));
-      CK(cudaMallocHost(&c->host_cnt, sizeof(unsigned long long) * 8));
+      CK(cudaHostAlloc(&c->host_red, sizeof(double) * 256, cudaHostAllocMapped));
+      CK(cudaHostAlloc(&c->host_cnt, sizeof(unsigned long long) * 8, cudaHostAllocMapped));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dev_red), c->host_red, 0));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dev_cnt), c->host_cnt, 0));
       if (const char* e = std::getenv("SI_SWEEP_WARPS64")) c->sweep_nw64 = std::atoi(e);
       if (const char* e = std::getenv("SI_SWEEP_WARPS32")) c->sweep_nw32 = std::atoi(e);
       if (const char* e = std::getenv("SI_SWEEP_WARP")) c->sweep_warp = std::atoi(e);
@@ -712,6 +737,15 @@ void si_destroy(si_ctx* c) {
     cudaEventDestroy(p.stop);
   }
   for (auto e : c->event_pool) cudaEventDestroy(e);
+  for (int k = 0; k < 2; ++k) {
+    c->slot_f[k].release();
+    c->slot_mask[k].release();
+    c->slot_out[k].release();
+    for (cudaEvent_t e : {c->ev_h2d[k], c->ev_solved[k], c->ev_d2h[k]})
+      if (e) cudaEventDestroy(e);
+  }
+  if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
   if (c->host_red) cudaFreeHost(c->host_red);
   if (c->host_cnt) cudaFreeHost(c->host_cnt);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -787,6 +821,63 @@ si_status si_run_method(si_ctx* ctx, int method, const double* f, const uint8_t*
   });
   rep->elapsed_ms = ms_since(t0);
   return st;
+}
+
+si_status si_run_method_batch(si_ctx* ctx, int method, int n, const double* const* f,
+                              const uint8_t* const* mask, int w, int h, int c,
+                              const si_options* opt, double* const* out, si_report* reports) {
+  return guard([&] {
+    check_arg(ctx && f && mask && out && n >= 0, "null argument");
+    check_dims(w, h, c);
+    si_options o;
+    if (opt) o = *opt; else si_default_options(&o);
+    set_device(ctx);
+    if (!ctx->h2d_stream) {
+      CK(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+      for (int k = 0; k < 2; ++k) {
+        CK(cudaEventCreateWithFlags(&ctx->ev_h2d[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_solved[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_d2h[k], cudaEventDisableTiming));
+      }
+    }
+    const size_t n_px = static_cast<size_t>(w) * h, img = n_px * c * sizeof(double);
+    for (int k = 0; k < 2; ++k) {
+      ctx->slot_f[k].ensure(img);
+      ctx->slot_mask[k].ensure(n_px);
+      ctx->slot_out[k].ensure(img);
+    }
+    auto h2d = [&](int k) {
+      const int s = k & 1;
+      CK(cudaMemcpyAsync(ctx->slot_f[s].ptr, f[k], img, cudaMemcpyHostToDevice, ctx->h2d_stream));
+      CK(cudaMemcpyAsync(ctx->slot_mask[s].ptr, mask[k], n_px, cudaMemcpyHostToDevice,
+                         ctx->h2d_stream));
+      CK(cudaEventRecord(ctx->ev_h2d[s], ctx->h2d_stream));
+    };
+    cudaStream_t cs = ctx->own_stream;
+    if (n > 0) h2d(0);
+    for (int k = 0; k < n; ++k) {
+      const int s = k & 1;
+      // the other slot's input was consumed by frame k-1 (solved synchronously)
+      if (k + 1 < n) h2d(k + 1);
+      CK(cudaStreamWaitEvent(cs, ctx->ev_h2d[s], 0));
+      if (k >= 2) CK(cudaStreamWaitEvent(cs, ctx->ev_d2h[s], 0));  // out slot free again
+      si_report local;
+      si_report* rep = reports ? &reports[k] : &local;
+      clear_report(rep);
+      const auto t0 = Clock::now();
+      run_device(ctx, method, ctx->slot_f[s].as<double>(), ctx->slot_mask[s].as<uint8_t>(), w, h,
+                 c, o, nullptr, ctx->slot_out[s].as<double>(), rep, nullptr, nullptr, cs, t0);
+      rep->elapsed_ms = ms_since(t0);
+      CK(cudaEventRecord(ctx->ev_solved[s], cs));
+      CK(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_solved[s], 0));
+      CK(cudaMemcpyAsync(out[k], ctx->slot_out[s].ptr, img, cudaMemcpyDeviceToHost,
+                         ctx->d2h_stream));
+      CK(cudaEventRecord(ctx->ev_d2h[s], ctx->d2h_stream));
+    }
+    CK(cudaStreamSynchronize(ctx->d2h_stream));
+    CK(cudaStreamSynchronize(ctx->h2d_stream));
+  });
 }
 
 }  // extern "C"
@@ -932,9 +1023,9 @@ si_status si_canonical_r0(si_ctx* ctx, const uint8_t* mask, int w, int h, int c,
     const size_t n = static_cast<size_t>(w) * h;
     const uint8_t* d_m = upload(x, ctx->in_mask, mask, n);
     const double* d_b = upload(x, ctx->in_f, b, n * c);
-    launch_residual<double>(x, d_m, d_b, d_b, w, h, c, normalizer == 1 ? 1 : 0,
-                            ctx->red_out.as<double>(), false);
-    download(x, ctx->host_red, ctx->red_out.ptr, c);
+    launch_residual<double>(x, d_m, d_b, d_b, w, h, c, normalizer == 1 ? 1 : 0, ctx->dev_red,
+                            false);
+    sync(x);
     *r0_norm = joint_norm(ctx->host_red, c);
   });
 }
@@ -965,7 +1056,7 @@ si_status si_schwarz_sweep(si_ctx* ctx, const uint8_t* mask, int w, int h, int c
                          overlap, flavour, o.alpha, lc, false,
                          ctx->counters.as<unsigned long long>());
     download(x, u_new, lb.u1.ptr, n * c);
-    download(x, ctx->host_cnt, ctx->counters.ptr, 2);
+    publish_counters(x, 2);
     if (failures) *failures = static_cast<long long>(ctx->host_cnt[0]);
     if (cg_iterations) *cg_iterations = static_cast<long long>(ctx->host_cnt[1]);
   });
@@ -983,8 +1074,9 @@ si_status si_residual_sumsq(si_ctx* ctx, const uint8_t* mask, int w, int h, int 
     const uint8_t* d_m = upload(x, ctx->in_mask, mask, n);
     const double* d_b = upload(x, ctx->in_f, b, n * c);
     const double* d_u = upload(x, ctx->aux, u, n * c);
-    launch_residual<double>(x, d_m, d_u, d_b, w, h, c, 0, ctx->red_out.as<double>(), false);
-    download(x, sumsq, ctx->red_out.ptr, c);
+    launch_residual<double>(x, d_m, d_u, d_b, w, h, c, 0, ctx->dev_red, false);
+    sync(x);
+    std::memcpy(sumsq, ctx->host_red, sizeof(double) * c);
   });
 }
 

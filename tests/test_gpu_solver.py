@@ -291,3 +291,15 @@ def test_non_convergence_is_reported_not_raised(solver):
                                                                max_outer_iterations=2))
     assert not res.report.converged and res.report.iterations == 2
     assert "did not converge" in res.report.diagnostic
+
+
+def test_batch_equals_individual_solves(solver):
+    """si_run_method_batch (overlapped copies) == run_method frame by frame, bitwise."""
+    frames = [random_instance(96, 64, 0.05, 3, 300 + k) for k in range(5)]
+    o = si.RunOptions(levels=2)
+    batch = solver.run_batch(si.Method.MultilevelOras, frames, o)
+    for (f, m), b in zip(frames, batch):
+        single = solver.run_method(si.Method.MultilevelOras, f, m, o)
+        assert np.array_equal(single.image.data, b.image.data)
+        assert single.report.level_iterations == b.report.level_iterations
+        assert b.report.converged
