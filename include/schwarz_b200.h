@@ -182,6 +182,48 @@ si_status si_local_operator_apply(si_ctx* ctx, const uint8_t* mask, int w, int h
                                   int overlap, int index, int flavour, double alpha,
                                   const double* v, double* out);
 
+/* ---- device building blocks for distributed (stripe) solves ---------------
+ * One very large image split into horizontal stripes across ranks
+ * (SURVEY.md §8e): every rank keeps full-size buffers but only computes its
+ * stripe; the caller moves halo rows and all-reduces the partial norms.
+ * All image pointers are DEVICE memory of ctx's device in the planar layout;
+ * `precision` selects the element type of b/u/values buffers (si_precision:
+ * double or float); d_f is always double.  Work runs on `stream` (NULL = the
+ * context's own) and is complete when the call returns. */
+
+/* level 0: b = f at known pixels, 0 elsewhere (multilevel.hpp:84-88); *known
+ * receives the known-pixel count. */
+si_status si_device_ingest(si_ctx* ctx, const double* d_f, const uint8_t* d_mask, int w, int h,
+                           int c, int precision, void* d_b, long long* known, void* stream);
+/* restrict_level (multilevel.hpp:33-70) on device buffers. */
+si_status si_device_restrict(si_ctx* ctx, const uint8_t* d_mask, const void* d_values, int w, int h,
+                             int c, int averaging, int precision, uint8_t* d_cmask,
+                             void* d_cvalues, void* stream);
+/* prolongate + snap (multilevel.hpp:101-128, 294-303): full fine image. */
+si_status si_device_prolong_snap(si_ctx* ctx, const void* d_coarse, int cw, int ch, int fw, int fh,
+                                 int c, const uint8_t* d_fmask, const void* d_fvalues,
+                                 int precision, void* d_fine, void* stream);
+/* per-channel sum of (b - A u)^2 over rows [row0, row1) (mode 0), or of b^2
+ * (mode 1, RhsNorm); sums: host array of c doubles.  known_invariant: 1 when
+ * u == b at known pixels and b == 0 at unknown ones (the multilevel flow). */
+si_status si_device_residual_rows(si_ctx* ctx, const uint8_t* d_mask, const void* d_u,
+                                  const void* d_b, int w, int h, int c, int row0, int row1,
+                                  int mode, int known_invariant, int precision, double* sums,
+                                  void* stream);
+/* One ORAS/RAS sweep restricted to block rows [by0, by1) of
+ * partition_domain(w, h, block, overlap): u_new is written on the owned
+ * rectangles of those blocks only.  Counters may be NULL. */
+si_status si_device_sweep_rows(si_ctx* ctx, const uint8_t* d_mask, const void* d_b,
+                               const void* d_u_old, void* d_u_new, int w, int h, int c,
+                               int block_size, int overlap, int by0, int by1, int flavour,
+                               const si_options* opt, int known_invariant, long long* failures,
+                               long long* cg_iterations, void* stream);
+/* Stripe geometry of one level for `rank` of `world` (host only).  out[8]:
+ * blocks_y, k0, k1 (block rows), own_lo, own_hi (pixel rows this rank owns),
+ * win_lo, win_hi (rows it must hold: sweep windows + residual stencil),
+ * valid (1 when every halo row is owned by rank-1 or rank+1). */
+si_status si_stripe_plan(int h, int block_size, int overlap, int world, int rank, int* out);
+
 /* ---- host-only helpers (no device needed) -------------------------------- */
 
 /* partition_domain (partition.hpp:67-106).  rects receives 8 ints per block:
@@ -192,6 +234,9 @@ si_status si_partition_domain(int w, int h, int block_size, int overlap, int* bl
  * the reference's seeded input generators (libstdc++ <random>). */
 si_status si_synthetic_test_image(int w, int h, int c, uint64_t seed, double* out);
 si_status si_random_mask(int w, int h, double density, uint64_t seed, uint8_t* out);
+/* sqrt(sum_c sqrt(sumsq[c])^2): the joint residual norm of run_schwarz_level
+ * (schwarz.hpp:290-295, accumulate contracted to an fma as in the gcc build). */
+double si_joint_norm(const double* sumsq, int c);
 /* mse_per_channel / psnr (metrics.hpp:30-56) on host buffers. */
 si_status si_psnr(const double* u, const double* f, int w, int h, int c, double* psnr_db);
 

@@ -103,9 +103,18 @@ SIGNATURES = {
     "si_restrict_level": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
     "si_prolongate": (_i, [_vp, _vp, _i, _i, _i, _i, _vp]),
     "si_local_operator_apply": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _i, _d, _vp, _vp]),
+    "si_device_ingest": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _llp, _vp]),
+    "si_device_restrict": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp]),
+    "si_device_prolong_snap": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp]),
+    "si_device_residual_rows": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _dp,
+                                     _vp]),
+    "si_device_sweep_rows": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i,
+                                  C.POINTER(si_options), _i, _llp, _llp, _vp]),
+    "si_stripe_plan": (_i, [_i, _i, _i, _i, _i, _ip]),
     "si_partition_domain": (_i, [_i, _i, _i, _i, _ip, _ip, _ip, _i]),
     "si_synthetic_test_image": (_i, [_i, _i, _i, C.c_uint64, _vp]),
     "si_random_mask": (_i, [_i, _i, _d, C.c_uint64, _vp]),
+    "si_joint_norm": (_d, [_dp, _i]),
     "si_psnr": (_i, [_vp, _vp, _i, _i, _i, _dp]),
     "si_set_profiling": (_i, [_vp, _i]),
     "si_get_kernel_stats": (_i, [_vp, C.POINTER(si_kernel_stats), _i]),

@@ -107,7 +107,10 @@ template <typename T>
 __global__ void __launch_bounds__(kRedThreads)
     residual_sumsq_kernel(const uint8_t* __restrict__ mask, const T* __restrict__ u,
                           const T* __restrict__ b, int W, int H, size_t N, int mode,
-                          int known_invariant, double* partials, double* out, unsigned int* ticket) {
+                          int known_invariant, int row0, int row1, double* partials, double* out,
+                          unsigned int* ticket) {
+  // rows [row0, row1) only (stripe mode); the stencil still sees rows
+  // row0-1 and row1 as neighbours.
   const int c = blockIdx.z;
   const T* __restrict__ uc = u + c * N;
   const T* __restrict__ bc = b + c * N;
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(kRedThreads)
   if (x < W) {
     const bool hw = x > 0, he = x + 1 < W;
 #pragma unroll 2
-    for (int y = blockIdx.y; y < H; y += gridDim.y) {
+    for (int y = row0 + static_cast<int>(blockIdx.y); y < row1; y += gridDim.y) {
       const size_t i = static_cast<size_t>(y) * W + x;
       T r;
       if (mode == 1) {

@@ -188,17 +188,21 @@ int grid_for(size_t n, int threads, int cap) {
 // ---------------------------------------------------------------- launches
 template <typename T>
 void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W, int H, int C,
-                     int mode, double* out, bool known_invariant = true) {
+                     int mode, double* out, bool known_invariant = true, int row0 = 0,
+                     int row1 = -1) {
+  if (row1 < 0) row1 = H;
   const size_t N = static_cast<size_t>(W) * H;
+  const int rows = std::max(1, row1 - row0);
   const int gx = (W + kRedThreads - 1) / kRedThreads;
-  const int gy = std::max(1, std::min(H, (2 * kRedBlocksMax + gx * C - 1) / (gx * C)));
+  const int gy = std::max(1, std::min(rows, (2 * kRedBlocksMax + gx * C - 1) / (gx * C)));
   x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(gx) * gy * C);
   x.c.ticket.ensure(sizeof(unsigned int) * 4);
   // algorithmic bytes: u (or b) once per pixel per channel + the mask
-  Timed t(x, K_RESIDUAL, static_cast<double>(N) * (C * sizeof(T) + (mode == 1 ? 0 : 1)));
+  Timed t(x, K_RESIDUAL,
+          static_cast<double>(W) * std::max(0, row1 - row0) * (C * sizeof(T) + (mode == 1 ? 0 : 1)));
   residual_sumsq_kernel<T><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
-      mask, u, b, W, H, N, mode, known_invariant ? 1 : 0, x.c.red_partials.as<double>(), out,
-      x.c.ticket.as<unsigned int>());
+      mask, u, b, W, H, N, mode, known_invariant ? 1 : 0, row0, row1,
+      x.c.red_partials.as<double>(), out, x.c.ticket.as<unsigned int>());
   CK(cudaGetLastError());
 }
 
@@ -253,7 +257,7 @@ void launch_sweep_nw(Ctx& x, const SweepArgs<T>& a, int nblocks, int C) {
 template <typename T>
 void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_new, int W, int H,
                   int C, int block, int overlap, int flavour, double alpha, const LocalCfg& lc,
-                  bool known_invariant, unsigned long long* counters) {
+                  bool known_invariant, unsigned long long* counters, int by0 = 0, int by1 = -1) {
   if (block > kMaxBlock)
     fail(SI_ERR_UNSUPPORTED, "block size " + std::to_string(block) + " exceeds the supported 32");
   SweepArgs<T> a;
@@ -273,8 +277,12 @@ void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_
   a.lcheck = lc.check;
   a.known_invariant = known_invariant;
   a.counters = counters;
-  const int nblocks = a.ax.count * a.ay.count;
-  const double bytes = static_cast<double>(a.N) * (2.0 * C * sizeof(T) + 1.0);
+  if (by1 < 0) by1 = a.ay.count;
+  a.by0 = by0;
+  const int nblocks = a.ax.count * (by1 - by0);
+  if (nblocks <= 0) return;
+  const double bytes = static_cast<double>(a.N) * (2.0 * C * sizeof(T) + 1.0) * (by1 - by0) /
+                       a.ay.count;
   Timed t(x, K_SWEEP, bytes);
   const int nw = sizeof(T) == 8 ? x.c.sweep_nw64 : x.c.sweep_nw32;
   if constexpr (sizeof(T) == 8) {
@@ -1146,6 +1154,176 @@ si_status si_local_operator_apply(si_ctx* ctx, const uint8_t* mask, int w, int h
   });
 }
 
+namespace {
+struct StripeGeom {
+  int nby, k0, k1, own_lo, own_hi, win_lo, win_hi;
+};
+
+StripeGeom stripe_geom(int h, int block, int overlap, int world, int rank) {
+  const Axis ay = Axis::make(h, block, overlap);
+  StripeGeom g;
+  g.nby = ay.count;
+  g.k0 = static_cast<int>(static_cast<long long>(rank) * ay.count / world);
+  g.k1 = static_cast<int>(static_cast<long long>(rank + 1) * ay.count / world);
+  if (g.k0 == g.k1) {
+    g.own_lo = g.own_hi = g.k0 < ay.count ? ay.owned_begin(g.k0) : h;
+    g.win_lo = g.win_hi = g.own_lo;
+    return g;
+  }
+  g.own_lo = ay.owned_begin(g.k0);
+  g.own_hi = ay.owned_end(g.k1 - 1);
+  // rows read by the sweeps of blocks k0..k1-1 (block window + residual ring)
+  // and by the residual stencil of the owned rows
+  g.win_lo = std::max(0, std::min(ay.anchor(g.k0) - 1, g.own_lo - 1));
+  g.win_hi = std::min(h, std::max(ay.anchor(g.k1 - 1) + block + 1, g.own_hi + 1));
+  return g;
+}
+}  // namespace
+
+si_status si_stripe_plan(int h, int block_size, int overlap, int world, int rank, int* out) {
+  return guard([&] {
+    check_arg(out != nullptr, "null argument");
+    check_arg(world >= 1 && rank >= 0 && rank < world, "stripe plan: invalid world/rank");
+    validate_partition(h, h, block_size, overlap);
+    const StripeGeom g = stripe_geom(h, block_size, overlap, world, rank);
+    bool valid = true;
+    if (g.k0 < g.k1) {
+      if (g.win_lo < g.own_lo) {  // halo above must be owned by rank-1
+        const StripeGeom up = stripe_geom(h, block_size, overlap, world, rank - 1);
+        valid &= rank > 0 && up.k0 < up.k1 && up.own_lo <= g.win_lo;
+      }
+      if (g.win_hi > g.own_hi) {
+        const StripeGeom dn = stripe_geom(h, block_size, overlap, world, rank + 1);
+        valid &= rank + 1 < world && dn.k0 < dn.k1 && dn.own_hi >= g.win_hi;
+      }
+    }
+    const int v[8] = {g.nby, g.k0, g.k1, g.own_lo, g.own_hi, g.win_lo, g.win_hi, valid ? 1 : 0};
+    std::memcpy(out, v, sizeof v);
+  });
+}
+
+si_status si_device_ingest(si_ctx* ctx, const double* d_f, const uint8_t* d_mask, int w, int h,
+                           int c, int precision, void* d_b, long long* known, void* stream) {
+  return guard([&] {
+    check_arg(ctx && d_f && d_mask && d_b, "null argument");
+    check_dims(w, h, c);
+    set_device(ctx);
+    Ctx x{*ctx, pick_stream(ctx, stream)};
+    begin_counters(x);
+    const size_t n = static_cast<size_t>(w) * h;
+    if (precision == SI_PRECISION_FP32)
+      ingest_kernel<float><<<grid_for(n, 256, 148 * 16), 256, 0, x.s>>>(
+          d_f, d_mask, n, c, static_cast<float*>(d_b), ctx->counters.as<unsigned long long>() + 2);
+    else
+      ingest_kernel<double><<<grid_for(n, 256, 148 * 16), 256, 0, x.s>>>(
+          d_f, d_mask, n, c, static_cast<double*>(d_b), ctx->counters.as<unsigned long long>() + 2);
+    CK(cudaGetLastError());
+    publish_counters(x, 3);
+    if (known) *known = static_cast<long long>(ctx->host_cnt[2]);
+  });
+}
+
+si_status si_device_restrict(si_ctx* ctx, const uint8_t* d_mask, const void* d_values, int w, int h,
+                             int c, int averaging, int precision, uint8_t* d_cmask,
+                             void* d_cvalues, void* stream) {
+  return guard([&] {
+    check_arg(ctx && d_mask && d_values && d_cmask && d_cvalues, "null argument");
+    check_dims(w, h, c);
+    check_arg(w >= 2 && h >= 2, "restrict_level: fine grid must be at least 2x2");
+    set_device(ctx);
+    Ctx x{*ctx, pick_stream(ctx, stream)};
+    if (precision == SI_PRECISION_FP32)
+      launch_restrict<float>(x, d_mask, static_cast<const float*>(d_values), w, h, c, averaging,
+                             d_cmask, static_cast<float*>(d_cvalues));
+    else
+      launch_restrict<double>(x, d_mask, static_cast<const double*>(d_values), w, h, c, averaging,
+                              d_cmask, static_cast<double*>(d_cvalues));
+    sync(x);
+  });
+}
+
+si_status si_device_prolong_snap(si_ctx* ctx, const void* d_coarse, int cw, int ch, int fw, int fh,
+                                 int c, const uint8_t* d_fmask, const void* d_fvalues,
+                                 int precision, void* d_fine, void* stream) {
+  return guard([&] {
+    check_arg(ctx && d_coarse && d_fine, "null argument");
+    check_arg(cw == (fw + 1) / 2 && ch == (fh + 1) / 2,
+              "prolongate: coarse grid is not the dyadic parent of the fine grid");
+    set_device(ctx);
+    Ctx x{*ctx, pick_stream(ctx, stream)};
+    if (precision == SI_PRECISION_FP32)
+      launch_prolong<float>(x, static_cast<const float*>(d_coarse), cw, ch, fw, fh, c, d_fmask,
+                            static_cast<const float*>(d_fvalues), static_cast<float*>(d_fine));
+    else
+      launch_prolong<double>(x, static_cast<const double*>(d_coarse), cw, ch, fw, fh, c, d_fmask,
+                             static_cast<const double*>(d_fvalues), static_cast<double*>(d_fine));
+    sync(x);
+  });
+}
+
+si_status si_device_residual_rows(si_ctx* ctx, const uint8_t* d_mask, const void* d_u,
+                                  const void* d_b, int w, int h, int c, int row0, int row1,
+                                  int mode, int known_invariant, int precision, double* sums,
+                                  void* stream) {
+  return guard([&] {
+    check_arg(ctx && d_mask && d_u && d_b && sums, "null argument");
+    check_dims(w, h, c);
+    check_arg(0 <= row0 && row0 <= row1 && row1 <= h, "residual rows out of range");
+    set_device(ctx);
+    Ctx x{*ctx, pick_stream(ctx, stream)};
+    prepare_red(x, c);
+    if (row0 == row1) {
+      for (int k = 0; k < c; ++k) sums[k] = 0.0;
+      return;
+    }
+    if (precision == SI_PRECISION_FP32)
+      launch_residual<float>(x, d_mask, static_cast<const float*>(d_u),
+                             static_cast<const float*>(d_b), w, h, c, mode, ctx->dev_red,
+                             known_invariant != 0, row0, row1);
+    else
+      launch_residual<double>(x, d_mask, static_cast<const double*>(d_u),
+                              static_cast<const double*>(d_b), w, h, c, mode, ctx->dev_red,
+                              known_invariant != 0, row0, row1);
+    sync(x);
+    std::memcpy(sums, ctx->host_red, sizeof(double) * c);
+  });
+}
+
+si_status si_device_sweep_rows(si_ctx* ctx, const uint8_t* d_mask, const void* d_b,
+                               const void* d_u_old, void* d_u_new, int w, int h, int c,
+                               int block_size, int overlap, int by0, int by1, int flavour,
+                               const si_options* opt, int known_invariant, long long* failures,
+                               long long* cg_iterations, void* stream) {
+  return guard([&] {
+    check_arg(ctx && d_mask && d_b && d_u_old && d_u_new, "null argument");
+    check_dims(w, h, c);
+    validate_partition(w, h, block_size, overlap);
+    const Axis ay = Axis::make(h, block_size, overlap);
+    check_arg(0 <= by0 && by0 <= by1 && by1 <= ay.count, "sweep: block rows out of range");
+    const si_options o = opts_or_default(opt);
+    validate_local(o);
+    if (flavour == SI_FLAVOUR_ORAS)
+      check_arg(std::isfinite(o.alpha), "run_schwarz_level: alpha must be finite");
+    set_device(ctx);
+    Ctx x{*ctx, pick_stream(ctx, stream)};
+    begin_counters(x);
+    const LocalCfg lc{o.local_tolerance, o.local_max_iterations, o.local_check_interval};
+    if (o.precision == SI_PRECISION_FP32)
+      launch_sweep<float>(x, d_mask, static_cast<const float*>(d_b),
+                          static_cast<const float*>(d_u_old), static_cast<float*>(d_u_new), w, h,
+                          c, block_size, overlap, flavour, o.alpha, lc, known_invariant != 0,
+                          ctx->counters.as<unsigned long long>(), by0, by1);
+    else
+      launch_sweep<double>(x, d_mask, static_cast<const double*>(d_b),
+                           static_cast<const double*>(d_u_old), static_cast<double*>(d_u_new), w,
+                           h, c, block_size, overlap, flavour, o.alpha, lc, known_invariant != 0,
+                           ctx->counters.as<unsigned long long>(), by0, by1);
+    publish_counters(x, 2);
+    if (failures) *failures = static_cast<long long>(ctx->host_cnt[0]);
+    if (cg_iterations) *cg_iterations = static_cast<long long>(ctx->host_cnt[1]);
+  });
+}
+
 si_status si_partition_domain(int w, int h, int block_size, int overlap, int* blocks_x,
                               int* blocks_y, int* rects, int rects_capacity) {
   return guard([&] {
@@ -1170,6 +1348,8 @@ si_status si_partition_domain(int w, int h, int block_size, int overlap, int* bl
       }
   });
 }
+
+double si_joint_norm(const double* sumsq, int c) { return joint_norm(sumsq, c); }
 
 si_status si_psnr(const double* u, const double* f, int w, int h, int c, double* psnr_db) {
   return guard([&] {

@@ -49,6 +49,7 @@ struct SweepArgs {
   int known_invariant;    // multilevel invariant: b = 0 at unknown pixels and u = b at
                        // known pixels (so r = 0 there); b is never read
   unsigned long long* counters;  // [0] failures, [1] CG iterations (may be null)
+  int by0;             // first block row of this launch (stripe mode; 0 otherwise)
 };
 
 template <typename T>
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
   __shared__ SweepSmem<T, NW> S;
 
   const int bx = blockIdx.x % a.ax.count;
-  const int by = blockIdx.x / a.ax.count;
+  const int by = a.by0 + static_cast<int>(blockIdx.x) / a.ax.count;
   const int ch = blockIdx.y;
   const int B = FULL ? kMaxBlock : a.ax.block;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

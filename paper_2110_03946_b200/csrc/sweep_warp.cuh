@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(32, (WarpOcc<T>::value)) oras_sweep_warp_kerne
   const int lane = threadIdx.x;
   const int cp = lane & 15, half = lane >> 4;
   const int c0 = 2 * cp, row0 = R * half;
-  const int bx = blockIdx.x % a.ax.count, by = blockIdx.x / a.ax.count;
+  const int bx = blockIdx.x % a.ax.count, by = a.by0 + static_cast<int>(blockIdx.x) / a.ax.count;
   const int x0 = a.ax.anchor(bx), y0 = a.ay.anchor(by);
   const int W = a.W, H = a.H;
   const int gx = x0 + c0;  // my columns gx, gx+1
