@@ -61,11 +61,14 @@ double ms_since(Clock::time_point t0) {
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
-  void ensure(size_t want) {
-    if (want <= bytes) return;
+  // returns true when (re)allocated; the new memory is zero-filled
+  bool ensure(size_t want) {
+    if (want <= bytes) return false;
     release();
     CK(cudaMalloc(&ptr, want));
+    CK(cudaMemset(ptr, 0, want));
     bytes = want;
+    return true;
   }
   void release() {
     if (ptr) cudaFree(ptr);

@@ -172,7 +172,7 @@ def test_device_stripes_match_single_gpu(world, w, h, c, levels):
     opts = dict(levels=levels, block_size=32, overlap=6)
     out = _run_threads(world, lambda r: S.DeviceBackend(si.Solver(0)), df, dm, opts)
     for u, rep in out:
-        assert rep.level_iterations == ref.report.level_iterations
+        assert rep.level_iterations == ref.report.level_iterations, (rep.trace, rep.plans)
         assert np.array_equal(u.cpu().numpy(), ref.image.data)
         got = np.array(rep.trace)
         want = np.array([r.rel_residual for r in ref.trace.rows])
