@@ -253,6 +253,10 @@ typedef struct si_kernel_stats {
   long long total_launches;
 } si_kernel_stats;
 si_status si_set_profiling(si_ctx* ctx, int enabled);
+/* Device self-tests of arithmetic shortcuts used by the kernels.  which = 0:
+ * division through a precomputed correctly rounded reciprocal equals IEEE
+ * division on n random operand pairs; *failures = mismatches. */
+si_status si_selftest(si_ctx* ctx, int which, long long n, long long* failures);
 si_status si_get_kernel_stats(si_ctx* ctx, si_kernel_stats* out, int reset);
 /* Pinned host memory for zero-staging host<->device copies. */
 si_status si_host_alloc(size_t bytes, void** ptr);

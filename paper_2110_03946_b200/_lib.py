@@ -117,6 +117,7 @@ SIGNATURES = {
     "si_joint_norm": (_d, [_dp, _i]),
     "si_psnr": (_i, [_vp, _vp, _i, _i, _i, _dp]),
     "si_set_profiling": (_i, [_vp, _i]),
+    "si_selftest": (_i, [_vp, _i, C.c_longlong, _llp]),
     "si_get_kernel_stats": (_i, [_vp, C.POINTER(si_kernel_stats), _i]),
     "si_host_alloc": (_i, [C.c_size_t, C.POINTER(_vp)]),
     "si_host_free": (_i, [_vp]),

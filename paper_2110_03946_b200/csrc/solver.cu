@@ -100,7 +100,7 @@ struct si_ctx {
   cudaStream_t own_stream = nullptr;
   std::vector<LevelBuf> levels;
   DevBuf in_f, in_mask, in_ref, out_img, aux;   // host-API staging
-  DevBuf red_partials, red_out, counters;
+  DevBuf red_partials, red_out, counters, scratch;
   DevBuf ticket;
   // Scalars cross PCIe through mapped (zero-copy) pinned memory written by
   // the kernels themselves: no copy-engine transfer that could queue behind a
@@ -249,7 +249,10 @@ struct LocalCfg {
 template <typename T, int NW>
 void launch_sweep_nw(Ctx& x, const SweepArgs<T>& a, int nblocks, int C) {
   if (a.ax.block == kMaxBlock && x.c.sweep_warp) {
-    oras_sweep_warp_kernel<T><<<dim3(nblocks, C), 32, 0, x.s>>>(a);
+    x.c.scratch.ensure(sizeof(T) * kMaxBlock * kMaxBlock * static_cast<size_t>(nblocks) * C);
+    SweepArgs<T> aw = a;
+    aw.scratch = x.c.scratch.as<T>();
+    oras_sweep_warp_kernel<T><<<dim3(nblocks, C), 32, 0, x.s>>>(aw);
   } else if (a.ax.block == kMaxBlock)
     oras_sweep_kernel<T, NW, true><<<dim3(nblocks, C), NW * 32, 0, x.s>>>(a);
   else
@@ -263,7 +266,7 @@ void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_
                   bool known_invariant, unsigned long long* counters, int by0 = 0, int by1 = -1) {
   if (block > kMaxBlock)
     fail(SI_ERR_UNSUPPORTED, "block size " + std::to_string(block) + " exceeds the supported 32");
-  SweepArgs<T> a;
+  SweepArgs<T> a{};
   a.mask = mask;
   a.b = b;
   a.u_old = u_old;
@@ -741,7 +744,7 @@ void si_destroy(si_ctx* c) {
     l.u1.release();
   }
   for (DevBuf* b : {&c->in_f, &c->in_mask, &c->in_ref, &c->out_img, &c->aux, &c->red_partials,
-                    &c->red_out, &c->counters, &c->ticket})
+                    &c->red_out, &c->counters, &c->ticket, &c->scratch})
     b->release();
   for (auto& p : c->pending) {
     cudaEventDestroy(p.start);
@@ -895,6 +898,36 @@ si_status si_run_method_batch(si_ctx* ctx, int method, int n, const double* cons
 
 // ---------------------------------------------------------------- building blocks
 namespace {
+
+// splitmix64
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// div_by_recip(a, b, RN(1/b)) == a / b over random normal doubles/floats,
+// including significands near all-ones; counts mismatches.
+__global__ void selftest_division_kernel(long long n, unsigned long long seed,
+                                         unsigned long long* bad) {
+  unsigned long long local = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long ra = mix64(seed ^ (2 * i)), rb = mix64(seed ^ (2 * i + 1));
+    // exponents in [2^-60, 2^60], random significands (every 8th b all-ones-ish)
+    const unsigned long long ea = 1023 - 60 + (ra >> 57) % 121, eb = 1023 - 60 + (rb >> 57) % 121;
+    unsigned long long mb = rb & 0xfffffffffffffull;
+    if ((i & 7) == 0) mb |= 0xffffffffff000ull;
+    const double a = __longlong_as_double((long long)((ea << 52) | (ra & 0xfffffffffffffull)));
+    const double b = __longlong_as_double((long long)((eb << 52) | mb));
+    if (div_by_recip(a, b, recip_rn(b)) != a / b) ++local;
+    const float af = (float)a * 1e-3f, bf = (float)b * 1e-3f;
+    if (bf != 0.0f && isfinite(af) && isfinite(bf) && div_by_recip(af, bf, recip_rn(bf)) != af / bf)
+      ++local;
+  }
+  if (local) atomicAdd(bad, local);
+}
 
 // LocalOperator::apply on one block (schwarz.hpp:57-75) with the diagonal of
 // build_local_operator (schwarz.hpp:115-130); one thread per block cell.
@@ -1353,6 +1386,20 @@ si_status si_partition_domain(int w, int h, int block_size, int overlap, int* bl
 }
 
 double si_joint_norm(const double* sumsq, int c) { return joint_norm(sumsq, c); }
+
+si_status si_selftest(si_ctx* ctx, int which, long long n, long long* failures) {
+  return guard([&] {
+    check_arg(ctx && failures && which == 0 && n >= 0, "invalid self-test");
+    set_device(ctx);
+    Ctx x{*ctx, ctx->own_stream};
+    begin_counters(x);
+    selftest_division_kernel<<<148 * 8, 256, 0, x.s>>>(n, 0x5eedull,
+                                                      ctx->counters.as<unsigned long long>());
+    CK(cudaGetLastError());
+    publish_counters(x, 1);
+    *failures = static_cast<long long>(ctx->host_cnt[0]);
+  });
+}
 
 si_status si_psnr(const double* u, const double* f, int w, int h, int c, double* psnr_db) {
   return guard([&] {

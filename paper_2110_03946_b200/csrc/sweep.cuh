@@ -50,6 +50,7 @@ struct SweepArgs {
                        // known pixels (so r = 0 there); b is never read
   unsigned long long* counters;  // [0] failures, [1] CG iterations (may be null)
   int by0;             // first block row of this launch (stripe mode; 0 otherwise)
+  T* scratch;          // one-warp variant: 32x32 rhs tile per (block, channel)
 };
 
 template <typename T>
@@ -84,12 +85,31 @@ template <typename T, int NW>
 __device__ __forceinline__ T cta_sum(T v, T (*red)[NW], int slot, int warp, int lane) {
   v = warp_sum(v);
   if (NW == 1) return v;
+#ifdef SI_ABL_NORED
+  return v;
+#endif
   if (lane == 0) red[slot][warp] = v;
   __syncthreads();
   T s = red[slot][0];
 #pragma unroll
   for (int w = 1; w < NW; ++w) s += red[slot][w];
   return s;
+}
+
+// a / b, correctly rounded, from a precomputed rcp = RN(1/b): q0 = RN(a*rcp)
+// is within an ulp of a/b, the residual a - b*q0 is exact under fma, and one
+// correction q0 + rcp*(a - b*q0) rounds to RN(a/b) for normal operands
+// (Markstein).  Lets beta = rr_new/rr take 1/rr computed an iteration early,
+// off the critical path; si_selftest(0, ...) checks it bit for bit against
+// the IEEE division.
+__device__ __forceinline__ double recip_rn(double b) { return __drcp_rn(b); }
+__device__ __forceinline__ float recip_rn(float b) { return __frcp_rn(b); }
+
+template <typename T>
+__device__ __forceinline__ T div_by_recip(T a, T b, T rcp) {
+  const T q0 = a * rcp;
+  const T e = fma(-b, q0, a);
+  return fma(e, rcp, q0);
 }
 
 // Thread-local part of a dot product: two interleaved accumulators (even and
@@ -350,12 +370,17 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
         t = t - vE;
         t = t - vN;
         t = t - vS;
+#ifdef SI_ABL_NOMASK
+        o[i] = t;
+#else
         o[i] = ((unk >> i) & 1u) ? t : T(0);
+#endif
       }
     };
 
     publish();
     T rr = cta_sum<T, NW>(dot2<T, R>(r, r), S.red, 1, warp, lane);  // also orders the pt staging
+    T rr_rcp = recip_rn(rr);
     collect();
     nb_p[0] = nb_r[0];  // p = r initially
     nb_p[1] = nb_r[1];
@@ -374,11 +399,17 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
       for (int iter = 1; iter <= a.lmax; ++iter) {
         apply(p, nb_p[0], nb_p[1], q);
         const T pAp = cta_sum<T, NW>(dot2<T, R>(p, q), S.red, 0, warp, lane);
+#ifndef SI_ABL_NOBREAK
         if (!(pAp > T(0)) || !isfinite(pAp)) {  // breakdown (cg.hpp:120-125)
           iters = iter - 1;
           break;
         }
+#endif
+#ifdef SI_ABL_NODIV
+        const T alpha = rr * T(0.5);
+#else
         const T alpha = rr / pAp;
+#endif
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           x[i] = fmaT(alpha, p[i], x[i]);
@@ -417,13 +448,18 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
           }
           rr_new = tt;
         }
-        const T beta = rr_new / rr;
+#ifdef SI_ABL_NODIV
+        const T beta = rr_new * T(0.25);
+#else
+        const T beta = div_by_recip(rr_new, rr, rr_rcp);  // == rr_new / rr
+#endif
 #pragma unroll
         for (int i = 0; i < R; ++i) p[i] = fmaT(beta, p[i], r[i]);
         stage(p);
         nb_p[0] = fmaT(beta, nb_p[0], nb_r[0]);
         nb_p[1] = fmaT(beta, nb_p[1], nb_r[1]);
         rr = rr_new;
+        rr_rcp = recip_rn(rr);
         if (iter == a.lmax) iters = a.lmax;
       }
     }

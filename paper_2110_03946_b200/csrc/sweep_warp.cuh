@@ -24,14 +24,14 @@ namespace sib {
 template <typename T>
 struct WarpSweepSmem {
   T xt[kMaxBlock][kMaxBlock];  // CG iterate x
-  T bt[kMaxBlock][kMaxBlock];  // local right-hand side
+  T qt[kMaxBlock][kMaxBlock];  // A p of the current iteration
 };
 
 #ifndef SI_WOCC64
-#define SI_WOCC64 8
+#define SI_WOCC64 12
 #endif
 #ifndef SI_WOCC32
-#define SI_WOCC32 12
+#define SI_WOCC32 14
 #endif
 
 template <typename T>
@@ -90,7 +90,11 @@ __global__ void __launch_bounds__(32, (WarpOcc<T>::value)) oras_sweep_warp_kerne
   const uint8_t* __restrict__ mask = a.mask;
   constexpr unsigned FULLM = 0xffffffffu;
 
-  T r[R][2], p[R][2], q[R][2];
+  T r[R][2], p[R][2];
+  // local right-hand side of this (block, channel), kept for the rare
+  // true-residual checks in a global scratch tile (L2/HBM, not registers)
+  T* __restrict__ bt = a.scratch + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) *
+                                       (kMaxBlock * kMaxBlock);
   uint32_t unk = 0;  // bit 2*i+k: cell (row0+i, c0+k) unknown
 
   // ---- setup: residual of block rows row0-1 .. row0+R (index j), ghosts 0 --
@@ -173,7 +177,7 @@ __global__ void __launch_bounds__(32, (WarpOcc<T>::value)) oras_sweep_warp_kerne
       }
       r[i][0] = t0;
       r[i][1] = t1;
-      store2(&S.bt[ly][c0], t0, t1);
+      store2(&bt[ly * kMaxBlock + c0], t0, t1);
       store2(&S.xt[ly][c0], T(0), T(0));
     }
   }
@@ -190,8 +194,10 @@ __global__ void __launch_bounds__(32, (WarpOcc<T>::value)) oras_sweep_warp_kerne
     dL[k] = half == 1 ? dB : dI[k];  // row i = R-1 is block row 31 only in the lower half
   }
 
-  // o = A v on my cells (LocalStencilOperator::apply, schwarz.hpp:146-159)
-  auto apply = [&](const T(&v)[R][2], T(&o)[R][2]) {
+  // q = A v on my cells (LocalStencilOperator::apply, schwarz.hpp:146-159),
+  // stored to the q tile; returns my part of v.q.
+  auto apply = [&](const T(&v)[R][2]) {
+    T acc0 = T(0), acc1 = T(0);
     // N neighbour of my row 0 / S neighbour of my row R-1 across the halves
     const T n0 = __shfl_up_sync(FULLM, v[R - 1][0], 16), n1 = __shfl_up_sync(FULLM, v[R - 1][1], 16);
     const T s0 = __shfl_down_sync(FULLM, v[0][0], 16), s1 = __shfl_down_sync(FULLM, v[0][1], 16);
@@ -215,9 +221,13 @@ __global__ void __launch_bounds__(32, (WarpOcc<T>::value)) oras_sweep_warp_kerne
       t1 = t1 - e;
       t1 = t1 - vn1;
       t1 = t1 - vs1;
-      o[i][0] = ((unk >> (2 * i)) & 1u) ? t0 : T(0);
-      o[i][1] = ((unk >> (2 * i + 1)) & 1u) ? t1 : T(0);
+      const T o0 = ((unk >> (2 * i)) & 1u) ? t0 : T(0);
+      const T o1 = ((unk >> (2 * i + 1)) & 1u) ? t1 : T(0);
+      store2(&S.qt[row0 + i][c0], o0, o1);
+      acc0 = fmaT(v[i][0], o0, acc0);
+      acc1 = fmaT(v[i][1], o1, acc1);
     }
+    return acc0 + acc1;
   };
   auto dot = [&](const T(&va)[R][2], const T(&vb)[R][2]) {
     T s0 = T(0), s1 = T(0);
@@ -238,6 +248,7 @@ __global__ void __launch_bounds__(32, (WarpOcc<T>::value)) oras_sweep_warp_kerne
       p[i][1] = r[i][1];
     }
     T rr = dot(r, r);
+    T rr_rcp = recip_rn(rr);
     const T r0 = sqrt(rr);
     const T thr = a.ltol * r0;
     const T thr2 = thr * thr;
@@ -248,8 +259,7 @@ __global__ void __launch_bounds__(32, (WarpOcc<T>::value)) oras_sweep_warp_kerne
     } else {
       int until_check = a.lcheck;
       for (int iter = 1; iter <= a.lmax; ++iter) {
-        apply(p, q);
-        const T pAp = dot(p, q);
+        const T pAp = warp_sum(apply(p));
         if (!(pAp > T(0)) || !isfinite(pAp)) {  // breakdown (cg.hpp:120-125)
           iters = iter - 1;
           break;
@@ -257,11 +267,12 @@ __global__ void __launch_bounds__(32, (WarpOcc<T>::value)) oras_sweep_warp_kerne
         const T alpha = rr / pAp;
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-          T xa, xb;
+          T xa, xb, qa, qb;
           load2(&S.xt[row0 + i][c0], xa, xb);
+          load2(&S.qt[row0 + i][c0], qa, qb);  // my own cells: no barrier needed
           store2(&S.xt[row0 + i][c0], fmaT(alpha, p[i][0], xa), fmaT(alpha, p[i][1], xb));
-          r[i][0] = fmaT(-alpha, q[i][0], r[i][0]);
-          r[i][1] = fmaT(-alpha, q[i][1], r[i][1]);
+          r[i][0] = fmaT(-alpha, qa, r[i][0]);
+          r[i][1] = fmaT(-alpha, qb, r[i][1]);
         }
         T rr_new = dot(r, r);
         if (--until_check == 0) until_check = a.lcheck;
@@ -288,31 +299,28 @@ __global__ void __launch_bounds__(32, (WarpOcc<T>::value)) oras_sweep_warp_kerne
               t = t - xn;
               t = t - xs;
               t = ((unk >> (2 * i + k)) & 1u) ? t : T(0);
-              q[i][k] = S.bt[ly][lx] - t;
+              // residual replacement target (r is not needed if this converges)
+              r[i][k] = bt[ly * kMaxBlock + lx] - t;
             }
           }
-          const T tt = dot(q, q);
+          const T tt = dot(r, r);
           const T rel = sqrt(tt) / r0;
           if (rel <= a.ltol) {
             iters = iter;
             converged = true;
             break;
           }
-#pragma unroll
-          for (int i = 0; i < R; ++i) {
-            r[i][0] = q[i][0];
-            r[i][1] = q[i][1];
-          }
           rr_new = tt;
           __syncwarp();  // x tile reads done before the next in-place update
         }
-        const T beta = rr_new / rr;
+        const T beta = div_by_recip(rr_new, rr, rr_rcp);  // == rr_new / rr
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           p[i][0] = fmaT(beta, p[i][0], r[i][0]);
           p[i][1] = fmaT(beta, p[i][1], r[i][1]);
         }
         rr = rr_new;
+        rr_rcp = recip_rn(rr);
         if (iter == a.lmax) iters = a.lmax;
       }
     }

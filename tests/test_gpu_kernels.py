@@ -178,3 +178,13 @@ def test_sweep_arbitrary_u_and_b(solver, oracle):
     got, _, _ = solver.schwarz_sweep(mask.known, b, u, 16, 5)
     want, _, _ = oracle.oracle_sweep(mask.known, b, u, 16, 5)
     assert np.abs(got - want).max() <= 1e-9
+
+
+def test_division_shortcut_is_ieee_exact(solver):
+    """beta = rr_new/rr runs as div_by_recip(rr_new, rr, RN(1/rr)); it must equal
+    the IEEE quotient bit for bit (fp64 and fp32)."""
+    import ctypes as C
+    from paper_2110_03946_b200 import _lib as L
+    bad = C.c_longlong(-1)
+    assert L.load().si_selftest(solver.handle, 0, 50_000_000, C.byref(bad)) == 0
+    assert bad.value == 0
