@@ -37,8 +37,9 @@ typedef enum {
   SI_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument (image.hpp:18-20) */
   SI_ERR_CUDA = 2,
   SI_ERR_OOM = 3,
-  SI_ERR_UNSUPPORTED = 4,      /* e.g. block_size > 32, method cg/mlcg */
-  SI_ERR_NO_DEVICE = 5
+  SI_ERR_UNSUPPORTED = 4,      /* e.g. block_size > 32 */
+  SI_ERR_NO_DEVICE = 5,
+  SI_ERR_RUNTIME = 6           /* reference: std::runtime_error (reduction.hpp:109-110) */
 } si_status;
 
 /* Method (methods.hpp:13). */
@@ -69,7 +70,7 @@ typedef struct si_options {
   int local_max_iterations;
   int local_check_interval;
   int max_outer_iterations;     /* 1000 */
-  int cg_max_iterations;        /* 100000 (mlcg; unsupported here) */
+  int cg_max_iterations;        /* 100000 (cg / mlcg level solver) */
   int cg_check_interval;        /* 4 */
   int normalizer;               /* si_normalizer, InitialGuess */
   int precision;                /* si_precision, FP64 (the reference's type) */

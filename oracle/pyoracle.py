@@ -45,6 +45,8 @@ class Options(C.Structure):
         ("max_outer_iterations", C.c_int),
         ("normalizer", C.c_int),
         ("flavour", C.c_int),
+        ("cg_max_iterations", C.c_int),
+        ("cg_check_interval", C.c_int),
     ]
 
 
@@ -66,7 +68,7 @@ class Report(C.Structure):
 
 
 def default_options(**kw) -> Options:
-    o = Options(1e-3, 3, 32, 6, 0.25, 1e-2, 0, 1e-2, 30, 30, 1000, 0, 1)
+    o = Options(1e-3, 3, 32, 6, 0.25, 1e-2, 0, 1e-2, 30, 30, 1000, 0, 1, 100000, 4)
     for k, v in kw.items():
         setattr(o, k, v)
     return o
@@ -190,7 +192,7 @@ def oracle_solve(f: np.ndarray, mask: np.ndarray, **opts) -> Solve:
     o = default_options(**opts)
     out = np.empty_like(f)
     rep = Report()
-    cap = o.max_outer_iterations + 2
+    cap = max(o.max_outer_iterations, 0) + 2 if o.flavour != 2 else o.cg_max_iterations + 2
     trace = np.zeros(cap)
     rc = oracle().or_multilevel_solve(f.ravel(), m.ravel(), w, h, c, C.byref(o), out.ravel(),
                                       C.byref(rep), trace, cap)

@@ -43,6 +43,8 @@ struct RefOptions {  // same field order as or_options in si_oracle.h
   int max_outer_iterations;
   int normalizer;
   int flavour;
+  int cg_max_iterations;
+  int cg_check_interval;
 };
 
 struct RefReport {  // same layout as or_report
@@ -85,6 +87,8 @@ si::RunOptions run_options(const RefOptions* o) {
   r.max_outer_iterations = o->max_outer_iterations;
   r.normalizer = o->normalizer ? si::ResidualNormalizer::RhsNorm
                                : si::ResidualNormalizer::InitialGuess;
+  r.cg_max_iterations = o->cg_max_iterations;
+  r.cg_check_interval = o->cg_check_interval;
   return r;
 }
 }  // namespace

@@ -27,6 +27,8 @@ void or_default_options(or_options* o) {
   o->max_outer_iterations = 1000;
   o->normalizer = 0;
   o->flavour = 1;
+  o->cg_max_iterations = 100000;
+  o->cg_check_interval = 4;
 }
 
 /* ---- deterministic sums: parallel.hpp:165-211 ------------------------- */
@@ -406,6 +408,238 @@ static double canonical_r0(const uint8_t* mask, int w, int h, int c, const doubl
   return sqrt(acc);
 }
 
+/* ---- CG level solver: reduction.hpp:26-145, cg.hpp:192-291,
+ *      multilevel.hpp:162-209 ---------------------------------------------- */
+typedef struct {
+  int w, h;
+  size_t n;            /* reduced size */
+  int32_t* unknown_of; /* pixel -> reduced index or -1 */
+  int32_t* pixel_of;
+  double* diag;
+} reduced_sys;
+
+static reduced_sys reduce_structure(const uint8_t* mask, int w, int h) {
+  reduced_sys s;
+  s.w = w;
+  s.h = h;
+  size_t np = (size_t)w * h;
+  s.unknown_of = (int32_t*)malloc(np * sizeof(int32_t));
+  s.pixel_of = (int32_t*)malloc(np * sizeof(int32_t));
+  s.n = 0;
+  for (size_t i = 0; i < np; ++i) {
+    s.unknown_of[i] = -1;
+    if (!mask[i]) {
+      s.unknown_of[i] = (int32_t)s.n;
+      s.pixel_of[s.n++] = (int32_t)i;
+    }
+  }
+  s.diag = (double*)malloc((s.n + 1) * sizeof(double));
+  for (size_t k = 0; k < s.n; ++k) {
+    int p = s.pixel_of[k], x = p % w, y = p / w;
+    s.diag[k] = (x > 0) + (x + 1 < w) + (y > 0) + (y + 1 < h);
+  }
+  return s;
+}
+
+static void reduced_free(reduced_sys* s) {
+  free(s->unknown_of);
+  free(s->pixel_of);
+  free(s->diag);
+}
+
+/* ReducedSystem::apply (reduction.hpp:36-58) */
+static void reduced_apply(const reduced_sys* s, const double* x, double* y) {
+  int w = s->w;
+  for (size_t k = 0; k < s->n; ++k) {
+    int32_t p = s->pixel_of[k];
+    int x_ = p % w, y_ = p / w;
+    double acc = s->diag[k] * x[k];
+    if (x_ > 0 && s->unknown_of[p - 1] >= 0) acc -= x[s->unknown_of[p - 1]];
+    if (x_ + 1 < w && s->unknown_of[p + 1] >= 0) acc -= x[s->unknown_of[p + 1]];
+    if (y_ > 0 && s->unknown_of[p - w] >= 0) acc -= x[s->unknown_of[p - w]];
+    if (y_ + 1 < s->h && s->unknown_of[p + w] >= 0) acc -= x[s->unknown_of[p + w]];
+    y[k] = acc;
+  }
+}
+
+/* cg_solve_lockstep (cg.hpp:192-291); sets *iters / *final_rel, returns converged. */
+static int cg_lockstep(const reduced_sys* s, double** b, double** x, int nc, double tol, int maxit,
+                       int check, double external_r0, double** u_obs, const double* bfull,
+                       size_t npix, or_report* rep, double* trace, int trace_cap, int sink,
+                       int* iters, double* final_rel) {
+  size_t n = s->n;
+  *iters = 0;
+  if (n == 0) {
+    *final_rel = 0.0;
+    return 1;
+  }
+  double** r = (double**)malloc(nc * sizeof(double*));
+  double** p = (double**)malloc(nc * sizeof(double*));
+  double* Ap = (double*)malloc(n * sizeof(double));
+  double *rr = (double*)calloc(nc, sizeof(double)), *rr_next = (double*)calloc(nc, sizeof(double));
+  char* frozen = (char*)calloc(nc, 1);
+  double joint0_sq = 0.0;
+  for (int c = 0; c < nc; ++c) {
+    r[c] = (double*)malloc(n * sizeof(double));
+    p[c] = (double*)malloc(n * sizeof(double));
+    reduced_apply(s, x[c], r[c]);
+    for (size_t i = 0; i < n; ++i) r[c][i] = b[c][i] - r[c][i];
+    rr[c] = det_dot(r[c], r[c], n);
+    joint0_sq += rr[c];
+    memcpy(p[c], r[c], n * sizeof(double));
+  }
+  double r0 = external_r0 > 0.0 ? external_r0 : sqrt(joint0_sq);
+  int converged = 0, done = 0;
+  if (r0 == 0.0 || sqrt(joint0_sq) <= tol * r0) {
+    *final_rel = r0 == 0.0 ? 0.0 : sqrt(joint0_sq) / r0;
+    converged = done = 1;
+  }
+  double freeze_sq = 1e-4 * tol * tol * r0 * r0;
+  double rel = done ? *final_rel : sqrt(joint0_sq) / r0;
+  for (int iter = 1; !done && iter <= maxit; ++iter) {
+    double joint_sq = 0.0;
+    int broke = 0;
+    for (int c = 0; c < nc; ++c) {
+      if (frozen[c] || rr[c] <= freeze_sq) {
+        frozen[c] = 1;
+        rr_next[c] = rr[c];
+        joint_sq += rr[c];
+        continue;
+      }
+      reduced_apply(s, p[c], Ap);
+      double pAp = det_dot(p[c], Ap, n);
+      if (!(pAp > 0.0) || !isfinite(pAp)) {
+        *iters = iter - 1;
+        *final_rel = rel;
+        broke = 1;
+        break;
+      }
+      double alpha = rr[c] / pAp;
+      for (size_t i = 0; i < n; ++i) x[c][i] += alpha * p[c][i];
+      for (size_t i = 0; i < n; ++i) r[c][i] += -alpha * Ap[i];
+      rr_next[c] = det_dot(r[c], r[c], n);
+      joint_sq += rr_next[c];
+    }
+    if (broke) {
+      done = 1;
+      break;
+    }
+    int cadence = iter % check == 0 || iter == maxit;
+    int maybe_done = sqrt(joint_sq) <= tol * r0;
+    if (cadence || maybe_done) {
+      double true_sq = 0.0;
+      for (int c = 0; c < nc; ++c) {
+        reduced_apply(s, x[c], Ap);
+        for (size_t i = 0; i < n; ++i) Ap[i] = b[c][i] - Ap[i];
+        double nc2 = det_dot(Ap, Ap, n);
+        true_sq += nc2;
+        if (!frozen[c]) {
+          memcpy(r[c], Ap, n * sizeof(double));
+          rr_next[c] = nc2;
+        }
+      }
+      rel = sqrt(true_sq) / r0;
+      if (sink) {
+        if (trace && rep->trace_rows < trace_cap) trace[rep->trace_rows] = rel;
+        rep->trace_rows++;
+      }
+      if (rel <= tol) {
+        *iters = iter;
+        *final_rel = rel;
+        converged = done = 1;
+        break;
+      }
+    }
+    for (int c = 0; c < nc; ++c) {
+      if (frozen[c]) continue;
+      double beta = rr[c] > 0.0 ? rr_next[c] / rr[c] : 0.0;
+      for (size_t i = 0; i < n; ++i) p[c][i] = r[c][i] + beta * p[c][i];
+      rr[c] = rr_next[c];
+    }
+    if (iter == maxit) {
+      *iters = maxit;
+      *final_rel = rel;
+    }
+  }
+  if (!done && maxit <= 0) {
+    *iters = maxit < 0 ? 0 : maxit;
+    *final_rel = rel;
+  }
+  (void)u_obs;
+  (void)bfull;
+  (void)npix;
+  for (int c = 0; c < nc; ++c) {
+    free(r[c]);
+    free(p[c]);
+  }
+  free(r);
+  free(p);
+  free(Ap);
+  free(rr);
+  free(rr_next);
+  free(frozen);
+  return converged;
+}
+
+/* run_cg_level (multilevel.hpp:162-209) */
+static level_outcome run_cg_level(const uint8_t* mask, int w, int h, int c, const double* bvals,
+                                  double* u, double tol, const or_options* opt, or_report* rep,
+                                  double* trace, int trace_cap, int sink) {
+  size_t np = (size_t)w * h;
+  reduced_sys s = reduce_structure(mask, w, h);
+  size_t n = s.n;
+  double** rhs = (double**)malloc(c * sizeof(double*));
+  double** x = (double**)malloc(c * sizeof(double*));
+  double* tmp = (double*)malloc((n + 1) * sizeof(double));
+  double r0_sq = 0.0, init_sq = 0.0;
+  for (int k = 0; k < c; ++k) {
+    const double* b = bvals + k * np;  /* build_rhs(values) == values */
+    rhs[k] = (double*)malloc((n + 1) * sizeof(double));
+    for (size_t q = 0; q < n; ++q) {  /* reduced_rhs (reduction.hpp:119-134) */
+      int32_t p = s.pixel_of[q];
+      int xx = p % w, yy = p / w;
+      double acc = b[p];
+      if (xx > 0 && s.unknown_of[p - 1] == -1) acc += b[p - 1];
+      if (xx + 1 < w && s.unknown_of[p + 1] == -1) acc += b[p + 1];
+      if (yy > 0 && s.unknown_of[p - w] == -1) acc += b[p - w];
+      if (yy + 1 < h && s.unknown_of[p + w] == -1) acc += b[p + w];
+      rhs[k][q] = acc;
+    }
+    double nrm = det_norm(rhs[k], n);
+    r0_sq = fma(nrm, nrm, r0_sq);
+    x[k] = (double*)malloc((n + 1) * sizeof(double));
+    for (size_t q = 0; q < n; ++q) x[k][q] = u[k * np + s.pixel_of[q]];
+  }
+  double r0 = sqrt(r0_sq);
+  for (int k = 0; k < c; ++k) {
+    reduced_apply(&s, x[k], tmp);
+    for (size_t q = 0; q < n; ++q) tmp[q] = rhs[k][q] - tmp[q];
+    double nrm = det_norm(tmp, n);
+    init_sq = fma(nrm, nrm, init_sq);
+  }
+  double rel0 = r0 > 0.0 ? sqrt(init_sq) / r0 : 0.0;
+  if (sink) {
+    if (trace && rep->trace_rows < trace_cap) trace[rep->trace_rows] = rel0;
+    rep->trace_rows++;
+  }
+  level_outcome out = {0, 0.0, 0};
+  out.converged = cg_lockstep(&s, rhs, x, c, tol, opt->cg_max_iterations, opt->cg_check_interval,
+                              r0, NULL, NULL, np, rep, trace, trace_cap, sink, &out.iterations,
+                              &out.final_rel);
+  for (int k = 0; k < c; ++k) {  /* embed_solution (reduction.hpp:138-145) */
+    const double* b = bvals + k * np;
+    for (size_t i = 0; i < np; ++i) u[k * np + i] = b[i];
+    for (size_t q = 0; q < n; ++q) u[k * np + s.pixel_of[q]] = x[k][q];
+    free(rhs[k]);
+    free(x[k]);
+  }
+  free(rhs);
+  free(x);
+  free(tmp);
+  reduced_free(&s);
+  return out;
+}
+
 /* ---- pyramid: multilevel.hpp:33-128 ------------------------------------ */
 int or_restrict_level(const uint8_t* mask, const double* values, int fw, int fh, int c,
                       int averaging, uint8_t* cmask, double* cvalues) {
@@ -524,9 +758,14 @@ int or_multilevel_solve(const double* f, const uint8_t* mask, int w, int h, int 
     be = be < H ? be : H;
     int oe = opt->overlap < be - 1 ? opt->overlap : be - 1;
     if (oe < 0) oe = 0;
-    double r0 = canonical_r0(lm[level], W, H, c, b, opt->normalizer);
-    level_outcome o = run_level(lm[level], W, H, c, b, u, r0, tol, be, oe, opt, rep, trace_rel,
-                                trace_cap, finest);
+    level_outcome o;
+    if (opt->flavour == 2) {
+      o = run_cg_level(lm[level], W, H, c, b, u, tol, opt, rep, trace_rel, trace_cap, finest);
+    } else {
+      double r0 = canonical_r0(lm[level], W, H, c, b, opt->normalizer);
+      o = run_level(lm[level], W, H, c, b, u, r0, tol, be, oe, opt, rep, trace_rel, trace_cap,
+                    finest);
+    }
     rep->level_iterations[level] = o.iterations;
     rep->level_final_rel[level] = o.final_rel;
     rep->level_converged[level] = o.converged;

@@ -38,7 +38,9 @@ typedef struct {
   int local_check_interval;
   int max_outer_iterations;
   int normalizer;              /* 0 InitialGuess, 1 RhsNorm (schwarz.hpp:36) */
-  int flavour;                 /* 0 RAS, 1 ORAS (schwarz.hpp:29) */
+  int flavour;                 /* 0 RAS, 1 ORAS (schwarz.hpp:29), 2 CG level solver */
+  int cg_max_iterations;       /* RunOptions::cg_max_iterations (methods.hpp:51) */
+  int cg_check_interval;       /* RunOptions::cg_check_interval (methods.hpp:54) */
 } or_options;
 
 typedef struct {

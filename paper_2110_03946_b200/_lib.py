@@ -19,6 +19,7 @@ SI_ERR_CUDA = 2
 SI_ERR_OOM = 3
 SI_ERR_UNSUPPORTED = 4
 SI_ERR_NO_DEVICE = 5
+SI_ERR_RUNTIME = 6
 
 
 class si_options(C.Structure):

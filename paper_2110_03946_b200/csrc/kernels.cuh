@@ -12,19 +12,27 @@ namespace sib {
 constexpr int kRedThreads = 256;
 constexpr int kRedBlocksMax = 1184;  // 148 SMs x 8
 
-// blk: this CTA's index among the nblk CTAs of its channel chn.
-__device__ void reduce_epilogue(double v, double* partials, double* out, unsigned int* ticket,
-                                int blk, int nblk, int chn, int nch) {
-  __shared__ double wsum[kRedThreads / 32];
+// K sums per CTA (v[k]); blk: this CTA's index among the nblk CTAs of its
+// channel chn (of nch).  Final results: out[k*nch + c].
+template <int K>
+__device__ void reduce_epilogue_k(const double (&vin)[K], double* partials, double* out,
+                                  unsigned int* ticket, int blk, int nblk, int chn, int nch) {
+  __shared__ double wsum[K][kRedThreads / 32];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  v = warp_sum(v);
-  if (lane == 0) wsum[warp] = v;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double v = warp_sum(vin[k]);
+    if (lane == 0) wsum[k][warp] = v;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < kRedThreads / 32; ++w) s += wsum[w];
-    partials[chn * nblk + blk] = s;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < kRedThreads / 32; ++w) s += wsum[k][w];
+      partials[(k * nch + chn) * nblk + blk] = s;
+    }
     __threadfence();
     const unsigned int total = gridDim.x * gridDim.y * gridDim.z;
     last = atomicAdd(ticket, 1u) == total - 1;
@@ -32,22 +40,29 @@ __device__ void reduce_epilogue(double v, double* partials, double* out, unsigne
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // Fixed-order final sum per channel: strided partial sums + butterfly.
-  for (int c = 0; c < nch; ++c) {
+  // Fixed-order final sum per (value, channel): strided partials + butterfly.
+  for (int kc = 0; kc < K * nch; ++kc) {
     double s = 0.0;
     for (int i = threadIdx.x; i < nblk; i += kRedThreads)
-      s += reinterpret_cast<volatile double*>(partials)[c * nblk + i];
+      s += reinterpret_cast<volatile double*>(partials)[kc * nblk + i];
     s = warp_sum(s);
     __syncthreads();
-    if (lane == 0) wsum[warp] = s;
+    if (lane == 0) wsum[0][warp] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int w = 0; w < kRedThreads / 32; ++w) t += wsum[w];
-      out[c] = t;
+      for (int w = 0; w < kRedThreads / 32; ++w) t += wsum[0][w];
+      out[kc] = t;
     }
   }
   if (threadIdx.x == 0) *ticket = 0u;
+}
+
+__device__ __forceinline__ void reduce_epilogue(double v, double* partials, double* out,
+                                                unsigned int* ticket, int blk, int nblk, int chn,
+                                                int nch) {
+  const double vv[1] = {v};
+  reduce_epilogue_k<1>(vv, partials, out, ticket, blk, nblk, chn, nch);
 }
 
 // K1: per channel sum of (b - A u)^2 (residual_into + vec::norm^2,

@@ -24,6 +24,7 @@
 #include "kernels.cuh"
 #include "sweep.cuh"
 #include "sweep_warp.cuh"
+#include "cg_level.cuh"
 
 using namespace sib;
 
@@ -85,6 +86,8 @@ struct LevelBuf {
   DevBuf mask, b, u0, u1;
 };
 
+constexpr int kFlavourCg = -1;  // level solver = multilevel CG (LevelSolver::Cg)
+
 enum Kind { K_RESIDUAL = 0, K_SWEEP = 1, K_RESTRICT = 2, K_PROLONG = 3, K_INGEST = 4, K_METRIC = 5 };
 
 struct PendingEvent {
@@ -101,6 +104,7 @@ struct si_ctx {
   std::vector<LevelBuf> levels;
   DevBuf in_f, in_mask, in_ref, out_img, aux;   // host-API staging
   DevBuf red_partials, red_out, counters, scratch;
+  DevBuf cg_rhs, cg_x, cg_r, cg_p, cg_q;        // multilevel-CG level vectors
   DevBuf ticket;
   // Scalars cross PCIe through mapped (zero-copy) pinned memory written by
   // the kernels themselves: no copy-engine transfer that could queue behind a
@@ -475,6 +479,172 @@ void prepare_red(Ctx& x, int C) {
 }
 
 // multilevel_solve (multilevel.hpp:239-310) for the Schwarz level solvers.
+// run_cg_level (multilevel.hpp:162-209) on device buffers: the reduced
+// system's lockstep CG (cg_solve_lockstep, cg.hpp:192-291) with every scalar
+// decision on the host, every vector operation in cg_level.cuh.
+template <typename T>
+LevelOutcome run_cg_level(Ctx& x, LevelView<T>& V, int C, double tol, const si_options& o,
+                          bool sink, const Trace& tr, const double* d_ref) {
+  LevelOutcome out;
+  check_arg(C <= kCgMaxChannels, "multilevel CG: at most 8 channels");
+  const int W = V.w, H = V.h;
+  const size_t N = static_cast<size_t>(W) * H;
+  for (DevBuf* b : {&x.c.cg_rhs, &x.c.cg_x, &x.c.cg_r, &x.c.cg_p, &x.c.cg_q})
+    b->ensure(N * C * sizeof(T));
+  T *rhs = x.c.cg_rhs.as<T>(), *xv = x.c.cg_x.as<T>(), *r = x.c.cg_r.as<T>(),
+    *p = x.c.cg_p.as<T>(), *q = x.c.cg_q.as<T>();
+  const int gx = (W + kRedThreads - 1) / kRedThreads;
+  const int gy = std::max(1, std::min(H, (2 * kRedBlocksMax + gx * C - 1) / (gx * C)));
+  const dim3 grid(gx, gy, C);
+  x.c.red_partials.ensure(sizeof(double) * 2 * static_cast<size_t>(gx) * gy * C);
+  x.c.ticket.ensure(sizeof(unsigned int) * 4);
+  double* red = x.c.dev_red;  // mapped host memory
+  double* hred = x.c.host_red;
+  auto P = [&] { return x.c.red_partials.as<double>(); };
+  auto tk = [&] { return x.c.ticket.as<unsigned int>(); };
+  const double vec_bytes = static_cast<double>(N) * C * sizeof(T);
+
+  {
+    Timed t(x, K_RESIDUAL, 6 * vec_bytes);
+    cg_init_kernel<T><<<grid, kRedThreads, 0, x.s>>>(V.mask, V.b, V.u[V.cur], rhs, xv, r, p, W, H,
+                                                     N, P(), red, tk());
+    CK(cudaGetLastError());
+  }
+  sync(x);
+  // r0 from the reduced rhs, row 0 from the initial residual (multilevel.hpp:169-189)
+  const double r0 = joint_norm(hred, C);
+  const double rel0 = r0 > 0.0 ? joint_norm(hred + C, C) / r0 : 0.0;
+  auto trace_row = [&](int it, double rel) {
+    if (!sink || !tr.fn) return;
+    double qv = std::numeric_limits<double>::quiet_NaN();
+    if (d_ref) {
+      cg_embed_kernel<T><<<grid, kRedThreads, 0, x.s>>>(V.mask, V.b, xv, V.u[V.cur ^ 1], W, H, N);
+      launch_sq_error<T>(x, V.u[V.cur ^ 1], d_ref, N, C, x.c.dev_red + 3 * C);
+      sync(x);
+      qv = psnr_from_sq(std::vector<double>(hred + 3 * C, hred + 4 * C), N);
+    }
+    tr.fn(it, ms_since(tr.t0), rel, qv, tr.user);
+  };
+  trace_row(0, rel0);
+
+  // ---- cg_solve_lockstep
+  std::vector<double> rr(hred + C, hred + 2 * C), rr_next(C), pAp(C);
+  double joint0 = 0.0;
+  for (int c = 0; c < C; ++c) joint0 += rr[c];
+  const double rz = r0 > 0.0 ? r0 : std::sqrt(joint0);
+  std::vector<char> frozen(C, 0);
+  bool done = false;
+  if (rz == 0.0 || std::sqrt(joint0) <= tol * rz) {
+    out.converged = true;
+    out.final_rel = rz == 0.0 ? 0.0 : std::sqrt(joint0) / rz;
+    done = true;
+  }
+  if (!done) {
+    check_arg(o.cg_max_iterations >= 0, "SolverConfig: max_iterations must be non-negative");
+    check_arg(o.cg_check_interval >= 1, "SolverConfig: residual_check_interval must be >= 1");
+    const double freeze_sq = 1e-4 * tol * tol * rz * rz;
+    double rel = std::sqrt(joint0) / rz;
+    out.final_rel = rel;
+    const int maxit = o.cg_max_iterations;
+    for (int iter = 1; iter <= maxit; ++iter) {
+      unsigned active = 0;
+      for (int c = 0; c < C; ++c) {
+        if (frozen[c] || rr[c] <= freeze_sq) {
+          frozen[c] = 1;
+          rr_next[c] = rr[c];
+        } else {
+          active |= 1u << c;
+        }
+      }
+      if (active) {
+        Timed t(x, K_SWEEP, 2 * vec_bytes);
+        cg_apply_dot_kernel<T><<<grid, kRedThreads, 0, x.s>>>(V.mask, p, q, W, H, N, active, P(),
+                                                              red, tk());
+        CK(cudaGetLastError());
+      }
+      sync(x);
+      CgCoef alpha{};
+      unsigned upd = 0;
+      int broke = -1;
+      for (int c = 0; c < C; ++c) {
+        if (!((active >> c) & 1u)) continue;
+        const double pa = hred[c];
+        if (!(pa > 0.0) || !std::isfinite(pa)) {  // breakdown (cg.hpp:243-250)
+          broke = c;
+          break;
+        }
+        alpha.v[c] = rr[c] / pa;
+        upd |= 1u << c;
+      }
+      if (upd) {
+        Timed t(x, K_SWEEP, 5 * vec_bytes);
+        cg_update_kernel<T><<<grid, kRedThreads, 0, x.s>>>(xv, p, r, q, W, H, N, upd, alpha, P(),
+                                                           red, tk());
+        CK(cudaGetLastError());
+        sync(x);
+      }
+      if (broke >= 0) {
+        // (multilevel_solve reports only converged / not converged for a level)
+        out.iterations = iter - 1;
+        out.final_rel = rel;
+        done = true;
+        break;  // partially updated channels stay as the reference leaves them
+      }
+      double joint_sq = 0.0;
+      for (int c = 0; c < C; ++c) {
+        if ((active >> c) & 1u) rr_next[c] = hred[c];
+        joint_sq += rr_next[c];
+      }
+      const bool cadence = iter % o.cg_check_interval == 0 || iter == maxit;
+      const bool maybe_done = std::sqrt(joint_sq) <= tol * rz;
+      if (cadence || maybe_done) {
+        unsigned replace = 0;
+        for (int c = 0; c < C; ++c)
+          if (!frozen[c]) replace |= 1u << c;
+        {
+          Timed t(x, K_RESIDUAL, 3 * vec_bytes);
+          cg_true_residual_kernel<T><<<grid, kRedThreads, 0, x.s>>>(V.mask, rhs, xv, r, W, H, N,
+                                                                    replace, P(), red, tk());
+          CK(cudaGetLastError());
+        }
+        sync(x);
+        double true_sq = 0.0;
+        for (int c = 0; c < C; ++c) {
+          true_sq += hred[c];
+          if (!frozen[c]) rr_next[c] = hred[c];
+        }
+        rel = std::sqrt(true_sq) / rz;
+        out.final_rel = rel;
+        trace_row(iter, rel);
+        if (rel <= tol) {
+          out.iterations = iter;
+          out.converged = true;
+          done = true;
+          break;
+        }
+      }
+      CgCoef beta{};
+      unsigned pa = 0;
+      for (int c = 0; c < C; ++c) {
+        if (frozen[c]) continue;
+        beta.v[c] = rr[c] > 0.0 ? rr_next[c] / rr[c] : 0.0;
+        rr[c] = rr_next[c];
+        pa |= 1u << c;
+      }
+      if (pa) {
+        cg_pupdate_kernel<T><<<grid, kRedThreads, 0, x.s>>>(p, r, W, H, N, pa, beta);
+        CK(cudaGetLastError());
+      }
+    }
+    if (!done) out.iterations = maxit;
+  }
+  // embed_solution (reduction.hpp:138-145) into the level's iterate
+  cg_embed_kernel<T><<<grid, kRedThreads, 0, x.s>>>(V.mask, V.b, xv, V.u[V.cur ^ 1], W, H, N);
+  CK(cudaGetLastError());
+  V.cur ^= 1;
+  return out;
+}
+
 // fixed_block >= 0 selects solve_schwarz's explicit, unclamped partition
 // (schwarz.hpp:349-389) instead of clamped_partition per level.
 template <typename T>
@@ -534,21 +704,33 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
     }
     const bool finest = level == 0;
     const double tol = finest ? o.tolerance : o.coarse_tolerance;
+    const bool cg_level = flavour == kFlavourCg;
     Clamped cp{fixed_block, fixed_overlap};
-    if (fixed_block < 0) cp = clamp_partition(V.w, V.h, o.block_size, o.overlap);
+    if (!cg_level && fixed_block < 0) cp = clamp_partition(V.w, V.h, o.block_size, o.overlap);
     if (flavour == SI_FLAVOUR_ORAS)
       check_arg(std::isfinite(o.alpha), "run_schwarz_level: alpha must be finite");
     if (!known_checked) {
       // build_rhs rejects an empty mask (operators.hpp:83): read the count
       // taken by the ingest kernel.
       publish_counters(x, 3);
+      // reduce_structure's singularity check (reduction.hpp:84-112) can only
+      // fail when no pixel is known (a component of the unknown region that
+      // touches no known pixel is the whole grid); it runs before build_rhs.
+      if (cg_level && x.c.host_cnt[2] == 0)
+        fail(SI_ERR_RUNTIME,
+             "reduce_structure: singular system (an unknown region touches no known pixel)");
       check_arg(x.c.host_cnt[2] > 0, "build_rhs: mask has no known pixels");
       known_checked = true;
     }
-    double r0 = 0.0;
-    launch_r0<T>(x, V, C, o.normalizer);
-    const LevelOutcome oc = run_level<T>(x, V, C, cp.block, cp.overlap, &r0, true, tol, flavour, o,
-                                         true, finest, tr, finest ? d_ref : nullptr, rep);
+    LevelOutcome oc;
+    if (cg_level) {
+      oc = run_cg_level<T>(x, V, C, tol, o, finest, tr, finest ? d_ref : nullptr);
+    } else {
+      double r0 = 0.0;
+      launch_r0<T>(x, V, C, o.normalizer);
+      oc = run_level<T>(x, V, C, cp.block, cp.overlap, &r0, true, tol, flavour, o, true, finest,
+                        tr, finest ? d_ref : nullptr, rep);
+    }
     rep->level_iterations[level] = oc.iterations;
     rep->level_final_rel[level] = oc.final_rel;
     rep->level_converged[level] = oc.converged;
@@ -621,13 +803,15 @@ int levels_for(int method, const si_options& o) {
   return (method == SI_METHOD_MLORAS || method == SI_METHOD_MLCG) ? o.levels : 1;
 }
 
-int flavour_for(int method) { return method == SI_METHOD_RAS ? SI_FLAVOUR_RAS : SI_FLAVOUR_ORAS; }
+int flavour_for(int method) {
+  if (method == SI_METHOD_CG || method == SI_METHOD_MLCG) return kFlavourCg;
+  return method == SI_METHOD_RAS ? SI_FLAVOUR_RAS : SI_FLAVOUR_ORAS;
+}
 
 void check_method(int method) {
   check_arg(method >= SI_METHOD_CG && method <= SI_METHOD_MLORAS,
             "unknown method (expected cg, mlcg, ras, oras or mloras)");
-  if (method == SI_METHOD_CG || method == SI_METHOD_MLCG)
-    fail(SI_ERR_UNSUPPORTED, "method cg/mlcg is not provided by the B200 build (ORAS path only)");
+
 }
 
 void check_dims(int w, int h, int c) {
@@ -668,6 +852,7 @@ const char* si_status_string(si_status s) {
     case SI_ERR_OOM: return "out of memory";
     case SI_ERR_UNSUPPORTED: return "unsupported";
     case SI_ERR_NO_DEVICE: return "no device";
+    case SI_ERR_RUNTIME: return "runtime error";
   }
   return "unknown";
 }
@@ -744,7 +929,8 @@ void si_destroy(si_ctx* c) {
     l.u1.release();
   }
   for (DevBuf* b : {&c->in_f, &c->in_mask, &c->in_ref, &c->out_img, &c->aux, &c->red_partials,
-                    &c->red_out, &c->counters, &c->ticket, &c->scratch})
+                    &c->red_out, &c->counters, &c->ticket, &c->scratch, &c->cg_rhs, &c->cg_x,
+                    &c->cg_r, &c->cg_p, &c->cg_q})
     b->release();
   for (auto& p : c->pending) {
     cudaEventDestroy(p.start);

@@ -49,6 +49,15 @@ SMALL = [
 ]
 
 
+CG_CASES = [
+    # w, h, c, density, seed, method, options
+    (256, 256, 1, 0.05, 1, "mlcg", dict(levels=2)),
+    (64, 48, 3, 0.07, 2, "cg", dict(levels=1, tolerance=1e-6)),
+    (123, 77, 3, 0.04, 3, "mlcg", dict(levels=3, cg_check_interval=1)),
+    (40, 30, 2, 0.1, 4, "cg", dict(levels=1, cg_max_iterations=5)),
+]
+
+
 def sha(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
@@ -93,6 +102,19 @@ def main():
                                "d": max(d, 1.5 / (w * h)), "seed_image": 1000 + seed,
                                "seed_mask": 77 + seed, "options": opts}
     np.savez_compressed(os.path.join(HERE, "small.npz"), **small)
+
+    # multilevel CG (the paper's baseline method) through run_method itself
+    cg = {}
+    for i, (w, h, c, d, seed, meth, opts) in enumerate(CG_CASES):
+        f, m = instance(w, h, c, d, 2000 + seed, 99 + seed)
+        run = P.ref_run_method(meth, f, m, flavour=2, **opts)
+        cg[f"case{i}_image"] = run.image
+        cg[f"case{i}_trace"] = run.trace
+        cg[f"case{i}_iterations"] = np.array([run.iterations, int(run.converged)])
+        hashes[f"cg{i}"] = {"image": sha(f), "mask": sha(m), "w": w, "h": h, "c": c, "d": d,
+                            "seed_image": 2000 + seed, "seed_mask": 99 + seed, "method": meth,
+                            "options": opts}
+    np.savez_compressed(os.path.join(HERE, "cg.npz"), **cg)
 
     # kernel probes: restriction (both averagings), prolongation, local operator
     k = {}

@@ -66,11 +66,12 @@ def test_option_validation_messages(kw, msg):
     assert msg in lib.si_last_error().decode()
 
 
-def test_cg_methods_are_reported_unsupported():
+def test_every_method_validates():
     lib = L.load()
     o = si.RunOptions().to_c()
-    assert lib.si_validate_options(int(si.Method.MultilevelCg), C.byref(o)) == L.SI_ERR_UNSUPPORTED
-    assert lib.si_validate_options(int(si.Method.Oras), C.byref(o)) == L.SI_OK
+    for m in si.Method:
+        assert lib.si_validate_options(int(m), C.byref(o)) == L.SI_OK
+    assert lib.si_validate_options(7, C.byref(o)) == L.SI_ERR_INVALID_ARGUMENT
 
 
 # ------------------------------------------------------------- partition

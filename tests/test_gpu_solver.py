@@ -45,7 +45,9 @@ def opts_dict(o: si.RunOptions, method):
                 local_tolerance=o.local.tolerance, local_max_iterations=o.local.max_iterations,
                 local_check_interval=o.local.residual_check_interval,
                 max_outer_iterations=o.max_outer_iterations, normalizer=int(o.normalizer),
-                flavour=0 if method == si.Method.Ras else 1)
+                flavour=(2 if method in (si.Method.Cg, si.Method.MultilevelCg) else
+                         0 if method == si.Method.Ras else 1),
+                cg_max_iterations=o.cg_max_iterations, cg_check_interval=o.cg_check_interval)
 
 
 @pytest.mark.parametrize("precision,bar", [(si.Precision.FP64, FP64), (si.Precision.FP32, FP32)])
@@ -281,8 +283,8 @@ def test_errors_mirror_reference(solver):
         solver.run_method(si.Method.Oras, f, si.InpaintingMask(8, 16, 1))
     with pytest.raises(si.InvalidArgument, match="alpha must be finite"):
         solver.run_method(si.Method.Oras, f, m, si.RunOptions(alpha=float("nan")))
-    with pytest.raises(si.Unsupported):
-        solver.run_method(si.Method.MultilevelCg, f, m)
+    with pytest.raises(si.SolverError, match="singular system"):  # reduction.hpp:109-110
+        solver.run_method(si.Method.MultilevelCg, f, si.InpaintingMask(16, 16))
 
 
 def test_non_convergence_is_reported_not_raised(solver):
@@ -303,3 +305,34 @@ def test_batch_equals_individual_solves(solver):
         assert np.array_equal(single.image.data, b.image.data)
         assert single.report.level_iterations == b.report.level_iterations
         assert b.report.converged
+
+
+# ---------------------------------------------------------------- multilevel CG
+CG_CASES = [
+    (si.Method.MultilevelCg, C1, dict(levels=2)),
+    (si.Method.Cg, (64, 48, 3, 0.07, 1), dict(tolerance=1e-6)),
+    (si.Method.MultilevelCg, (123, 77, 3, 0.04, 3), dict(cg_check_interval=1)),
+    (si.Method.MultilevelCg, (96, 96, 1, 0.3, 3), dict(tolerance=1e-8, cg_check_interval=3)),
+    (si.Method.Cg, (40, 30, 2, 0.1, 1), dict(cg_max_iterations=5)),   # hits the cap
+]
+
+
+@pytest.mark.parametrize("method,cfg,kw", CG_CASES)
+def test_cg_level_solver_matches_oracle(solver, oracle, method, cfg, kw):
+    """run_cg_level + cg_solve_lockstep (multilevel.hpp:162-209, cg.hpp:192-291)."""
+    w, h, c, d, _ = cfg
+    f, m = random_instance(w, h, d, c, 500 + w)
+    o = si.RunOptions(**kw)
+    res = solver.run_method(method, f, m, o)
+    ora = oracle.oracle_solve(f.data, m.known, **opts_dict(o, method))
+    compare(res, ora, FP64, levels=False)
+
+
+@pytest.mark.slow
+def test_c2_mlcg_matches_oracle(solver, oracle):
+    f, m = config_instance(C2)
+    o = si.RunOptions(levels=2)
+    res = solver.run_method(si.Method.MultilevelCg, f, m, o)
+    ora = oracle.oracle_solve(f.data, m.known, **opts_dict(o, si.Method.MultilevelCg))
+    assert ora.iterations == 17
+    compare(res, ora, FP64, levels=False)

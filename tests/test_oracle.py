@@ -81,6 +81,23 @@ def test_oracle_small_cases(oracle):
     assert i == 12
 
 
+def test_oracle_cg_cases(oracle):
+    """The CG level solver restatement (reduction.hpp, cg.hpp:192-291) against
+    run_method("cg"/"mlcg") of the reference."""
+    g = np.load(os.path.join(GOLD, "cg.npz"))
+    i = 0
+    while f"case{i}_image" in g:
+        cfg = INPUTS[f"cg{i}"]
+        f, m = gen(cfg["w"], cfg["h"], cfg["c"], cfg["d"], cfg["seed_image"], cfg["seed_mask"])
+        res = oracle.oracle_solve(f, m, flavour=2, **cfg["options"])
+        its, conv = g[f"case{i}_iterations"]
+        assert (res.iterations, int(res.converged)) == (its, conv)
+        assert np.allclose(res.trace, g[f"case{i}_trace"], rtol=1e-12, atol=0)
+        assert np.abs(res.image - g[f"case{i}_image"]).max() <= 1e-12
+        i += 1
+    assert i == 4
+
+
 def test_oracle_kernels_bitwise(oracle):
     g = np.load(os.path.join(GOLD, "kernels.npz"))
     for avg in (0, 1):
