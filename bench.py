@@ -288,6 +288,25 @@ def main():
     t_e2e = max_over_ranks(time.perf_counter() - t0)
     e2e_value = world * e2e_steps / t_e2e
 
+    # ---- the same through the CLI's wire format (P6 pixels + P4 mask in, P6
+    # out; read_pnm/write_pnm decode and quantise run on the device)
+    pnm_in, pnm_out = [], []
+    for j in range(len(pinned_in)):
+        px = torch.empty((H4K, W4K, C4K), dtype=torch.uint8).pin_memory()
+        pb = torch.empty((H4K, (W4K + 7) // 8), dtype=torch.uint8).pin_memory()
+        px.numpy()[...] = si.quantise_pnm(frames[j][0])
+        pb.numpy()[...] = si.pack_pbm(frames[j][1])
+        pnm_in.append((px.numpy(), pb.numpy()))
+    for j in range(e2e_steps):
+        pnm_out.append(torch.empty((H4K, W4K, C4K), dtype=torch.uint8).pin_memory().numpy())
+    pnm_frames = [pnm_in[j % len(pnm_in)] for j in range(e2e_steps)]
+    solver.run_pnm_batch(si.Method.MultilevelOras, pnm_frames[:2], opts, pnm_out[:2])  # warm
+    barrier()
+    t0 = time.perf_counter()
+    solver.run_pnm_batch(si.Method.MultilevelOras, pnm_frames, opts, pnm_out)
+    t_pnm = max_over_ranks(time.perf_counter() - t0)
+    pnm_value = world * e2e_steps / t_pnm
+
     # ---- roofline of the dominant kernel (K2 sweep)
     sw = stats["sweep"]
     peaks = {}
@@ -331,6 +350,11 @@ def main():
                 "d2h_bytes_per_step": int(C4K * n * 8),
                 "api": "si_run_method_batch (host f64 planar + u8 mask in, f64 out; pinned)",
                 "frames": e2e_steps},
+        "e2e_pnm": {"value": pnm_value, "unit": "frames/s",
+                    "h2d_bytes_per_step": int(C4K * n + H4K * ((W4K + 7) // 8)),
+                    "d2h_bytes_per_step": int(C4K * n),
+                    "api": "si_run_pnm_batch (P6 + P4 payloads in, P6 out; pinned)",
+                    "frames": e2e_steps},
         "gpu_launches": int(stats["total_launches"]),
         "clocks": clk,
         "outer_iterations_per_level": list(iters[-1]) if iters else None,

@@ -140,6 +140,16 @@ si_status si_run_method_batch(si_ctx* ctx, int method, int n, const double* cons
                               const uint8_t* const* mask, int w, int h, int c,
                               const si_options* opt, double* const* out, si_report* reports);
 
+/* The CLI's wire format (pnm.hpp): pixels[k] is a P5/P6 payload (w*h*c bytes,
+ * interleaved, value = byte/255, c = 1 or 3), mask_pbm[k] a P4 payload
+ * ((w+7)/8 bytes per row, MSB first, bit 1 = known), out_pixels[k] receives the
+ * P5/P6 payload of the result (clamp to [0,1], lround(255 v): write_pnm,
+ * pnm.hpp:130-147).  Decoding and quantisation run on the device, so a 4K RGB
+ * frame moves 25 MB + 1 MB in and 25 MB out instead of 207 MB + 199 MB. */
+si_status si_run_pnm_batch(si_ctx* ctx, int method, int n, const uint8_t* const* pixels,
+                           const uint8_t* const* mask_pbm, int w, int h, int c,
+                           const si_options* opt, uint8_t* const* out_pixels, si_report* reports);
+
 /* solve_schwarz(f, mask, partition_domain(w,h,block,overlap), options, reference)
  * (schwarz.hpp:349-389): single level on an explicit, unclamped partition.
  * flavour: si_flavour; host buffers. */

@@ -93,6 +93,8 @@ SIGNATURES = {
                                   _vp, C.POINTER(si_report), TRACE_FN, _vp, _vp]),
     "si_run_method_batch": (_i, [_vp, _i, _i, C.POINTER(_vp), C.POINTER(_vp), _i, _i, _i,
                                  C.POINTER(si_options), C.POINTER(_vp), C.POINTER(si_report)]),
+    "si_run_pnm_batch": (_i, [_vp, _i, _i, C.POINTER(_vp), C.POINTER(_vp), _i, _i, _i,
+                              C.POINTER(si_options), C.POINTER(_vp), C.POINTER(si_report)]),
     "si_solve_schwarz": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _i, _i, C.POINTER(si_options), _vp,
                               _vp, C.POINTER(si_report), TRACE_FN, _vp]),
     "si_run_schwarz_level": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _i, _i, _d, _d, _i,

@@ -414,6 +414,34 @@ class Solver:
                                              f0.channels, C.byref(o), op, reps))
         return [SolveResult(outs[k], ConvergenceTrace(), _report(reps[k])) for k in range(n)]
 
+    def run_pnm_batch(self, method: Method, frames, options: Optional[RunOptions] = None,
+                      outputs=None) -> List[SolveReport]:
+        """The CLI wire format (pnm.hpp) end to end on the device: frames is a
+        list of (pixels, mask_pbm) with pixels the P5/P6 payload as a uint8 array
+        (h, w) or (h, w, 3) and mask_pbm the P4 payload (h, (w+7)//8) uint8;
+        returns (reports, outputs) with outputs the P5/P6 payloads."""
+        options = options or RunOptions()
+        n = len(frames)
+        if n == 0:
+            return [], []
+        px0 = np.asarray(frames[0][0])
+        h, w = px0.shape[:2]
+        c = 1 if px0.ndim == 2 else px0.shape[2]
+        ins = [np.ascontiguousarray(p, dtype=np.uint8) for p, _ in frames]
+        masks = [np.ascontiguousarray(m, dtype=np.uint8) for _, m in frames]
+        for p_, m_ in zip(ins, masks):
+            if p_.shape != px0.shape or m_.shape != (h, (w + 7) // 8):
+                raise InvalidArgument("run_pnm_batch: frames must share one shape")
+        outs = outputs or [np.empty_like(ins[0]) for _ in range(n)]
+        ip = (C.c_void_p * n)(*[a.ctypes.data for a in ins])
+        mp = (C.c_void_p * n)(*[a.ctypes.data for a in masks])
+        op = (C.c_void_p * n)(*[a.ctypes.data for a in outs])
+        reps = (L.si_report * n)()
+        o = options.to_c()
+        _check(self._lib.si_run_pnm_batch(self._h, int(method), n, ip, mp, w, h, c, C.byref(o),
+                                          op, reps))
+        return [_report(reps[k]) for k in range(n)], outs
+
     def solve_schwarz(self, f: ImageBuffer, mask: InpaintingMask, partition: SubdomainPartition,
                       options: Optional[SchwarzSolveOptions] = None,
                       reference: Optional[ImageBuffer] = None) -> SolveResult:
@@ -661,6 +689,20 @@ def random_mask(width: int, height: int, density: float, seed: int) -> Inpaintin
     if st != L.SI_OK:
         raise InvalidArgument("random_mask: invalid dimensions or density")
     return InpaintingMask(known=out)
+
+
+def pack_pbm(mask: InpaintingMask) -> np.ndarray:
+    """P4 payload of a mask (write_mask_pbm, pnm.hpp:190-205): MSB first, rows padded."""
+    return np.packbits(mask.known != 0, axis=1, bitorder="big")
+
+
+def quantise_pnm(img: ImageBuffer) -> np.ndarray:
+    """P5/P6 payload of an image (write_pnm's quantise, pnm.hpp:82-85): clamp to
+    [0, 1] and round half away from zero; (h, w) or (h, w, 3) uint8."""
+    v = np.clip(img.data, 0.0, 1.0) * 255.0
+    fl = np.floor(v)
+    q = (fl + (v - fl >= 0.5)).astype(np.uint8)
+    return q[0] if img.channels == 1 else np.ascontiguousarray(np.moveaxis(q, 0, -1))
 
 
 def mse_per_channel(u: ImageBuffer, f: ImageBuffer) -> List[float]:

@@ -361,6 +361,33 @@ __global__ void __launch_bounds__(256, 4)
   }
 }
 
+// read_pnm / read_mask_pbm payloads (pnm.hpp:98-188): interleaved bytes ->
+// planar f = byte / 255.0; P4 bits (MSB first, rows padded to bytes) -> mask.
+__global__ void unpack_pnm_kernel(const uint8_t* __restrict__ pix, const uint8_t* __restrict__ pbm,
+                                  int W, int H, int C, double* __restrict__ f,
+                                  uint8_t* __restrict__ mask) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= W) return;
+  const size_t N = static_cast<size_t>(W) * H, row_bytes = (static_cast<size_t>(W) + 7) / 8;
+  for (int y = blockIdx.y; y < H; y += gridDim.y) {
+    const size_t i = static_cast<size_t>(y) * W + x;
+    for (int c = 0; c < C; ++c) f[c * N + i] = pix[i * C + c] / 255.0;
+    mask[i] = (pbm[y * row_bytes + x / 8] >> (7 - x % 8)) & 1;
+  }
+}
+
+// quantise (pnm.hpp:82-85): clamp to [0, 1], lround(255 v); planar -> interleaved.
+__global__ void quantise_kernel(const double* __restrict__ u, size_t N, int C,
+                                uint8_t* __restrict__ out) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < N; i += stride)
+    for (int c = 0; c < C; ++c) {
+      const double v = u[c * N + i];
+      const double cl = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+      out[i * C + c] = static_cast<uint8_t>(llround(cl * 255.0));
+    }
+}
+
 template <typename Tin, typename Tout>
 __global__ void convert_kernel(const Tin* __restrict__ in, Tout* __restrict__ out, size_t n) {
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;

@@ -836,6 +836,83 @@ void run_device(si_ctx* ctx, int method, const double* d_f, const uint8_t* d_mas
   end_counters(x, rep);
 }
 
+// Batch pipeline shared by si_run_method_batch (f64 planar in/out) and
+// si_run_pnm_batch (PNM/PBM payloads in/out): two staging slots, H2D of frame
+// k+1 and D2H of frame k-1 on their own streams while frame k is solved.
+void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint8_t* const* mask,
+               int w, int h, int c, const si_options* opt, void* const* out, si_report* reports,
+               bool pnm) {
+  check_dims(w, h, c);
+  si_options o;
+  if (opt) o = *opt; else si_default_options(&o);
+  set_device(ctx);
+  if (!ctx->h2d_stream) {
+    CK(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaEventCreateWithFlags(&ctx->ev_h2d[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_solved[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_d2h[k], cudaEventDisableTiming));
+    }
+  }
+  const size_t n_px = static_cast<size_t>(w) * h, img = n_px * c * sizeof(double);
+  const size_t row_bytes = (static_cast<size_t>(w) + 7) / 8;
+  const size_t in_bytes = pnm ? n_px * c : img, mask_bytes = pnm ? row_bytes * h : n_px;
+  const size_t out_bytes = pnm ? n_px * c : img;
+  for (int k = 0; k < 2; ++k) {
+    ctx->slot_f[k].ensure(img + (pnm ? in_bytes + 16 : 0));
+    ctx->slot_mask[k].ensure(n_px + (pnm ? mask_bytes + 16 : 0));
+    ctx->slot_out[k].ensure(img + (pnm ? out_bytes + 16 : 0));
+  }
+  // pnm: the raw payloads sit behind the decoded buffers in the same slot
+  auto raw_in = [&](int s) { return ctx->slot_f[s].as<uint8_t>() + (pnm ? img : 0); };
+  auto raw_mask = [&](int s) { return ctx->slot_mask[s].as<uint8_t>() + (pnm ? n_px : 0); };
+  auto raw_out = [&](int s) { return ctx->slot_out[s].as<uint8_t>() + (pnm ? img : 0); };
+  auto h2d = [&](int k) {
+    const int s = k & 1;
+    CK(cudaMemcpyAsync(raw_in(s), in[k], in_bytes, cudaMemcpyHostToDevice, ctx->h2d_stream));
+    CK(cudaMemcpyAsync(raw_mask(s), mask[k], mask_bytes, cudaMemcpyHostToDevice,
+                       ctx->h2d_stream));
+    CK(cudaEventRecord(ctx->ev_h2d[s], ctx->h2d_stream));
+  };
+  cudaStream_t cs = ctx->own_stream;
+  if (n > 0) h2d(0);
+  for (int k = 0; k < n; ++k) {
+    const int s = k & 1;
+    // the other slot's input was consumed by frame k-1 (solved synchronously)
+    if (k + 1 < n) h2d(k + 1);
+    CK(cudaStreamWaitEvent(cs, ctx->ev_h2d[s], 0));
+    if (k >= 2) CK(cudaStreamWaitEvent(cs, ctx->ev_d2h[s], 0));  // out slot free again
+    si_report local;
+    si_report* rep = reports ? &reports[k] : &local;
+    clear_report(rep);
+    const auto t0 = Clock::now();
+    if (pnm) {
+      // read_pnm / read_mask_pbm (pnm.hpp:98-188) on device
+      unpack_pnm_kernel<<<dim3((w + 255) / 256, std::min(h, 65535)), 256, 0, cs>>>(
+          raw_in(s), raw_mask(s), w, h, c, ctx->slot_f[s].as<double>(),
+          ctx->slot_mask[s].as<uint8_t>());
+      CK(cudaGetLastError());
+    }
+    run_device(ctx, method, ctx->slot_f[s].as<double>(), ctx->slot_mask[s].as<uint8_t>(), w, h, c,
+               o, nullptr, ctx->slot_out[s].as<double>(), rep, nullptr, nullptr, cs, t0);
+    if (pnm) {
+      // write_pnm's quantise (pnm.hpp:82-85, 130-147)
+      quantise_kernel<<<grid_for(n_px, 256, 148 * 16), 256, 0, cs>>>(
+          ctx->slot_out[s].as<double>(), n_px, c, raw_out(s));
+      CK(cudaGetLastError());
+    }
+    rep->elapsed_ms = ms_since(t0);
+    CK(cudaEventRecord(ctx->ev_solved[s], cs));
+    CK(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_solved[s], 0));
+    CK(cudaMemcpyAsync(out[k], raw_out(s), out_bytes, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    CK(cudaEventRecord(ctx->ev_d2h[s], ctx->d2h_stream));
+  }
+  CK(cudaStreamSynchronize(ctx->d2h_stream));
+  CK(cudaStreamSynchronize(ctx->h2d_stream));
+  CK(cudaStreamSynchronize(cs));
+}
+
 }  // namespace
 
 extern "C" {
@@ -1028,55 +1105,19 @@ si_status si_run_method_batch(si_ctx* ctx, int method, int n, const double* cons
                               const si_options* opt, double* const* out, si_report* reports) {
   return guard([&] {
     check_arg(ctx && f && mask && out && n >= 0, "null argument");
-    check_dims(w, h, c);
-    si_options o;
-    if (opt) o = *opt; else si_default_options(&o);
-    set_device(ctx);
-    if (!ctx->h2d_stream) {
-      CK(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
-      for (int k = 0; k < 2; ++k) {
-        CK(cudaEventCreateWithFlags(&ctx->ev_h2d[k], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ctx->ev_solved[k], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ctx->ev_d2h[k], cudaEventDisableTiming));
-      }
-    }
-    const size_t n_px = static_cast<size_t>(w) * h, img = n_px * c * sizeof(double);
-    for (int k = 0; k < 2; ++k) {
-      ctx->slot_f[k].ensure(img);
-      ctx->slot_mask[k].ensure(n_px);
-      ctx->slot_out[k].ensure(img);
-    }
-    auto h2d = [&](int k) {
-      const int s = k & 1;
-      CK(cudaMemcpyAsync(ctx->slot_f[s].ptr, f[k], img, cudaMemcpyHostToDevice, ctx->h2d_stream));
-      CK(cudaMemcpyAsync(ctx->slot_mask[s].ptr, mask[k], n_px, cudaMemcpyHostToDevice,
-                         ctx->h2d_stream));
-      CK(cudaEventRecord(ctx->ev_h2d[s], ctx->h2d_stream));
-    };
-    cudaStream_t cs = ctx->own_stream;
-    if (n > 0) h2d(0);
-    for (int k = 0; k < n; ++k) {
-      const int s = k & 1;
-      // the other slot's input was consumed by frame k-1 (solved synchronously)
-      if (k + 1 < n) h2d(k + 1);
-      CK(cudaStreamWaitEvent(cs, ctx->ev_h2d[s], 0));
-      if (k >= 2) CK(cudaStreamWaitEvent(cs, ctx->ev_d2h[s], 0));  // out slot free again
-      si_report local;
-      si_report* rep = reports ? &reports[k] : &local;
-      clear_report(rep);
-      const auto t0 = Clock::now();
-      run_device(ctx, method, ctx->slot_f[s].as<double>(), ctx->slot_mask[s].as<uint8_t>(), w, h,
-                 c, o, nullptr, ctx->slot_out[s].as<double>(), rep, nullptr, nullptr, cs, t0);
-      rep->elapsed_ms = ms_since(t0);
-      CK(cudaEventRecord(ctx->ev_solved[s], cs));
-      CK(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_solved[s], 0));
-      CK(cudaMemcpyAsync(out[k], ctx->slot_out[s].ptr, img, cudaMemcpyDeviceToHost,
-                         ctx->d2h_stream));
-      CK(cudaEventRecord(ctx->ev_d2h[s], ctx->d2h_stream));
-    }
-    CK(cudaStreamSynchronize(ctx->d2h_stream));
-    CK(cudaStreamSynchronize(ctx->h2d_stream));
+    run_batch(ctx, method, n, reinterpret_cast<const void* const*>(f), mask, w, h, c, opt,
+              reinterpret_cast<void* const*>(out), reports, false);
+  });
+}
+
+si_status si_run_pnm_batch(si_ctx* ctx, int method, int n, const uint8_t* const* pixels,
+                           const uint8_t* const* mask_pbm, int w, int h, int c,
+                           const si_options* opt, uint8_t* const* out_pixels, si_report* reports) {
+  return guard([&] {
+    check_arg(ctx && pixels && mask_pbm && out_pixels && n >= 0, "null argument");
+    check_arg(c == 1 || c == 3, "write_pnm: only 1- or 3-channel images are supported");
+    run_batch(ctx, method, n, reinterpret_cast<const void* const*>(pixels), mask_pbm, w, h, c,
+              opt, reinterpret_cast<void* const*>(out_pixels), reports, true);
   });
 }
 

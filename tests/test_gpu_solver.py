@@ -336,3 +336,27 @@ def test_c2_mlcg_matches_oracle(solver, oracle):
     ora = oracle.oracle_solve(f.data, m.known, **opts_dict(o, si.Method.MultilevelCg))
     assert ora.iterations == 17
     compare(res, ora, FP64, levels=False)
+
+
+# ---------------------------------------------------------------- PNM wire format
+@pytest.mark.parametrize("w,h,c", [(160, 120, 3), (97, 61, 1), (256, 256, 3)])
+def test_pnm_batch_matches_decoded_pipeline(solver, oracle, w, h, c):
+    """read_pnm -> run_method -> write_pnm (pnm.hpp) with decode/quantise on the
+    device equals the same pipeline through the f64 API (bit-exact bytes), and
+    the CPU oracle's pipeline up to rounding-boundary bytes."""
+    frames, decoded = [], []
+    for k in range(3):
+        f, m = random_instance(w, h, 0.06, c, 40 + k)
+        px = si.quantise_pnm(f)
+        frames.append((px, si.pack_pbm(m)))
+        fd = (px.astype(np.float64) / 255.0)
+        fd = fd[None] if c == 1 else np.moveaxis(fd, -1, 0)
+        decoded.append((si.ImageBuffer(data=fd), m))
+    reps, outs = solver.run_pnm_batch(si.Method.MultilevelOras, frames, si.RunOptions(levels=2))
+    for (fd, m), rep, out in zip(decoded, reps, outs):
+        ref = solver.run_method(si.Method.MultilevelOras, fd, m, si.RunOptions(levels=2))
+        assert rep.level_iterations == ref.report.level_iterations
+        assert np.array_equal(out, si.quantise_pnm(ref.image))
+        ora = oracle.oracle_solve(fd.data, m.known, levels=2)
+        diff = np.abs(out.astype(int) - si.quantise_pnm(si.ImageBuffer(data=ora.image)).astype(int))
+        assert diff.max() <= 1 and np.count_nonzero(diff) <= max(1, diff.size // 10000)
