@@ -251,11 +251,41 @@ double si_joint_norm(const double* sumsq, int c);
 /* mse_per_channel / psnr (metrics.hpp:30-56) on host buffers. */
 si_status si_psnr(const double* u, const double* f, int w, int h, int c, double* psnr_db);
 
+/* ---- Voronoi densification (masks.hpp:45-215) -------------------------- */
+
+/* DensifyOptions (masks.hpp:145-151). */
+typedef struct si_densify_options {
+  double initial_density;  /* <= 0: start at a quarter of the target */
+  double cell_fraction;    /* share of cells refined per sweep (0.20) */
+  double inner_tolerance;  /* tolerance of the guiding inpainting runs (1e-3) */
+  int max_sweeps;          /* 100 */
+  si_options solve;        /* MultilevelSolveOptions of the guide solver (multilevel
+                              ORAS); its tolerance is replaced by inner_tolerance */
+} si_densify_options;
+void si_default_densify_options(si_densify_options* o);
+/* voronoi_densify(f, target_density, seed, options) (masks.hpp:155-212):
+ * grows random_mask(w, h, initial, seed) towards round(target * w * h) known
+ * pixels; every sweep inpaints with the multilevel ORAS path, assigns Voronoi
+ * cells, ranks them by (squared error desc, area desc, site index asc) and
+ * plants a known pixel at the worst pixel of the first
+ * max(1, cell_fraction * sites) cells.  The whole loop runs on the device.
+ * mask_out: w*h bytes.  Invalid targets -> SI_ERR_INVALID_ARGUMENT with the
+ * reference's messages (masks.hpp:157-160). */
+si_status si_voronoi_densify(si_ctx* ctx, const double* f, int w, int h, int c,
+                             double target_density, uint64_t seed, const si_densify_options* opt,
+                             uint8_t* mask_out, int* sweeps, int* reached_target);
+/* assign_nearest_site (masks.hpp:54-139): sites = known pixel indices in
+ * ascending order (capacity w*h), site_of[p] = index of p's nearest site
+ * (squared Euclidean distance, ties to the lower site index). */
+si_status si_assign_nearest_site(si_ctx* ctx, const uint8_t* mask, int w, int h, int32_t* sites,
+                                 int32_t* site_of, int* num_sites);
+
 /* ---- instrumentation ---------------------------------------------------- */
 
 /* Per-kernel device time (CUDA events on the launching stream) accumulated
  * while profiling is enabled; kind: 0 residual (K1), 1 sweep (K2), 2 restrict
- * (K3), 3 prolong (K4), 4 ingest/export (K5), 5 metrics (K6).
+ * (K3), 3 prolong (K4), 4 ingest/export (K5), 5 metrics (K6), 6 Voronoi
+ * densification (D1-D6).
  * total_launches counts every kernel launched by the context, always. */
 typedef struct si_kernel_stats {
   long long launches[8];

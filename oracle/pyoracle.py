@@ -106,6 +106,11 @@ def _load_oracle():
                                             C.c_int, C.c_int, C.c_double, _f64, _f64]
     lib.or_partition_axis.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
                                       C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    _i32 = _P(dtype=np.int32, flags="C_CONTIGUOUS")
+    lib.or_assign_nearest_site.argtypes = [_u8, C.c_int, C.c_int, _i32, _i32, C.POINTER(C.c_int)]
+    lib.or_voronoi_densify.argtypes = [_f64, C.c_int, C.c_int, C.c_int, _u8, C.c_longlong,
+                                       C.c_double, C.c_double, C.c_int, C.POINTER(Options), _u8,
+                                       C.POINTER(C.c_int)]
     return lib
 
 
@@ -157,6 +162,11 @@ def ref():
                                               _f64, C.c_int, ip]
         lib.ref_canonical_r0.argtypes = [_u8, C.c_int, C.c_int, C.c_int, _f64, C.c_int]
         lib.ref_canonical_r0.restype = C.c_double
+        _i32 = _P(dtype=np.int32, flags="C_CONTIGUOUS")
+        lib.ref_assign_nearest_site.argtypes = [_u8, C.c_int, C.c_int, _i32, _i32, ip]
+        lib.ref_voronoi_densify.argtypes = [_f64, C.c_int, C.c_int, C.c_int, C.c_double,
+                                            C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                            C.c_int, C.POINTER(Options), _u8, ip, ip]
         _ref = lib
     return _ref
 
@@ -313,3 +323,68 @@ def oracle_partition_axis(extent, block, overlap):
     cnt = C.c_int()
     oracle().or_partition_axis(extent, block, overlap, a, C.byref(cnt), e)
     return list(a[: cnt.value]), list(e[: cnt.value])
+
+
+# ---------------------------------------------------------------- densification
+def _assign(fn, mask):
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    h, w = m.shape
+    sites = np.empty(w * h, np.int32)
+    site_of = np.empty(w * h, np.int32)
+    k = C.c_int()
+    if fn(m.ravel(), w, h, sites, site_of, C.byref(k)) != 0:
+        raise ValueError("assign_nearest_site: mask has no known pixels")
+    return sites[: k.value].copy(), site_of.reshape(h, w)
+
+
+def oracle_assign_nearest_site(mask):
+    """(sites, site_of) of the C restatement (masks.hpp:54-139)."""
+    return _assign(oracle().or_assign_nearest_site, mask)
+
+
+def ref_assign_nearest_site(mask):
+    return _assign(ref().ref_assign_nearest_site, mask)
+
+
+def densify_seed_density(target: float, n: int, initial: float = 0.0) -> float:
+    """Starting density of voronoi_densify (masks.hpp:166-167)."""
+    init = initial if initial > 0.0 else target / 4.0
+    return 1.5 / n if init * n < 1.0 else init
+
+
+def densify_target(target: float, n: int) -> int:
+    """target_k of masks.hpp:163-165 (llround = half away from zero)."""
+    v = target * n
+    k = int(np.floor(v + 0.5)) if v >= 0 else int(np.ceil(v - 0.5))
+    return max(1, min(n, k))
+
+
+def oracle_voronoi_densify(f, seed_mask, target, cell_fraction=0.20, inner_tolerance=1e-3,
+                           max_sweeps=100, **opts):
+    """voronoi_densify of the C restatement from the seed mask; (mask, sweeps)."""
+    f = _flat(f)
+    c, h, w = f.shape
+    o = default_options(**opts)
+    out = np.empty((h, w), np.uint8)
+    sw = C.c_int()
+    seed = np.ascontiguousarray(seed_mask, dtype=np.uint8)
+    if oracle().or_voronoi_densify(f.ravel(), w, h, c, seed.ravel(), densify_target(target, w * h),
+                                   cell_fraction, inner_tolerance, max_sweeps, C.byref(o),
+                                   out.ravel(), C.byref(sw)) != 0:
+        raise ValueError("oracle: invalid argument")
+    return out, sw.value
+
+
+def ref_voronoi_densify(f, target, seed, initial_density=0.0, cell_fraction=0.20,
+                        inner_tolerance=1e-3, max_sweeps=100, **opts):
+    """schwarz_inpaint::voronoi_densify; returns (mask, sweeps, reached)."""
+    f = _flat(f)
+    c, h, w = f.shape
+    o = default_options(**opts)
+    out = np.empty((h, w), np.uint8)
+    sw, rc_ = C.c_int(), C.c_int()
+    if ref().ref_voronoi_densify(f.ravel(), w, h, c, target, seed, initial_density, cell_fraction,
+                                 inner_tolerance, max_sweeps, C.byref(o), out.ravel(),
+                                 C.byref(sw), C.byref(rc_)) != 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return out, sw.value, bool(rc_.value)

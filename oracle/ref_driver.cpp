@@ -361,4 +361,55 @@ double ref_canonical_r0(const uint8_t* mask, int w, int h, int c, const double* 
                                      : si::ResidualNormalizer::InitialGuess);
 }
 
+// assign_nearest_site (masks.hpp:54-139) as the reference computes it.
+int ref_assign_nearest_site(const uint8_t* mask, int w, int h, int32_t* sites, int32_t* site_of,
+                            int* num_sites) {
+  try {
+    auto a = si::assign_nearest_site(make_mask(mask, w, h));
+    std::memcpy(sites, a.sites.data(), sizeof(int32_t) * a.sites.size());
+    std::memcpy(site_of, a.site_of.data(), sizeof(int32_t) * a.site_of.size());
+    *num_sites = static_cast<int>(a.sites.size());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// voronoi_densify (masks.hpp:155-212); the guide solver's options come from
+// RefOptions (MultilevelSolveOptions, multilevel.hpp:132-142).
+int ref_voronoi_densify(const double* f, int w, int h, int c, double target, uint64_t seed,
+                        double initial_density, double cell_fraction, double inner_tolerance,
+                        int max_sweeps, const RefOptions* o, uint8_t* mask_out, int* sweeps,
+                        int* reached) {
+  try {
+    si::DensifyOptions d;
+    d.initial_density = initial_density;
+    d.cell_fraction = cell_fraction;
+    d.inner_tolerance = inner_tolerance;
+    d.max_sweeps = max_sweeps;
+    d.solve.levels = o->levels;
+    d.solve.tolerance = o->tolerance;
+    d.solve.coarse_tolerance = o->coarse_tolerance;
+    d.solve.averaging = o->averaging ? si::CoarseAveraging::AllPixels
+                                     : si::CoarseAveraging::KnownOnly;
+    d.solve.block_size = o->block_size;
+    d.solve.overlap = o->overlap;
+    d.solve.schwarz.alpha = o->alpha;
+    d.solve.schwarz.local =
+        si::SolverConfig{o->local_tolerance, o->local_max_iterations, o->local_check_interval};
+    d.solve.schwarz.max_outer_iterations = o->max_outer_iterations;
+    d.solve.normalizer = o->normalizer ? si::ResidualNormalizer::RhsNorm
+                                       : si::ResidualNormalizer::InitialGuess;
+    auto r = si::voronoi_densify(make_image(f, w, h, c), target, seed, d);
+    std::memcpy(mask_out, r.mask.known.data(), r.mask.known.size());
+    *sweeps = r.sweeps;
+    *reached = r.reached_target ? 1 : 0;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 }  // extern "C"

@@ -796,3 +796,174 @@ int or_multilevel_solve(const double* f, const uint8_t* mask, int w, int h, int 
   }
   return 0;
 }
+
+/* ---- Voronoi densification: masks.hpp:45-215 ---------------------------- */
+
+/* Exact nearest known pixel under squared Euclidean distance, ties to the
+ * lower site index (assign_nearest_site, masks.hpp:54-139).  Same search as
+ * the reference: sites are binned on a square grid of side
+ * max(1, floor(sqrt(n/m))) and rings of bins are visited around the pixel's
+ * bin until the ring's minimum possible distance exceeds the best one found;
+ * bins whose rectangle is farther than the best are skipped.  The result is
+ * the lexicographic minimum of (distance, site index) over all sites. */
+int or_assign_nearest_site(const uint8_t* mask, int w, int h, int32_t* sites, int32_t* site_of,
+                           int* num_sites) {
+  const size_t n = (size_t)w * h;
+  int m = 0;
+  for (size_t i = 0; i < n; ++i)
+    if (mask[i]) sites[m++] = (int32_t)i;
+  *num_sites = m;
+  if (m == 0) return 1;
+  int cell = (int)sqrt((double)n / m);
+  if (cell < 1) cell = 1;
+  const int gw = (w + cell - 1) / cell, gh = (h + cell - 1) / cell;
+  const size_t nb = (size_t)gw * gh;
+  int32_t* start = (int32_t*)calloc(nb + 1, sizeof(int32_t));
+  int32_t* members = (int32_t*)malloc((size_t)m * sizeof(int32_t));
+  int32_t* fill = (int32_t*)malloc(nb * sizeof(int32_t));
+  for (int s = 0; s < m; ++s) {
+    int x = sites[s] % w, y = sites[s] / w;
+    start[(size_t)(y / cell) * gw + x / cell + 1]++;
+  }
+  for (size_t b = 0; b < nb; ++b) start[b + 1] += start[b];
+  memcpy(fill, start, nb * sizeof(int32_t));
+  for (int s = 0; s < m; ++s) {
+    int x = sites[s] % w, y = sites[s] / w;
+    members[fill[(size_t)(y / cell) * gw + x / cell]++] = s;
+  }
+  const int rings = gw > gh ? gw : gh;
+  for (int py = 0; py < h; ++py) {
+    for (int px = 0; px < w; ++px) {
+      const int cx = px / cell, cy = py / cell;
+      long long best_d = -1;
+      int best = -1;
+      for (int ring = 0; ring <= rings; ++ring) {
+        if (best >= 0 && ring >= 1) {
+          long long reach = (long long)(ring - 1) * cell + 1;
+          if (reach * reach > best_d) break;
+        }
+        for (int by = cy - ring; by <= cy + ring; ++by) {
+          if (by < 0 || by >= gh) continue;
+          int edge_row = by == cy - ring || by == cy + ring;
+          int step = edge_row ? 1 : 2 * ring;
+          for (int bx = cx - ring; bx <= cx + ring; bx += step > 0 ? step : 1) {
+            if (bx < 0 || bx >= gw) continue;
+            int x0 = bx * cell, x1 = x0 + cell - 1, y0 = by * cell, y1 = y0 + cell - 1;
+            if (x1 > w - 1) x1 = w - 1;
+            if (y1 > h - 1) y1 = h - 1;
+            long long dx = px < x0 ? x0 - px : (px > x1 ? px - x1 : 0);
+            long long dy = py < y0 ? y0 - py : (py > y1 ? py - y1 : 0);
+            if (best >= 0 && dx * dx + dy * dy > best_d) continue;
+            size_t b = (size_t)by * gw + bx;
+            for (int k = start[b]; k < start[b + 1]; ++k) {
+              int s = members[k];
+              long long ex = sites[s] % w - px, ey = sites[s] / w - py;
+              long long d = ex * ex + ey * ey;
+              if (best < 0 || d < best_d || (d == best_d && s < best)) {
+                best_d = d;
+                best = s;
+              }
+            }
+            if (step == 0) break;
+          }
+        }
+      }
+      site_of[(size_t)py * w + px] = best;
+    }
+  }
+  free(start);
+  free(members);
+  free(fill);
+  return 0;
+}
+
+typedef struct {
+  double err;
+  long long area;
+  int index;
+} cell_rank;
+
+/* Ranking of masks.hpp:189-194: error desc, area desc, site index asc. */
+static int cell_rank_cmp(const void* pa, const void* pb) {
+  const cell_rank* a = (const cell_rank*)pa;
+  const cell_rank* b = (const cell_rank*)pb;
+  if (a->err != b->err) return a->err > b->err ? -1 : 1;
+  if (a->area != b->area) return a->area > b->area ? -1 : 1;
+  return a->index < b->index ? -1 : (a->index > b->index);
+}
+
+/* voronoi_densify (masks.hpp:155-212) from a given seed mask (the caller
+ * draws it with random_mask, masks.hpp:170).  Each sweep: inpaint with the
+ * multilevel ORAS solver at inner_tolerance, assign Voronoi cells, sum the
+ * squared error of the unknown pixels of every cell in pixel order, rank the
+ * cells and plant a known pixel at the worst pixel of the first
+ * max(1, floor(cell_fraction * m)) cells (capped by the cells with pixels and
+ * by the remaining target). */
+int or_voronoi_densify(const double* f, int w, int h, int c, const uint8_t* seed_mask,
+                       long long target_k, double cell_fraction, double inner_tolerance,
+                       int max_sweeps, const or_options* solve, uint8_t* mask, int* sweeps) {
+  const size_t n = (size_t)w * h;
+  memcpy(mask, seed_mask, n);
+  long long known = 0;
+  for (size_t i = 0; i < n; ++i) known += mask[i] != 0;
+  or_options so = *solve;
+  so.tolerance = inner_tolerance;
+  so.flavour = 1;
+  double* u = (double*)malloc((size_t)c * n * sizeof(double));
+  int32_t* sites = (int32_t*)malloc(n * sizeof(int32_t));
+  int32_t* site_of = (int32_t*)malloc(n * sizeof(int32_t));
+  cell_rank* cells = (cell_rank*)malloc(n * sizeof(cell_rank));
+  double* worst_e = (double*)malloc(n * sizeof(double));
+  int32_t* worst_p = (int32_t*)malloc(n * sizeof(int32_t));
+  int rc = 0;
+  *sweeps = 0;
+  while (known < target_k && *sweeps < max_sweeps) {
+    or_report rep;
+    if (or_multilevel_solve(f, mask, w, h, c, &so, u, &rep, NULL, 0)) {
+      rc = 1;
+      break;
+    }
+    int m = 0;
+    or_assign_nearest_site(mask, w, h, sites, site_of, &m);
+    for (int s = 0; s < m; ++s) {
+      cells[s].err = 0.0;
+      cells[s].area = 0;
+      cells[s].index = s;
+      worst_e[s] = -1.0;
+      worst_p[s] = -1;
+    }
+    for (size_t p = 0; p < n; ++p) {
+      if (mask[p]) continue;
+      int s = site_of[p];
+      double e = 0.0;
+      for (int k = 0; k < c; ++k) {
+        double d = u[k * n + p] - f[k * n + p];
+        e = fma(d, d, e);
+      }
+      cells[s].err += e;
+      cells[s].area++;
+      if (e > worst_e[s]) {
+        worst_e[s] = e;
+        worst_p[s] = (int32_t)p;
+      }
+    }
+    int used = 0;
+    for (int s = 0; s < m; ++s)
+      if (cells[s].area > 0) cells[used++] = cells[s];
+    qsort(cells, (size_t)used, sizeof(cell_rank), cell_rank_cmp);
+    long long quota = (long long)(cell_fraction * (double)m);
+    if (quota < 1) quota = 1;
+    if (quota > used) quota = used;
+    if (quota > target_k - known) quota = target_k - known;
+    for (long long i = 0; i < quota; ++i) mask[worst_p[cells[i].index]] = 1;
+    known += quota;
+    ++*sweeps;
+  }
+  free(u);
+  free(sites);
+  free(site_of);
+  free(cells);
+  free(worst_e);
+  free(worst_p);
+  return rc;
+}

@@ -84,6 +84,16 @@ void or_schwarz_sweep(const uint8_t* mask, int w, int h, int c, const double* b,
 void or_local_operator_apply(const uint8_t* mask, int w, int h, int x0, int y0, int bw, int bh,
                              int flavour, double alpha, const double* v, double* out);
 
+/* assign_nearest_site (masks.hpp:54-139): sites = known pixel indices
+ * ascending (capacity w*h), site_of[p] = index into sites.  Returns 1 when the
+ * mask has no known pixel. */
+int or_assign_nearest_site(const uint8_t* mask, int w, int h, int32_t* sites, int32_t* site_of,
+                           int* num_sites);
+/* voronoi_densify (masks.hpp:155-212) from the seed mask random_mask drew. */
+int or_voronoi_densify(const double* f, int w, int h, int c, const uint8_t* seed_mask,
+                       long long target_k, double cell_fraction, double inner_tolerance,
+                       int max_sweeps, const or_options* solve, uint8_t* mask, int* sweeps);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,12 +7,13 @@ CUDA behind the C ABI in ``include/schwarz_b200.h``); this package is the
 Python mirror of the reference interface.
 """
 from .api import (  # noqa: F401
-    CoarseAveraging, ConvergenceTrace, ImageBuffer, InpaintingMask, InvalidArgument, LevelSolver,
+    CoarseAveraging, ConvergenceTrace, DensifyOptions, DensifyResult, ImageBuffer, InpaintingMask, InvalidArgument, LevelSolver,
     Method, MultilevelSolveOptions, Precision, ResidualNormalizer, RunOptions, SchwarzFlavour,
     SchwarzOptions, SchwarzSolveOptions, SolveReport, SolveResult, Solver, SolverConfig,
     SolverError, Subdomain, SubdomainPartition, TraceRow, Unsupported, canonical_r0,
     clamped_partition, default_solver, is_multilevel, kDefaultOrasAlpha, method_name,
-    mse_per_channel, multilevel_solve, pack_pbm, quantise_pnm, parse_method, partition_domain, psnr, random_mask,
-    run_batch, run_method, run_schwarz_level, solve_schwarz, synthetic_test_image)
+    mse_per_channel, multilevel_solve, pack_pbm, quantise_pnm, parse_method, partition_domain,
+    psnr, random_mask, run_batch, run_method, run_schwarz_level, solve_schwarz,
+    synthetic_test_image, VoronoiAssignment, assign_nearest_site, voronoi_densify)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -68,6 +68,16 @@ class si_kernel_stats(C.Structure):
     ]
 
 
+class si_densify_options(C.Structure):
+    _fields_ = [
+        ("initial_density", C.c_double),
+        ("cell_fraction", C.c_double),
+        ("inner_tolerance", C.c_double),
+        ("max_sweeps", C.c_int),
+        ("solve", si_options),
+    ]
+
+
 TRACE_FN = C.CFUNCTYPE(None, C.c_int, C.c_double, C.c_double, C.c_double, C.c_void_p)
 
 _vp = C.c_void_p
@@ -117,6 +127,10 @@ SIGNATURES = {
     "si_partition_domain": (_i, [_i, _i, _i, _i, _ip, _ip, _ip, _i]),
     "si_synthetic_test_image": (_i, [_i, _i, _i, C.c_uint64, _vp]),
     "si_random_mask": (_i, [_i, _i, _d, C.c_uint64, _vp]),
+    "si_default_densify_options": (None, [C.POINTER(si_densify_options)]),
+    "si_voronoi_densify": (_i, [_vp, _vp, _i, _i, _i, _d, C.c_uint64,
+                                C.POINTER(si_densify_options), _vp, _ip, _ip]),
+    "si_assign_nearest_site": (_i, [_vp, _vp, _i, _i, _vp, _vp, _ip]),
     "si_joint_norm": (_d, [_dp, _i]),
     "si_psnr": (_i, [_vp, _vp, _i, _i, _i, _dp]),
     "si_set_profiling": (_i, [_vp, _i]),

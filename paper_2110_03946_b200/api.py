@@ -173,6 +173,38 @@ class MultilevelSolveOptions:  # multilevel.hpp:132-142
     precision: Precision = Precision.FP64
 
 
+def _ml_run_options(o: MultilevelSolveOptions) -> "RunOptions":
+    return RunOptions(tolerance=o.tolerance, levels=o.levels, block_size=o.block_size,
+                      overlap=o.overlap, alpha=o.schwarz.alpha,
+                      coarse_tolerance=o.coarse_tolerance, averaging=o.averaging,
+                      local=o.schwarz.local, max_outer_iterations=o.schwarz.max_outer_iterations,
+                      normalizer=o.normalizer, precision=o.precision)
+
+
+@dataclass
+class DensifyOptions:  # masks.hpp:145-151
+    initial_density: float = 0.0   # <= 0: start at a quarter of the target
+    cell_fraction: float = 0.20    # share of cells refined per sweep
+    inner_tolerance: float = 1e-3  # tolerance of the guiding inpainting runs
+    max_sweeps: int = 100
+    solve: MultilevelSolveOptions = field(default_factory=MultilevelSolveOptions)
+
+    def to_c(self) -> L.si_densify_options:
+        d = L.si_densify_options()
+        d.initial_density = self.initial_density
+        d.cell_fraction = self.cell_fraction
+        d.inner_tolerance = self.inner_tolerance
+        d.max_sweeps = self.max_sweeps
+        d.solve = _ml_run_options(self.solve).to_c()
+        return d
+
+
+@dataclass
+class VoronoiAssignment:  # masks.hpp:45-48
+    sites: np.ndarray     # int32 known pixel indices, ascending
+    site_of: np.ndarray   # int32 (h, w): index into sites
+
+
 # ----------------------------------------------------------------- data
 class ImageBuffer:
     """Planar image [c][y][x] of doubles (image.hpp:24-63)."""
@@ -477,12 +509,7 @@ class Solver:
             method = Method.MultilevelCg
         else:
             method = Method.MultilevelOras if solver == LevelSolver.Oras else Method.Ras
-        ro = RunOptions(tolerance=options.tolerance, levels=options.levels,
-                        block_size=options.block_size, overlap=options.overlap,
-                        alpha=options.schwarz.alpha, coarse_tolerance=options.coarse_tolerance,
-                        averaging=options.averaging, local=options.schwarz.local,
-                        max_outer_iterations=options.schwarz.max_outer_iterations,
-                        normalizer=options.normalizer, precision=options.precision)
+        ro = _ml_run_options(options)
         if method == Method.Ras and options.levels != 1:
             # RAS level solver on a pyramid: the C ABI's RAS method is single level;
             # route multilevel RAS through the ORAS path with alpha = 1 (identical
@@ -492,6 +519,31 @@ class Solver:
         elif method == Method.Ras:
             pass
         return self.run_method(method, f, mask, ro, reference)
+
+    def voronoi_densify(self, f: ImageBuffer, target_density: float, seed: int,
+                        options: Optional[DensifyOptions] = None) -> "DensifyResult":
+        """voronoi_densify (masks.hpp:155-212), the whole loop on the device."""
+        options = options or DensifyOptions()
+        out = np.zeros((f.height, f.width), np.uint8)
+        sweeps, reached = C.c_int(), C.c_int()
+        d = options.to_c()
+        _check(self._lib.si_voronoi_densify(self._h, f.data.ctypes.data, f.width, f.height,
+                                            f.channels, float(target_density), int(seed),
+                                            C.byref(d), out.ctypes.data, C.byref(sweeps),
+                                            C.byref(reached)))
+        return DensifyResult(InpaintingMask(known=out), sweeps.value, bool(reached.value))
+
+    def assign_nearest_site(self, mask: InpaintingMask) -> VoronoiAssignment:
+        """assign_nearest_site (masks.hpp:54-139) on the device."""
+        n = mask.width * mask.height
+        sites = np.empty(n, np.int32)
+        site_of = np.empty((mask.height, mask.width), np.int32)
+        k = C.c_int()
+        known = np.ascontiguousarray(mask.known, dtype=np.uint8)
+        _check(self._lib.si_assign_nearest_site(self._h, known.ctypes.data, mask.width,
+                                                mask.height, sites.ctypes.data,
+                                                site_of.ctypes.data, C.byref(k)))
+        return VoronoiAssignment(sites[: k.value].copy(), site_of)
 
     def run_schwarz_level(self, mask: InpaintingMask, partition: SubdomainPartition,
                           b: np.ndarray, u: np.ndarray, r0_norm: float, tolerance: float,
@@ -603,6 +655,22 @@ class Solver:
                    "algorithmic_bytes": s.algorithmic_bytes[i]} for i, n in enumerate(names)}
         out["total_launches"] = s.total_launches
         return out
+
+
+@dataclass
+class DensifyResult:  # masks.hpp:153-157
+    mask: "InpaintingMask"
+    sweeps: int = 0
+    reached_target: bool = False
+
+
+def voronoi_densify(f: ImageBuffer, target_density: float, seed: int,
+                    options: Optional[DensifyOptions] = None) -> DensifyResult:
+    return default_solver().voronoi_densify(f, target_density, seed, options)
+
+
+def assign_nearest_site(mask: InpaintingMask) -> VoronoiAssignment:
+    return default_solver().assign_nearest_site(mask)
 
 
 def _require_same_grid(f: ImageBuffer, mask: InpaintingMask):

@@ -25,6 +25,9 @@
 #include "sweep.cuh"
 #include "sweep_warp.cuh"
 #include "cg_level.cuh"
+#include "densify.cuh"
+
+#include <cub/cub.cuh>
 
 using namespace sib;
 
@@ -86,9 +89,24 @@ struct LevelBuf {
   DevBuf mask, b, u0, u1;
 };
 
+// Voronoi densification work arrays (masks.hpp:45-215).
+struct VoronoiBufs {
+  DevBuf f, mask, u, flag, rank, sites, bin_start, bin_cursor, members, site_of;
+  DevBuf key, key2, pix, pix2, err, area, area2, seg, bits, bits2, worst, order, order2, tmp, small;
+  void release() {
+    for (DevBuf* b : {&f, &mask, &u, &flag, &rank, &sites, &bin_start, &bin_cursor, &members,
+                      &site_of, &key, &key2, &pix, &pix2, &err, &area, &area2, &seg, &bits,
+                      &bits2, &worst, &order, &order2, &tmp, &small})
+      b->release();
+  }
+};
+
 constexpr int kFlavourCg = -1;  // level solver = multilevel CG (LevelSolver::Cg)
 
-enum Kind { K_RESIDUAL = 0, K_SWEEP = 1, K_RESTRICT = 2, K_PROLONG = 3, K_INGEST = 4, K_METRIC = 5 };
+enum Kind {
+  K_RESIDUAL = 0, K_SWEEP = 1, K_RESTRICT = 2, K_PROLONG = 3, K_INGEST = 4, K_METRIC = 5,
+  K_VORONOI = 6
+};
 
 struct PendingEvent {
   int kind;
@@ -123,6 +141,7 @@ struct si_ctx {
   // batch pipeline: two staging slots, one stream per copy direction
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   DevBuf slot_f[2], slot_mask[2], slot_out[2];
+  VoronoiBufs vz;                               // densification
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_solved[2] = {nullptr, nullptr},
               ev_d2h[2] = {nullptr, nullptr};
 };
@@ -297,10 +316,12 @@ void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_
   const int nw = sizeof(T) == 8 ? x.c.sweep_nw64 : x.c.sweep_nw32;
   if constexpr (sizeof(T) == 8) {
     if (nw == 2) launch_sweep_nw<T, 2>(x, a, nblocks, C);
+    else if (nw == 8) launch_sweep_nw<T, 8>(x, a, nblocks, C);
     else launch_sweep_nw<T, 4>(x, a, nblocks, C);
   } else {
     if (nw == 1) launch_sweep_nw<T, 1>(x, a, nblocks, C);
     else if (nw == 2) launch_sweep_nw<T, 2>(x, a, nblocks, C);
+    else if (nw == 8) launch_sweep_nw<T, 8>(x, a, nblocks, C);
     else launch_sweep_nw<T, 4>(x, a, nblocks, C);
   }
 }
@@ -913,6 +934,214 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
   CK(cudaStreamSynchronize(cs));
 }
 
+// ---------------------------------------------------------------- densify
+// CUB device-wide primitives with their temporary storage in vz.tmp.
+template <typename F>
+void cub_call(Ctx& x, F&& fn) {
+  size_t bytes = 0;
+  CK(fn(static_cast<void*>(nullptr), bytes));
+  x.c.vz.tmp.ensure(std::max<size_t>(bytes, 256));
+  CK(fn(x.c.vz.tmp.ptr, bytes));
+}
+
+// assign_nearest_site (masks.hpp:54-139) of a device mask into vz.sites /
+// vz.site_of; returns the site count m.
+int assign_device(Ctx& x, const uint8_t* d_mask, int W, int H) {
+  auto& z = x.c.vz;
+  const size_t n = static_cast<size_t>(W) * H;
+  const int ni = static_cast<int>(n);
+  z.flag.ensure(n * 4);
+  z.rank.ensure(n * 4);
+  z.sites.ensure(n * 4);
+  z.site_of.ensure(n * 4);
+  z.small.ensure(64);
+  int32_t* flag = z.flag.as<int32_t>();
+  int32_t* rank = z.rank.as<int32_t>();
+  int m = 0;
+  {
+    Timed t(x, K_VORONOI, static_cast<double>(n) * 13.0);
+    site_flags_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, x.s>>>(d_mask, n, flag);
+    CK(cudaGetLastError());
+    cub_call(x, [&](void* tmp, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(tmp, b, flag, rank, ni, x.s);
+    });
+    sites_scatter_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, x.s>>>(d_mask, rank, n,
+                                                                     z.sites.as<int32_t>());
+    CK(cudaGetLastError());
+    int32_t tail[2];
+    CK(cudaMemcpyAsync(&tail[0], rank + n - 1, 4, cudaMemcpyDeviceToHost, x.s));
+    CK(cudaMemcpyAsync(&tail[1], flag + n - 1, 4, cudaMemcpyDeviceToHost, x.s));
+    CK(cudaStreamSynchronize(x.s));
+    m = tail[0] + tail[1];
+  }
+  check_arg(m > 0, "assign_nearest_site: mask has no known pixels");
+  const int cell = std::max(1, static_cast<int>(std::sqrt(static_cast<double>(n) / m)));
+  const int gw = (W + cell - 1) / cell, gh = (H + cell - 1) / cell;
+  const size_t nb = static_cast<size_t>(gw) * gh;
+  z.bin_start.ensure((nb + 1) * 4);
+  z.bin_cursor.ensure((nb + 1) * 4);
+  z.members.ensure(static_cast<size_t>(m) * 4);
+  int32_t* start = z.bin_start.as<int32_t>();
+  int32_t* cursor = z.bin_cursor.as<int32_t>();
+  {
+    Timed t(x, K_VORONOI, static_cast<double>(m) * 24.0 + nb * 12.0);
+    CK(cudaMemsetAsync(cursor, 0, (nb + 1) * 4, x.s));
+    bucket_count_kernel<<<grid_for(m, 256, 148 * 8), 256, 0, x.s>>>(z.sites.as<int32_t>(), m, W,
+                                                                    cell, gw, cursor);
+    CK(cudaGetLastError());
+    cub_call(x, [&](void* tmp, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(tmp, b, cursor, start, static_cast<int>(nb + 1), x.s);
+    });
+    CK(cudaMemcpyAsync(cursor, start, nb * 4, cudaMemcpyDeviceToDevice, x.s));
+    bucket_fill_kernel<<<grid_for(m, 256, 148 * 8), 256, 0, x.s>>>(
+        z.sites.as<int32_t>(), m, W, cell, gw, cursor, z.members.as<int32_t>());
+    CK(cudaGetLastError());
+  }
+  {
+    Timed t(x, K_VORONOI, static_cast<double>(n) * 4.0);
+    assign_sites_kernel<<<dim3((W + 31) / 32, (H + 7) / 8), 256, 0, x.s>>>(
+        z.sites.as<int32_t>(), start, z.members.as<int32_t>(), W, H, cell, gw, gh,
+        z.site_of.as<int32_t>());
+    CK(cudaGetLastError());
+  }
+  return m;
+}
+
+// One sweep's cell statistics and ranking (masks.hpp:175-203) from the guide
+// solution d_u; plants the worst pixels of the first `quota` cells into
+// d_mask and returns how many were planted.
+long long densify_plant(Ctx& x, const uint8_t* mask_view, uint8_t* d_mask, const double* d_u,
+                        const double* d_f, int W, int H, int C, int m, double cell_fraction,
+                        long long remaining) {
+  auto& z = x.c.vz;
+  const size_t n = static_cast<size_t>(W) * H;
+  const int ni = static_cast<int>(n);
+  z.key.ensure(n * 4);
+  z.key2.ensure(n * 4);
+  z.pix.ensure(n * 4);
+  z.pix2.ensure(n * 4);
+  z.err.ensure(n * 8);
+  z.area.ensure((static_cast<size_t>(m) + 1) * 4);
+  z.area2.ensure((static_cast<size_t>(m) + 1) * 4);
+  z.seg.ensure((static_cast<size_t>(m) + 1) * 4);
+  z.bits.ensure(static_cast<size_t>(m) * 8);
+  z.bits2.ensure(static_cast<size_t>(m) * 8);
+  z.worst.ensure(static_cast<size_t>(m) * 4);
+  z.order.ensure(static_cast<size_t>(m) * 4);
+  z.order2.ensure(static_cast<size_t>(m) * 4);
+  int32_t* area = z.area.as<int32_t>();
+  int* nonempty = z.small.as<int>();
+  int key_bits = 1;
+  while ((1ll << key_bits) <= m) ++key_bits;
+  {
+    Timed t(x, K_VORONOI, static_cast<double>(n) * (C * 16.0 + 1 + 4 + 12));
+    CK(cudaMemsetAsync(area, 0, (static_cast<size_t>(m) + 1) * 4, x.s));
+    CK(cudaMemsetAsync(nonempty, 0, 4, x.s));
+    cell_keys_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, x.s>>>(
+        mask_view, z.site_of.as<int32_t>(), d_u, d_f, n, C, m, z.key.as<int32_t>(),
+        z.pix.as<int32_t>(), z.err.as<double>(), area);
+    CK(cudaGetLastError());
+  }
+  {
+    Timed t(x, K_VORONOI, static_cast<double>(n) * 16.0 * 2);
+    cub_call(x, [&](void* tmp, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(tmp, b, z.key.as<int32_t>(), z.key2.as<int32_t>(),
+                                             z.pix.as<int32_t>(), z.pix2.as<int32_t>(), ni, 0,
+                                             key_bits, x.s);
+    });
+    cub_call(x, [&](void* tmp, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(tmp, b, area, z.seg.as<int32_t>(), m + 1, x.s);
+    });
+  }
+  {
+    Timed t(x, K_VORONOI, static_cast<double>(n) * 12.0 + m * 24.0);
+    cell_reduce_kernel<<<grid_for(m, 128, 148 * 16), 128, 0, x.s>>>(
+        z.seg.as<int32_t>(), z.pix2.as<int32_t>(), z.err.as<double>(), m,
+        z.bits.as<unsigned long long>(), z.worst.as<int32_t>(), z.order.as<int32_t>(), nonempty);
+    CK(cudaGetLastError());
+  }
+  {
+    Timed t(x, K_VORONOI, static_cast<double>(m) * 48.0);
+    // stable: area desc, ties keep index asc; then error desc, ties keep (area desc, index asc)
+    cub_call(x, [&](void* tmp, size_t& b) {
+      return cub::DeviceRadixSort::SortPairsDescending(tmp, b, area, z.area2.as<int32_t>(),
+                                                       z.order.as<int32_t>(),
+                                                       z.order2.as<int32_t>(), m, 0, 32, x.s);
+    });
+    gather_bits_kernel<<<grid_for(m, 256, 148 * 8), 256, 0, x.s>>>(
+        z.bits.as<unsigned long long>(), z.order2.as<int32_t>(), m,
+        z.bits2.as<unsigned long long>());
+    CK(cudaGetLastError());
+    cub_call(x, [&](void* tmp, size_t& b) {
+      return cub::DeviceRadixSort::SortPairsDescending(
+          tmp, b, z.bits2.as<unsigned long long>(), z.bits.as<unsigned long long>(),
+          z.order2.as<int32_t>(), z.order.as<int32_t>(), m, 0, 64, x.s);
+    });
+  }
+  int used = 0;
+  CK(cudaMemcpyAsync(&used, nonempty, 4, cudaMemcpyDeviceToHost, x.s));
+  CK(cudaStreamSynchronize(x.s));
+  long long quota = std::max<long long>(1, static_cast<long long>(cell_fraction * static_cast<double>(m)));
+  quota = std::min<long long>({quota, static_cast<long long>(used), remaining});
+  if (quota > 0) {
+    Timed t(x, K_VORONOI, static_cast<double>(quota) * 9.0);
+    plant_kernel<<<grid_for(quota, 256, 148 * 8), 256, 0, x.s>>>(
+        z.order.as<int32_t>(), z.worst.as<int32_t>(), static_cast<int>(quota), d_mask);
+    CK(cudaGetLastError());
+  }
+  return quota;
+}
+
+// voronoi_densify (masks.hpp:155-212).  f is host planar f64; the whole loop
+// (guide solves, assignment, ranking, planting) stays on the device.
+void voronoi_densify(si_ctx* ctx, const double* f, int w, int h, int c, double target,
+                     uint64_t seed, const si_densify_options& d, uint8_t* mask_out, int* sweeps,
+                     int* reached) {
+  check_arg(target > 0.0 && target <= 1.0, "voronoi_densify: target density must lie in (0, 1]");
+  check_arg(d.initial_density <= 0.0 || d.initial_density < target,
+            "voronoi_densify: initial density must lie below the target");
+  check_dims(w, h, c);
+  check_arg(static_cast<double>(w) * h < 2147483647.0,
+            "voronoi_densify: images beyond 2^31 pixels are not supported");
+  const size_t n = static_cast<size_t>(w) * h;
+  const long long target_k = std::max<long long>(
+      1, std::min<long long>(static_cast<long long>(n),
+                             std::llround(target * static_cast<double>(n))));
+  double init = d.initial_density > 0.0 ? d.initial_density : target / 4.0;
+  if (init * static_cast<double>(n) < 1.0) init = 1.5 / static_cast<double>(n);
+  std::vector<uint8_t> seed_mask(n);
+  check_arg(si_random_mask(w, h, init, seed, seed_mask.data()) == SI_OK,
+            "random_mask: density rounds to zero known pixels");
+  long long known = 0;
+  for (uint8_t v : seed_mask) known += v != 0;
+
+  si_options so = d.solve;
+  so.tolerance = d.inner_tolerance;
+  validate_options_common(so);
+  Ctx x{*ctx, ctx->own_stream};
+  auto& z = ctx->vz;
+  z.f.ensure(n * c * 8);
+  z.mask.ensure(n);
+  z.u.ensure(n * c * 8);
+  CK(cudaMemcpyAsync(z.f.ptr, f, n * c * 8, cudaMemcpyHostToDevice, x.s));
+  CK(cudaMemcpyAsync(z.mask.ptr, seed_mask.data(), n, cudaMemcpyHostToDevice, x.s));
+  int sw = 0;
+  while (known < target_k && sw < d.max_sweeps) {
+    si_report rep;
+    clear_report(&rep);
+    run_device(ctx, SI_METHOD_MLORAS, z.f.as<double>(), z.mask.as<uint8_t>(), w, h, c, so,
+               nullptr, z.u.as<double>(), &rep, nullptr, nullptr, x.s, Clock::now());
+    const int m = assign_device(x, z.mask.as<uint8_t>(), w, h);
+    known += densify_plant(x, z.mask.as<uint8_t>(), z.mask.as<uint8_t>(), z.u.as<double>(),
+                           z.f.as<double>(), w, h, c, m, d.cell_fraction, target_k - known);
+    ++sw;
+  }
+  CK(cudaMemcpyAsync(mask_out, z.mask.ptr, n, cudaMemcpyDeviceToHost, x.s));
+  sync(x);
+  *sweeps = sw;
+  *reached = known >= target_k;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1009,6 +1238,7 @@ void si_destroy(si_ctx* c) {
                     &c->red_out, &c->counters, &c->ticket, &c->scratch, &c->cg_rhs, &c->cg_x,
                     &c->cg_r, &c->cg_p, &c->cg_q})
     b->release();
+  c->vz.release();
   for (auto& p : c->pending) {
     cudaEventDestroy(p.start);
     cudaEventDestroy(p.stop);
@@ -1041,6 +1271,7 @@ si_status si_trim(si_ctx* c) {
       l.u1.release();
     }
     for (DevBuf* b : {&c->in_f, &c->in_mask, &c->in_ref, &c->out_img, &c->aux}) b->release();
+    c->vz.release();
   });
 }
 
@@ -1676,6 +1907,53 @@ si_status si_host_alloc(size_t bytes, void** ptr) {
 
 si_status si_host_free(void* ptr) {
   return guard([&] { CK(cudaFreeHost(ptr)); });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+void si_default_densify_options(si_densify_options* o) {
+  if (!o) return;
+  o->initial_density = 0.0;
+  o->cell_fraction = 0.20;
+  o->inner_tolerance = 1e-3;
+  o->max_sweeps = 100;
+  si_default_options(&o->solve);
+}
+
+si_status si_voronoi_densify(si_ctx* ctx, const double* f, int w, int h, int c,
+                             double target_density, uint64_t seed, const si_densify_options* opt,
+                             uint8_t* mask_out, int* sweeps, int* reached_target) {
+  return guard([&] {
+    check_arg(ctx && f && mask_out && sweeps && reached_target, "null argument");
+    set_device(ctx);
+    si_densify_options d;
+    if (opt)
+      d = *opt;
+    else
+      si_default_densify_options(&d);
+    voronoi_densify(ctx, f, w, h, c, target_density, seed, d, mask_out, sweeps, reached_target);
+  });
+}
+
+si_status si_assign_nearest_site(si_ctx* ctx, const uint8_t* mask, int w, int h, int32_t* sites,
+                                 int32_t* site_of, int* num_sites) {
+  return guard([&] {
+    check_arg(ctx && mask && sites && site_of && num_sites, "null argument");
+    check_arg(w > 0 && h > 0, "InpaintingMask: dimensions must be positive");
+    set_device(ctx);
+    Ctx x{*ctx, ctx->own_stream};
+    const size_t n = static_cast<size_t>(w) * h;
+    auto& z = ctx->vz;
+    z.mask.ensure(n);
+    CK(cudaMemcpyAsync(z.mask.ptr, mask, n, cudaMemcpyHostToDevice, x.s));
+    const int m = assign_device(x, z.mask.as<uint8_t>(), w, h);
+    CK(cudaMemcpyAsync(sites, z.sites.ptr, static_cast<size_t>(m) * 4, cudaMemcpyDeviceToHost, x.s));
+    CK(cudaMemcpyAsync(site_of, z.site_of.ptr, n * 4, cudaMemcpyDeviceToHost, x.s));
+    sync(x);
+    *num_sites = m;
+  });
 }
 
 }  // extern "C"

@@ -10,8 +10,9 @@ the reference's own outputs on seeded inputs from its own generators:
                 per-channel sums and 4096 sampled output pixels
   small.npz     12 small instances over the option space, full outputs
   kernels.npz   restriction / prolongation / local-operator probes
+  densify.npz   assign_nearest_site / voronoi_densify (masks.hpp) outputs
 
-Usage: python tests/golden/make_golden.py
+Usage: python tests/golden/make_golden.py [--only densify]
 """
 import hashlib
 import json
@@ -58,6 +59,46 @@ CG_CASES = [
 ]
 
 
+DENSIFY_CASES = [
+    # image (w, h, c, seed) or ("flat", w, h, value), target, seed, DensifyOptions fields, solve
+    ((64, 64, 1, 3), 0.08, 17, dict(max_sweeps=50), {}),
+    ((48, 48, 1, 5), 0.10, 23, dict(initial_density=0.02), {}),
+    ((128, 128, 1, 7), 0.05, 31, {}, {}),
+    (("flat", 32, 32, 0.25), 0.10, 3, {}, {}),
+    ((96, 80, 3, 9), 0.06, 5, dict(cell_fraction=0.3), dict(levels=2, block_size=16, overlap=3)),
+    ((200, 150, 3, 11), 0.04, 8, dict(inner_tolerance=1e-4), {}),
+]
+
+ASSIGN_CASES = [  # masks_test.cpp:65-77 trials, then larger and degenerate masks
+    *[(5 + 4 * (t % 5), 4 + 3 * (t % 4), 0.1 + 0.05 * t, 500 + t) for t in range(12)],
+    (300, 200, 0.03, 5), (257, 129, 0.004, 6), (64, 64, 1.0 / 4096, 7), (1, 1, 1.0, 8),
+]
+
+
+def densify_image(spec):
+    if spec[0] == "flat":
+        _, w, h, v = spec
+        return np.full((1, h, w), v)
+    w, h, c, seed = spec
+    return P.ref_synthetic_test_image(w, h, c, seed)
+
+
+def densify_fixtures():
+    out = {}
+    for i, (spec, target, seed, dopts, sopts) in enumerate(DENSIFY_CASES):
+        f = densify_image(spec)
+        mask, sweeps, reached = P.ref_voronoi_densify(f, target, seed, **dopts, **sopts)
+        out[f"densify{i}_mask"] = mask
+        out[f"densify{i}_stats"] = np.array([sweeps, int(reached), int(mask.sum())])
+    for i, (w, h, d, seed) in enumerate(ASSIGN_CASES):
+        m = P.ref_random_mask(w, h, d, seed)
+        sites, site_of = P.ref_assign_nearest_site(m)
+        out[f"assign{i}_mask"] = m
+        out[f"assign{i}_site_of"] = site_of
+    np.savez_compressed(os.path.join(HERE, "densify.npz"), **out)
+    print("densify fixtures:", [int(out[f"densify{i}_stats"][0]) for i in range(len(DENSIFY_CASES))])
+
+
 def sha(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
@@ -70,6 +111,10 @@ def main():
     if not P.ref_available():
         sys.exit("oracle/_ref/libref.so missing: run `make -C oracle` where /root/reference exists")
     P.ref().ref_set_threads(0)
+    if "--only" in sys.argv and "densify" in sys.argv:
+        densify_fixtures()
+        return
+    densify_fixtures()
     hashes = {}
     for name, cfg in CONFIGS.items():
         f, m = instance(cfg["w"], cfg["h"], cfg["c"], cfg["d"], 7, 11)

@@ -144,3 +144,69 @@ def test_ref_driver_levels_loop_equals_run_method(oracle):
     a = oracle.ref_run_method("mloras", f, m, levels=3)
     b = oracle.ref_solve_levels(f, m, levels=3)
     assert np.array_equal(a.image, b.image) and np.array_equal(a.trace, b.trace)
+
+
+# ---------------------------------------------------------------- densification
+DENS = np.load(os.path.join(GOLD, "densify.npz"))
+
+
+def _densify_cases():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("make_golden", os.path.join(GOLD, "make_golden.py"))
+    mg = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mg)
+    return mg
+
+
+MG = _densify_cases()
+
+
+def densify_input(spec):
+    if spec[0] == "flat":
+        _, w, h, v = spec
+        return np.full((1, h, w), v)
+    w, h, c, seed = spec
+    return si.synthetic_test_image(w, h, c, seed).data
+
+
+def test_oracle_assignment_matches_reference_fixtures(oracle):
+    """assign_nearest_site (masks.hpp:54-139): the restatement equals the
+    reference on masks_test.cpp's trials plus larger and degenerate masks."""
+    for i, (w, h, d, seed) in enumerate(MG.ASSIGN_CASES):
+        m = si.random_mask(w, h, d, seed).known
+        assert np.array_equal(m, DENS[f"assign{i}_mask"])
+        sites, site_of = oracle.oracle_assign_nearest_site(m)
+        assert np.array_equal(site_of, DENS[f"assign{i}_site_of"]), i
+        assert np.array_equal(sites, np.flatnonzero(m.ravel()))
+
+
+def test_oracle_assignment_brute_force_and_ties(oracle):
+    """masks_test.cpp:79-103: the equidistant column goes to the lower site;
+    every site owns itself; brute force agrees."""
+    m = np.zeros((7, 7), np.uint8)
+    m[3, 1] = m[3, 5] = 1
+    _, site_of = oracle.oracle_assign_nearest_site(m)
+    assert (site_of[:, 3] == 0).all()
+    m = si.random_mask(40, 40, 0.06, 9).known
+    sites, site_of = oracle.oracle_assign_nearest_site(m)
+    assert (site_of.ravel()[sites] == np.arange(len(sites))).all()
+    ys, xs = np.divmod(sites, 40)
+    py, px = np.mgrid[0:40, 0:40]
+    d = (py[..., None] - ys) ** 2 + (px[..., None] - xs) ** 2
+    assert np.array_equal(site_of, np.argmin(d, axis=-1))  # argmin: first (lowest) index on ties
+
+
+@pytest.mark.parametrize("i", range(6))
+def test_oracle_densify_matches_reference_fixtures(oracle, i):
+    """voronoi_densify (masks.hpp:155-212) restated in C equals the reference's
+    mask and sweep count from the same seed mask."""
+    spec, target, seed, dopts, sopts = MG.DENSIFY_CASES[i]
+    f = densify_input(spec)
+    c, h, w = f.shape
+    init = oracle.densify_seed_density(target, w * h, dopts.get("initial_density", 0.0))
+    seed_mask = si.random_mask(w, h, init, seed).known
+    kw = {k: v for k, v in dopts.items() if k != "initial_density"}
+    mask, sweeps = oracle.oracle_voronoi_densify(f, seed_mask, target, **kw, **sopts)
+    gs, greached, gcount = DENS[f"densify{i}_stats"]
+    assert sweeps == gs and int(mask.sum()) == gcount
+    assert np.array_equal(mask, DENS[f"densify{i}_mask"])
