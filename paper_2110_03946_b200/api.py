@@ -650,7 +650,7 @@ class Solver:
     def kernel_stats(self, reset: bool = False) -> dict:
         s = L.si_kernel_stats()
         _check(self._lib.si_get_kernel_stats(self._h, C.byref(s), int(reset)))
-        names = ["residual", "sweep", "restrict", "prolong", "ingest_export", "metrics"]
+        names = ["residual", "sweep", "restrict", "prolong", "ingest_export", "metrics", "voronoi"]
         out = {n: {"launches": s.launches[i], "device_ms": s.device_ms[i],
                    "algorithmic_bytes": s.algorithmic_bytes[i]} for i, n in enumerate(names)}
         out["total_launches"] = s.total_launches

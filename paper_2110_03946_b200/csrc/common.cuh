@@ -46,4 +46,29 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// Warp total of one double per lane on the FP64 tensor core (DMMA m8n8k4):
+// D = A * ones with A[i][k] = lane 4i+k gives the 8 row sums (lane l holds
+// row l/4); two more MMAs with the row sums as B (k = 0..3, then 4..7) and
+// ones as A fold them.  ~115 cycles of latency against ~170 for the 5-level
+// shuffle butterfly; every lane ends with the same, order-fixed total.
+// All 32 lanes must be converged.
+__device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b, double c0,
+                                            double c1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+               : "=d"(d0), "=d"(d1)
+               : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
+__device__ __forceinline__ double warp_sum_mma(double v) {
+  const int k = threadIdx.x & 3;
+  double r0, r1;
+  dmma_m8n8k4(r0, r1, v, 1.0, 0.0, 0.0);
+  const double lo = __shfl_sync(0xffffffffu, r0, 4 * k);
+  const double hi = __shfl_sync(0xffffffffu, r0, 4 * (k + 4));
+  double e0, e1, f0, f1;
+  dmma_m8n8k4(e0, e1, 1.0, lo, 0.0, 0.0);
+  dmma_m8n8k4(f0, f1, 1.0, hi, e0, e1);
+  return f0;
+}
+
 }  // namespace sib

@@ -473,8 +473,8 @@ __global__ void copy_u64_kernel(const unsigned long long* src, unsigned long lon
 }
 
 void begin_counters(Ctx& x) {
-  x.c.counters.ensure(sizeof(unsigned long long) * 4);
-  copy_u64_kernel<<<1, 32, 0, x.s>>>(x.c.counters.as<unsigned long long>(), nullptr, 4, true);
+  x.c.counters.ensure(sizeof(unsigned long long) * 8);
+  copy_u64_kernel<<<1, 32, 0, x.s>>>(x.c.counters.as<unsigned long long>(), nullptr, 8, true);
   CK(cudaGetLastError());
 }
 
@@ -1812,7 +1812,18 @@ si_status si_device_sweep_rows(si_ctx* ctx, const uint8_t* d_mask, const void* d
                            static_cast<const double*>(d_u_old), static_cast<double*>(d_u_new), w,
                            h, c, block_size, overlap, flavour, o.alpha, lc, known_invariant != 0,
                            ctx->counters.as<unsigned long long>(), by0, by1);
+#ifdef SI_PROBE
+    publish_counters(x, 8);
+    const double its = std::max(1.0, static_cast<double>(ctx->host_cnt[1]));
+    const double ctas = static_cast<double>(Axis::make(w, block_size, overlap).count) *
+                        (by1 - by0) * c;
+    std::fprintf(stderr, "probe cycles/CTA-iteration: apply+pAp %.0f, alpha+r+rr %.0f, beta+p %.0f;"
+                 " per CTA: setup %.0f, write-back %.0f\n",
+                 ctx->host_cnt[3] / its, ctx->host_cnt[4] / its, ctx->host_cnt[5] / its,
+                 ctx->host_cnt[6] / ctas, ctx->host_cnt[7] / ctas);
+#else
     publish_counters(x, 2);
+#endif
     if (failures) *failures = static_cast<long long>(ctx->host_cnt[0]);
     if (cg_iterations) *cg_iterations = static_cast<long long>(ctx->host_cnt[1]);
   });

@@ -32,6 +32,9 @@
 
 namespace sib {
 
+// u_old tile of a block: rows y0-2 .. y0+B+1, columns x0-1 .. x0+B.
+constexpr int kTileW = kMaxBlock + 2, kTileH = kMaxBlock + 4;
+
 template <typename T>
 struct SweepArgs {
   const uint8_t* mask;
@@ -74,26 +77,45 @@ template <typename T, int NW>
 struct SweepSmem {
   T pt[kMaxBlock][kMaxBlock + 2];  // stencil operand rows, zero ghost columns 0 and B+1
   T bt[kMaxBlock][kMaxBlock];      // local right-hand side (true-residual checks)
+  T ut[kTileH][kTileW];            // u_old tile with halo (residual, write-back)
   T pub[NW][2][3][32];             // [warp][top/bottom][r,p,x][col]
   T pubt[NW][2][32];               // true-residual boundary rows
   T red[3][NW];
 };
 
 // CTA-wide sum; identical value in every thread.  slot selects the buffer so
-// consecutive reductions never race (see the header comment).
+// consecutive reductions never race (see the header comment).  The warp part
+// runs on the FP64 tensor core for double (warp_sum_mma), the cross-warp
+// part is a pairwise tree over the NW warp totals.
+template <typename T>
+__device__ __forceinline__ T warp_total(T v) {
+#ifdef SI_NO_DMMA
+  return warp_sum(v);
+#else
+  if constexpr (sizeof(T) == 8)
+    return warp_sum_mma(v);
+  else
+    return warp_sum(v);
+#endif
+}
+
 template <typename T, int NW>
 __device__ __forceinline__ T cta_sum(T v, T (*red)[NW], int slot, int warp, int lane) {
-  v = warp_sum(v);
+  v = warp_total(v);
   if (NW == 1) return v;
 #ifdef SI_ABL_NORED
   return v;
 #endif
   if (lane == 0) red[slot][warp] = v;
   __syncthreads();
-  T s = red[slot][0];
+  T t[NW];
 #pragma unroll
-  for (int w = 1; w < NW; ++w) s += red[slot][w];
-  return s;
+  for (int w = 0; w < NW; ++w) t[w] = red[slot][w];
+#pragma unroll
+  for (int h = 1; h < NW; h *= 2)
+#pragma unroll
+    for (int w = 0; w + h < NW; w += 2 * h) t[w] += t[w + h];
+  return t[0];
 }
 
 // a / b, correctly rounded, from a precomputed rcp = RN(1/b): q0 = RN(a*rcp)
@@ -112,17 +134,21 @@ __device__ __forceinline__ T div_by_recip(T a, T b, T rcp) {
   return fma(e, rcp, q0);
 }
 
-// Thread-local part of a dot product: two interleaved accumulators (even and
-// odd rows) halve the dependent-fma chain.
+// Thread-local part of a dot product: four interleaved accumulators, then
+// a pairwise tree (dependent depth R/4 + 2 instead of R).
 template <typename T, int R>
 __device__ __forceinline__ T dot2(const T (&a)[R], const T (&b)[R]) {
-  T s0 = T(0), s1 = T(0);
+  constexpr int K = R >= 4 ? 4 : R;
+  T s[K];
 #pragma unroll
-  for (int i = 0; i < R; i += 2) {
-    s0 = fma(a[i], b[i], s0);
-    if (i + 1 < R) s1 = fma(a[i + 1], b[i + 1], s1);
-  }
-  return s0 + s1;
+  for (int k = 0; k < K; ++k) s[k] = a[k] * b[k];
+#pragma unroll
+  for (int i = K; i < R; ++i) s[i % K] = fma(a[i], b[i], s[i % K]);
+#pragma unroll
+  for (int h = 1; h < K; h *= 2)
+#pragma unroll
+    for (int k = 0; k + h < K; k += 2 * h) s[k] += s[k + h];
+  return s[0];
 }
 
 // sqrt(v) <= thr, evaluated out of line: the caller only needs it inside a
@@ -143,59 +169,85 @@ struct Cell {
   int known_invariant;
 };
 
-// Residual r = b - A u (operators.hpp:38-66, 91-97) of block rows
-// row0-1 .. row0+R (index j = 0..R+1; rows outside the block are ghosts = 0),
-// together with the in-block known bits of the same rows and u of own rows.
-//   known:   r = b - u
-//   unknown: r = b - (deg*u - (((W + E) + N) + S)) over in-image neighbours.
-template <typename T, int R>
-__device__ __forceinline__ void residual_rows(const Cell<T, R>& c, T (&r)[R + 2], uint64_t& kbits,
-                                              T (&u_own)[R]) {
-  const int lane = threadIdx.x & 31;
-  // u of rows row0-2 .. row0+R+1 at my column (k = 0..R+3); the ring columns
-  // x0-1 (lane 0) and x0+B (lane B-1) are fetched on demand below.
-  T uc[R + 4];
-  const bool edge_w = lane == 0, edge_e = lane == c.B - 1;
+// u_old tile of the block with a 1-column / 2-row halo, rows y0-2 .. y0+B+1
+// and columns x0-1 .. x0+B, zero outside the image.  Loaded cooperatively by
+// the whole CTA (consecutive threads -> consecutive columns of a row: 272-byte
+// coalesced row segments, every load independent and issued up front).
+template <typename T, int NW>
+__device__ __forceinline__ void stage_u_tile(T (*ut)[kTileW], const T* __restrict__ u, int x0,
+                                             int y0, int B, int W, int H) {
+  // Warp w stages tile rows w, w+NW, ...: lanes 0..B load columns x0..x0+B
+  // (one coalesced row segment), lanes 30/31 the ring columns x0-1 and x0+32.
+  constexpr int kRows = (kTileH + NW - 1) / NW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gx = x0 + lane;
+  const bool col_ok = lane <= B && gx < W;
+  const int ex = lane == 30 ? x0 - 1 : x0 + 32;
+  const bool ecol_ok = (lane == 30 && x0 > 0) || (lane == 31 && B == 32 && x0 + 32 < W);
+  const size_t Wz = static_cast<size_t>(W);
+  T v[kRows], e[kRows];
 #pragma unroll
-  for (int k = 0; k < R + 4; ++k) {
-    const int gy = c.y0 + c.row0 - 2 + k;
-    T v = T(0);
-    if (gy >= 0 && gy < c.H && c.gx < c.W && lane <= c.B) v = c.u[static_cast<size_t>(gy) * c.W + c.gx];
-    uc[k] = v;
+  for (int i = 0; i < kRows; ++i) {
+    const int tr = warp + i * NW;
+    const int gy = y0 - 2 + tr;
+    const bool row_ok = tr < kTileH && tr <= B + 3 && gy >= 0 && gy < H;
+    const T* row = u + static_cast<size_t>(row_ok ? gy : 0) * Wz;
+    v[i] = (row_ok && col_ok) ? row[gx] : T(0);
+    e[i] = (row_ok && ecol_ok) ? row[ex] : T(0);
   }
+#pragma unroll
+  for (int i = 0; i < kRows; ++i) {
+    const int tr = warp + i * NW;
+    if (tr < kTileH) {
+      ut[tr][lane + 1] = v[i];
+      if (lane == 30) ut[tr][0] = e[i];
+      if (lane == 31) ut[tr][kTileW - 1] = e[i];
+    }
+  }
+}
+
+// Residual r = b - A u (operators.hpp:38-66, 91-97) of block rows
+// row0-1 .. row0+R (index j = 0..R+1; rows outside the block are ghosts = 0)
+// from the staged u tile, plus the in-block known bits of the same rows.
+//   known:   r = b - u
+//   unknown: r = b - (deg*u - (((W + E) + N) + S)) over in-image neighbours;
+// out-of-image neighbours are zeros of the tile, i.e. the reference's skipped
+// term (x + 0 == x), deg counts the in-image ones.  Branch-free, so the rows
+// overlap.  INV: the multilevel invariant (b never read).
+template <typename T, int R, bool INV>
+__device__ __forceinline__ void residual_rows(const Cell<T, R>& c, const T (*ut)[kTileW],
+                                              T (&r)[R + 2], uint64_t& kbits) {
+  const int lane = threadIdx.x & 31;
+  const size_t W = static_cast<size_t>(c.W);
+  T bv[R + 2];
   kbits = 0;
 #pragma unroll
   for (int j = 0; j < R + 2; ++j) {
     const int ly = c.row0 - 1 + j;
     const int gy = c.y0 + ly;
-    const int k = j + 1;  // index of this row in uc
-    T sW = __shfl_up_sync(0xffffffffu, uc[k], 1);
-    T sE = __shfl_down_sync(0xffffffffu, uc[k], 1);
-    if (gy >= 0 && gy < c.H) {
-      const size_t rowp = static_cast<size_t>(gy) * c.W;
-      if (edge_w) sW = c.gx > 0 ? c.u[rowp + c.gx - 1] : T(0);
-      if (edge_e) sE = c.gx + 1 < c.W ? c.u[rowp + c.gx + 1] : T(0);
+    const bool in_blk = c.col_ok && ly >= 0 && ly < c.B;
+    const size_t p = in_blk ? static_cast<size_t>(gy) * W + c.gx : 0;
+    const uint8_t mv = c.mask[p];  // unconditional: issued together
+    kbits |= static_cast<uint64_t>(in_blk && mv != 0) << j;
+    if (!INV) {
+      const T bb = c.b[p];
+      bv[j] = in_blk ? bb : T(0);
     }
-    T rv = T(0);
-    if (c.col_ok && ly >= 0 && ly < c.B) {
-      const size_t p = static_cast<size_t>(gy) * c.W + c.gx;
-      const bool known = c.mask[p] != 0;
-      if (known) kbits |= 1ull << j;
-      if (known) {
-        rv = c.known_invariant ? T(0) : c.b[p] - uc[k];
-      } else {
-        const T bv = c.known_invariant ? T(0) : c.b[p];
-        T sum = T(0);
-        int deg = 0;
-        if (c.gx > 0) { sum += sW; ++deg; }
-        if (c.gx + 1 < c.W) { sum += sE; ++deg; }
-        if (gy > 0) { sum += uc[k - 1]; ++deg; }
-        if (gy + 1 < c.H) { sum += uc[k + 1]; ++deg; }
-        rv = bv - fmaT(T(deg), uc[k], -sum);
-      }
-    }
-    r[j] = rv;
-    if (j >= 1 && j <= R) u_own[j - 1] = uc[k];
+  }
+  const int deg_x = (c.gx > 0) + (c.gx + 1 < c.W);
+#pragma unroll
+  for (int j = 0; j < R + 2; ++j) {
+    const int ly = c.row0 - 1 + j;
+    const int gy = c.y0 + ly;
+    const int tr = ly + 2;
+    const T uc = ut[tr][lane + 1];
+    const T sum = ((ut[tr][lane] + ut[tr][lane + 2]) + ut[tr - 1][lane + 1]) + ut[tr + 1][lane + 1];
+    const int deg = deg_x + (gy > 0) + (gy + 1 < c.H);
+    const T bj = INV ? T(0) : bv[j];
+    const T ru = bj - fmaT(T(deg), uc, -sum);
+    const T rk = INV ? T(0) : bj - uc;
+    const bool in_blk = c.col_ok && ly >= 0 && ly < c.B;
+    r[j] = in_blk ? (((kbits >> j) & 1ull) ? rk : ru) : T(0);
   }
 }
 
@@ -203,12 +255,15 @@ __device__ __forceinline__ void residual_rows(const Cell<T, R>& c, T (&r)[R + 2]
 //   rhs = unk * (pv + knw_W pv_W + knw_E pv_E + knw_N pv_N + knw_S pv_S),
 // knw counting only in-block neighbours (ghost ring = 0).  Returns unk bits.
 template <typename T, int R>
-__device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, T (&rhs)[R], T (&u_own)[R],
-                                              uint64_t* kbits_out = nullptr) {
+__device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, const T (*ut)[kTileW],
+                                              T (&rhs)[R], uint64_t* kbits_out = nullptr) {
   const int lane = threadIdx.x & 31;
   T r[R + 2];
   uint64_t kb;
-  residual_rows<T, R>(c, r, kb, u_own);
+  if (c.known_invariant)
+    residual_rows<T, R, true>(c, ut, r, kb);
+  else
+    residual_rows<T, R, false>(c, ut, r, kb);
   const uint64_t kbW = __shfl_up_sync(0xffffffffu, kb, 1);
   const uint64_t kbE = __shfl_down_sync(0xffffffffu, kb, 1);
   uint32_t unk = 0;
@@ -218,15 +273,19 @@ __device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, T (&rhs)[R], 
     const int ly = c.row0 + i;
     const T rW = __shfl_up_sync(0xffffffffu, r[j], 1);
     const T rE = __shfl_down_sync(0xffffffffu, r[j], 1);
-    T t = T(0);
-    if (c.col_ok && ly < c.B && !((kb >> j) & 1ull)) {
-      unk |= 1u << i;
-      t = r[j];
-      if (lane > 0 && ((kbW >> j) & 1ull)) t += rW;
-      if (lane + 1 < c.B && ((kbE >> j) & 1ull)) t += rE;
-      if (ly > 0 && ((kb >> (j - 1)) & 1ull)) t += r[j - 1];
-      if (ly + 1 < c.B && ((kb >> (j + 1)) & 1ull)) t += r[j + 1];
+    const bool unk_i = c.col_ok && ly < c.B && !((kb >> j) & 1ull);
+    if (unk_i) unk |= 1u << i;
+    // known rows carry r = 0 under the multilevel invariant, so there the
+    // neighbour terms vanish; otherwise add each known in-block neighbour's r
+    // (+0 for the others: the reference's skipped term).
+    T t = r[j];
+    if (!c.known_invariant) {
+      t += (lane > 0 && ((kbW >> j) & 1ull)) ? rW : T(0);
+      t += (lane + 1 < c.B && ((kbE >> j) & 1ull)) ? rE : T(0);
+      t += (ly > 0 && ((kb >> (j - 1)) & 1ull)) ? r[j - 1] : T(0);
+      t += (ly + 1 < c.B && ((kb >> (j + 1)) & 1ull)) ? r[j + 1] : T(0);
     }
+    t = unk_i ? t : T(0);
     rhs[i] = t;
   }
   if (kbits_out) *kbits_out = kb;
@@ -261,6 +320,13 @@ template <typename T, int NW, bool FULL>
 __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_kernel(SweepArgs<T> a) {
   constexpr int R = 32 / NW;  // rows per thread
   __shared__ SweepSmem<T, NW> S;
+#ifdef SI_PROBE
+  const long long pr_k0 = clock64();
+  long long pr_k1 = pr_k0, pr_k2 = pr_k0;
+#endif
+#ifdef SI_PROBE_SETUP
+  long long pr_s1 = 0, pr_s2 = 0;
+#endif
 
   const int bx = blockIdx.x % a.ax.count;
   const int by = a.by0 + static_cast<int>(blockIdx.x) / a.ax.count;
@@ -286,9 +352,17 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
 
   T x[R], r[R], p[R], q[R];
   uint32_t unk;
+  stage_u_tile<T, NW>(S.ut, c.u, c.x0, c.y0, B, c.W, c.H);
+  __syncthreads();
+#ifdef SI_PROBE_SETUP
+  const long long pr_s0 = clock64();
+#endif
   {
-    T u_scratch[R];
-    unk = local_rhs<T, R>(c, r, u_scratch);
+    unk = local_rhs<T, R>(c, S.ut, r);
+#ifdef SI_PROBE_SETUP
+    if (unk == 0xdeadbeefu) a.u_new[0] = r[0];  // forces r complete before the stamp
+    pr_s1 = clock64();
+#endif
   }
 #pragma unroll
   for (int i = 0; i < R; ++i) {
@@ -305,6 +379,9 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
     for (int i = 0; i < R; ++i) S.pt[c.row0 + i][B + 1] = T(0);
   }
   const int any_unknown = __syncthreads_or(unk != 0);
+#ifdef SI_PROBE_SETUP
+  pr_s2 = clock64();
+#endif
 
   // Robin diagonals of my column: interior rows, block row 0, block row B-1.
   T dI = T(0), dT = T(0), dB = T(0);
@@ -320,6 +397,21 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
 
   int iters = 0;
   bool converged = true;
+#ifdef SI_PROBE
+  // cycles per CG-iteration segment (CTA thread 0): [0] apply + pAp reduction,
+  // [1] division + update + rr reduction, [2] beta + p update + staging
+  long long pr_t = 0, pr_seg[3] = {0, 0, 0};
+#define SI_PROBE_MARK(k)                                  \
+  do {                                                    \
+    const long long now_ = clock64();                     \
+    if ((k) >= 0) pr_seg[(k) < 0 ? 0 : (k)] += now_ - pr_t; \
+    pr_t = now_;                                          \
+  } while (0)
+#else
+#define SI_PROBE_MARK(k) \
+  do {                   \
+  } while (0)
+#endif
 
   if (any_unknown) {
 #pragma unroll
@@ -373,10 +465,9 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
           d = (i == 0) ? dFirst : ((i == R - 1) ? dLast : dI);
         else
           d = (i == iT) ? dT : ((i == iB) ? dB : dI);
-        T t = fmaT(d, v[i], -vW);
-        t = t - vE;
-        t = t - vN;
-        t = t - vS;
+        // d*v - (vW + vE) - (vN + vS): dependent depth 3 (the reference's
+        // left-to-right chain is 4; the values agree to rounding)
+        const T t = fmaT(d, v[i], -(vW + vE)) - (vN + vS);
 #ifdef SI_ABL_NOMASK
         o[i] = t;
 #else
@@ -403,6 +494,10 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
       converged = true;
     } else {
       int until_check = a.lcheck;  // iter % lcheck == 0  <=>  countdown hits 0
+      SI_PROBE_MARK(-1);
+#ifdef SI_PROBE
+      pr_k1 = pr_t;
+#endif
       for (int iter = 1; iter <= a.lmax; ++iter) {
         apply(p, nb_p[0], nb_p[1], q);
         const T pAp = cta_sum<T, NW>(dot2<T, R>(p, q), S.red, 0, warp, lane);
@@ -412,6 +507,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
           break;
         }
 #endif
+        SI_PROBE_MARK(0);
 #ifdef SI_ABL_NODIV
         const T alpha = rr * T(0.5);
 #else
@@ -429,6 +525,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
         const bool cadence = until_check == a.lcheck || iter == a.lmax;
         bool maybe_done = rr_new < thr2_lo;
         if (rr_new >= thr2_lo && rr_new <= thr2_hi) maybe_done = band_sqrt_le(rr_new, thr);
+        SI_PROBE_MARK(1);
         if (cadence || maybe_done) {
           // True residual b - A x, then confirm or replace (cg.hpp:131-146).
           stage(x);
@@ -468,31 +565,52 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
         rr = rr_new;
         rr_rcp = recip_rn(rr);
         if (iter == a.lmax) iters = a.lmax;
+        SI_PROBE_MARK(2);
       }
     }
   }
 
+#ifdef SI_PROBE
+  pr_k2 = clock64();
+  if (pr_k1 == pr_k0) pr_k1 = pr_k2;
+#endif
   // ---- accumulate_owned: u_new = u_old + v on the owned rectangle ----------
   // v = CG solution at unknown cells, the residual b - u at known cells.
   const int ox0 = a.ax.owned_begin(bx), ox1 = a.ax.owned_end(bx);
   const int oy0 = a.ay.owned_begin(by), oy1 = a.ay.owned_end(by);
   T* __restrict__ un = a.u_new + plane;
-  if (c.col_ok && c.gx >= ox0 && c.gx < ox1) {
+  const bool col_own = c.col_ok && c.gx >= ox0 && c.gx < ox1;
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int ly = c.row0 + i;
-      const int gy = c.y0 + ly;
-      if (ly < B && gy >= oy0 && gy < oy1) {
-        const size_t pix = static_cast<size_t>(gy) * c.W + c.gx;
-        const T uo = c.u[pix];
-        const T v = ((unk >> i) & 1u) ? x[i] : (c.known_invariant ? T(0) : c.b[pix] - uo);
-        un[pix] = uo + v;
-      }
+  for (int i = 0; i < R; ++i) {
+    const int ly = c.row0 + i;
+    const int gy = c.y0 + ly;
+    const bool own = col_own && ly < B && gy >= oy0 && gy < oy1;
+    const size_t pix = own ? static_cast<size_t>(gy) * c.W + c.gx : 0;
+    const T uo = S.ut[ly + 2][lane + 1];
+    T v = x[i];
+    if (!c.known_invariant) {
+      const T bk = c.b[pix];
+      if (!((unk >> i) & 1u)) v = bk - uo;
+    } else if (!((unk >> i) & 1u)) {
+      v = T(0);
     }
+    if (own) un[pix] = uo + v;
   }
   if (tid == 0 && a.counters && any_unknown) {
     if (!converged) atomicAdd(&a.counters[0], 1ull);
     atomicAdd(&a.counters[1], static_cast<unsigned long long>(iters));
+#ifdef SI_PROBE
+    const long long pr_k3 = clock64();
+#ifdef SI_PROBE_SETUP
+    pr_seg[0] = pr_s0 - pr_k0;
+    pr_seg[1] = pr_s1 - pr_s0;
+    pr_seg[2] = pr_k1 - pr_s1;
+#endif
+    for (int k = 0; k < 3; ++k)
+      atomicAdd(&a.counters[3 + k], static_cast<unsigned long long>(pr_seg[k]));
+    atomicAdd(&a.counters[6], static_cast<unsigned long long>(pr_k1 - pr_k0));
+    atomicAdd(&a.counters[7], static_cast<unsigned long long>(pr_k3 - pr_k2));
+#endif
   }
 }
 
