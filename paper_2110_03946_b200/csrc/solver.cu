@@ -316,12 +316,10 @@ void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_
   const int nw = sizeof(T) == 8 ? x.c.sweep_nw64 : x.c.sweep_nw32;
   if constexpr (sizeof(T) == 8) {
     if (nw == 2) launch_sweep_nw<T, 2>(x, a, nblocks, C);
-    else if (nw == 8) launch_sweep_nw<T, 8>(x, a, nblocks, C);
     else launch_sweep_nw<T, 4>(x, a, nblocks, C);
   } else {
     if (nw == 1) launch_sweep_nw<T, 1>(x, a, nblocks, C);
     else if (nw == 2) launch_sweep_nw<T, 2>(x, a, nblocks, C);
-    else if (nw == 8) launch_sweep_nw<T, 8>(x, a, nblocks, C);
     else launch_sweep_nw<T, 4>(x, a, nblocks, C);
   }
 }
