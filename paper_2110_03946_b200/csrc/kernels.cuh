@@ -67,19 +67,133 @@ __device__ __forceinline__ void reduce_epilogue(double v, double* partials, doub
 
 // K1: per channel sum of (b - A u)^2 (residual_into + vec::norm^2,
 // operators.hpp:38-66/91-97, cg.hpp:46-50); mode 1: sum of b^2 (RhsNorm).
-// Each warp walks a vertical strip of kResRows rows that is 32*V pixels
-// wide (V consecutive pixels per lane, vector loads when rows are aligned),
-// keeping the rows above and below in registers, so u is read from memory
-// once per pixel.  known_invariant: b is zero
-// at unknown pixels (the multilevel data flow), so it is only read where the
-// mask is set.
-constexpr int kResRows = 8;
+// Grid (x segments of kRedThreads columns, bands of kResBand rows, channel).
+// The CTA copies its band of u plus a one-pixel halo into shared memory with
+// cp.async (every load in flight at once, zero fill outside the image, u read
+// from memory once per pixel plus a 2-row halo per band), then each thread
+// evaluates the stencil of its column from shared memory.  known_invariant:
+// u == b at known pixels and b == 0 elsewhere (the multilevel data flow), so
+// b is never read.
+constexpr int kResBand = 16;
+constexpr int kResTileW = kRedThreads + 2;
+static_assert(kResBand + 2 <= 32, "halo loaders assume at most 32 band rows");
+
+__device__ __forceinline__ void cp_async_zfill(void* smem, const void* gmem, int bytes, bool ok) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int src = ok ? bytes : 0;
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src));
+}
+
+template <typename T, bool INV>
+__global__ void __launch_bounds__(kRedThreads)
+    residual_sumsq_kernel(const uint8_t* __restrict__ mask, const T* __restrict__ u,
+                          const T* __restrict__ b, int W, int H, size_t N, int mode, int row0,
+                          int row1, double* partials, double* out, unsigned int* ticket) {
+  // rows [row0, row1) only (stripe mode); the stencil still sees rows
+  // row0-1 and row1 as neighbours.
+  __shared__ T tile[kResBand + 2][kResTileW];
+  const int c = blockIdx.z;
+  const T* __restrict__ uc = u + c * N;
+  const T* __restrict__ bc = b + c * N;
+  const int x0 = blockIdx.x * kRedThreads;
+  const int x = x0 + threadIdx.x;
+  const int y0 = row0 + static_cast<int>(blockIdx.y) * kResBand;
+  const int ny = min(kResBand, row1 - y0);
+  const bool xin = x < W;
+  const size_t Wz = static_cast<size_t>(W);
+  double acc = 0.0;
+  if (mode == 1) {
+    T v[kResBand];
+#pragma unroll
+    for (int k = 0; k < kResBand; ++k)
+      v[k] = (xin && k < ny) ? __ldg(bc + static_cast<size_t>(y0 + k) * Wz + x) : T(0);
+#pragma unroll
+    for (int k = 0; k < kResBand; ++k) {
+      const double d = static_cast<double>(v[k]);
+      acc = fma(d, d, acc);
+    }
+  } else {
+    // tile[k][1 + j] = u(y0 - 1 + k, x0 + j); column 0 / kResTileW-1 = the
+    // halo columns x0 - 1 / x0 + kRedThreads.  Thread t copies column t of
+    // every band row; threads 0..17 and 32..49 copy one halo element each.
+    const int nrows = min(kResBand + 2, ny + 2);
+    const T* col = uc + x;
+#pragma unroll
+    for (int k = 0; k < kResBand + 2; ++k) {
+      const int gy = y0 - 1 + k;
+      const bool ok = k < nrows && gy >= 0 && gy < H && xin;
+      cp_async_zfill(&tile[k][threadIdx.x + 1], ok ? col + static_cast<ptrdiff_t>(gy) * W : uc,
+                     sizeof(T), ok);
+    }
+    {
+      const int t = threadIdx.x;
+      const bool west = t < kResBand + 2, east = t >= 32 && t < 32 + kResBand + 2;
+      if (west || east) {
+        const int k = west ? t : t - 32;
+        const int gy = y0 - 1 + k;
+        const int gx = west ? x0 - 1 : x0 + kRedThreads;
+        const bool ok = k < nrows && gy >= 0 && gy < H && gx >= 0 && gx < W;
+        cp_async_zfill(&tile[k][west ? 0 : kResTileW - 1],
+                       ok ? uc + static_cast<size_t>(gy) * Wz + gx : uc, sizeof(T), ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    // mask bytes (and b when the invariant does not hold) of my column,
+    // loaded while the copies are in flight
+    uint8_t mk[kResBand];
+    T bv[kResBand];
+    const size_t base = xin ? static_cast<size_t>(y0) * Wz + x : 0;
+#pragma unroll
+    for (int k = 0; k < kResBand; ++k) {
+      const bool in = xin && k < ny;
+      const size_t i = in ? base + static_cast<size_t>(k) * Wz : 0;
+      const uint8_t m = __ldg(mask + i);
+      mk[k] = in ? m : uint8_t(0);
+      if (!INV) {
+        const T bb = __ldg(bc + i);
+        bv[k] = in ? bb : T(0);
+      }
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+    const int t = threadIdx.x + 1;
+    const int deg_x = (x > 0) + (x + 1 < W);
+    const T deg_in = T(deg_x + 2);  // rows with both vertical neighbours
+    T up = tile[0][t], ctr = tile[1][t];
+#pragma unroll
+    for (int k = 0; k < kResBand; ++k) {
+      const int y = y0 + k;
+      const T dn = tile[k + 2][t];
+      // operators.hpp:44-58: ((W + E) + N) + S over in-image neighbours; an
+      // absent neighbour is a zero of the tile (x + 0 == x), deg counts the
+      // present ones.  Known pixels: r = b - u (+0 under the invariant).
+      const T sum = ((tile[k + 1][t - 1] + tile[k + 1][t + 1]) + up) + dn;
+      const T deg = (y > 0 && y + 1 < H) ? deg_in : T(deg_x + (y > 0) + (y + 1 < H));
+      const T au = fma(deg, ctr, -sum);
+      T r;
+      if (INV)
+        r = mk[k] ? T(0) : au;  // (0 - au)^2 == au^2
+      else
+        r = mk[k] ? bv[k] - ctr : bv[k] - au;
+      const double rd = (xin && k < ny) ? static_cast<double>(r) : 0.0;
+      acc = fma(rd, rd, acc);
+      up = ctr;
+      ctr = dn;
+    }
+  }
+  reduce_epilogue(acc, partials, out, ticket, blockIdx.y * gridDim.x + blockIdx.x,
+                  gridDim.x * gridDim.y, blockIdx.z, gridDim.z);
+}
 
 template <typename T>
 struct Pair {
   T a, b;
 };
 
+// Two horizontally adjacent values of a row (vector load when aligned).
 template <typename T, bool VEC>
 __device__ __forceinline__ Pair<T> load_pair(const T* __restrict__ row, int x, int W) {
   if (VEC) {
@@ -97,76 +211,6 @@ __device__ __forceinline__ Pair<T> load_pair(const T* __restrict__ row, int x, i
   if (x < W) r.a = row[x];
   if (x + 1 < W) r.b = row[x + 1];
   return r;
-}
-
-// V consecutive values of one row starting at x (zero outside [0, W)).
-template <typename T, int V, bool VEC>
-__device__ __forceinline__ void load_run(const T* __restrict__ row, int x, int W, T (&v)[V]) {
-  if (VEC && x + V <= W) {
-#pragma unroll
-    for (int k = 0; k < V; k += 2) {
-      const Pair<T> p = load_pair<T, true>(row, x + k, W);
-      v[k] = p.a;
-      v[k + 1] = p.b;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < V; ++k) v[k] = (x + k < W) ? row[x + k] : T(0);
-  }
-}
-
-// Grid (x segments of kRedThreads pixels, row groups, channel); each CTA
-// walks rows y = blockIdx.y, y += gridDim.y.  No integer division per pixel;
-// the five stencil reads of u hit L1/L2 (DRAM sees u once).
-template <typename T>
-__global__ void __launch_bounds__(kRedThreads)
-    residual_sumsq_kernel(const uint8_t* __restrict__ mask, const T* __restrict__ u,
-                          const T* __restrict__ b, int W, int H, size_t N, int mode,
-                          int known_invariant, int row0, int row1, double* partials, double* out,
-                          unsigned int* ticket) {
-  // rows [row0, row1) only (stripe mode); the stencil still sees rows
-  // row0-1 and row1 as neighbours.
-  const int c = blockIdx.z;
-  const T* __restrict__ uc = u + c * N;
-  const T* __restrict__ bc = b + c * N;
-  const int x = blockIdx.x * kRedThreads + threadIdx.x;
-  double acc = 0.0;
-  if (x < W) {
-    const bool hw = x > 0, he = x + 1 < W;
-#pragma unroll 2
-    for (int y = row0 + static_cast<int>(blockIdx.y); y < row1; y += gridDim.y) {
-      const size_t i = static_cast<size_t>(y) * W + x;
-      T r;
-      if (mode == 1) {
-        r = __ldg(bc + i);
-      } else {
-        const uint8_t m = __ldg(mask + i);
-        const T ctr = __ldg(uc + i);
-        const T vw = hw ? __ldg(uc + i - 1) : T(0);
-        const T ve = he ? __ldg(uc + i + 1) : T(0);
-        const T vn = y > 0 ? __ldg(uc + i - W) : T(0);
-        const T vs = y + 1 < H ? __ldg(uc + i + W) : T(0);
-        if (m) {
-          // invariant (multilevel data flow): u == b at known pixels, so the
-          // reference's b - u is exactly +0 there and b need not be read.
-          r = known_invariant ? T(0) : __ldg(bc + i) - ctr;
-        } else {
-          // operators.hpp:44-58: ((W + E) + N) + S over in-image neighbours
-          T sum = T(0);
-          int deg = 0;
-          if (hw) { sum += vw; ++deg; }
-          if (he) { sum += ve; ++deg; }
-          if (y > 0) { sum += vn; ++deg; }
-          if (y + 1 < H) { sum += vs; ++deg; }
-          r = (known_invariant ? T(0) : __ldg(bc + i)) - fma(T(deg), ctr, -sum);
-        }
-      }
-      const double rd = static_cast<double>(r);
-      acc = fma(rd, rd, acc);
-    }
-  }
-  reduce_epilogue(acc, partials, out, ticket, blockIdx.y * gridDim.x + blockIdx.x,
-                  gridDim.x * gridDim.y, blockIdx.z, gridDim.z);
 }
 
 // K6: per channel sum of (255 u - 255 f)^2 (mse_per_channel, metrics.hpp:30-47).

@@ -220,15 +220,20 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
   const size_t N = static_cast<size_t>(W) * H;
   const int rows = std::max(1, row1 - row0);
   const int gx = (W + kRedThreads - 1) / kRedThreads;
-  const int gy = std::max(1, std::min(rows, (2 * kRedBlocksMax + gx * C - 1) / (gx * C)));
+  const int gy = (rows + kResBand - 1) / kResBand;
   x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(gx) * gy * C);
   x.c.ticket.ensure(sizeof(unsigned int) * 4);
   // algorithmic bytes: u (or b) once per pixel per channel + the mask
   Timed t(x, K_RESIDUAL,
           static_cast<double>(W) * std::max(0, row1 - row0) * (C * sizeof(T) + (mode == 1 ? 0 : 1)));
-  residual_sumsq_kernel<T><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
-      mask, u, b, W, H, N, mode, known_invariant ? 1 : 0, row0, row1,
-      x.c.red_partials.as<double>(), out, x.c.ticket.as<unsigned int>());
+  if (known_invariant)
+    residual_sumsq_kernel<T, true><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
+        mask, u, b, W, H, N, mode, row0, row1, x.c.red_partials.as<double>(), out,
+        x.c.ticket.as<unsigned int>());
+  else
+    residual_sumsq_kernel<T, false><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
+        mask, u, b, W, H, N, mode, row0, row1, x.c.red_partials.as<double>(), out,
+        x.c.ticket.as<unsigned int>());
   CK(cudaGetLastError());
 }
 
