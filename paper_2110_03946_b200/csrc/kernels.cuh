@@ -3,6 +3,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace sib {
 
@@ -14,10 +15,10 @@ constexpr int kRedBlocksMax = 1184;  // 148 SMs x 8
 
 // K sums per CTA (v[k]); blk: this CTA's index among the nblk CTAs of its
 // channel chn (of nch).  Final results: out[k*nch + c].
-template <int K>
+template <int K, int NT = kRedThreads>
 __device__ void reduce_epilogue_k(const double (&vin)[K], double* partials, double* out,
                                   unsigned int* ticket, int blk, int nblk, int chn, int nch) {
-  __shared__ double wsum[K][kRedThreads / 32];
+  __shared__ double wsum[K][NT / 32];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -30,7 +31,7 @@ __device__ void reduce_epilogue_k(const double (&vin)[K], double* partials, doub
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       double s = 0.0;
-      for (int w = 0; w < kRedThreads / 32; ++w) s += wsum[k][w];
+      for (int w = 0; w < NT / 32; ++w) s += wsum[k][w];
       partials[(k * nch + chn) * nblk + blk] = s;
     }
     __threadfence();
@@ -43,7 +44,7 @@ __device__ void reduce_epilogue_k(const double (&vin)[K], double* partials, doub
   // Fixed-order final sum per (value, channel): strided partials + butterfly.
   for (int kc = 0; kc < K * nch; ++kc) {
     double s = 0.0;
-    for (int i = threadIdx.x; i < nblk; i += kRedThreads)
+    for (int i = threadIdx.x; i < nblk; i += NT)
       s += reinterpret_cast<volatile double*>(partials)[kc * nblk + i];
     s = warp_sum(s);
     __syncthreads();
@@ -51,18 +52,19 @@ __device__ void reduce_epilogue_k(const double (&vin)[K], double* partials, doub
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
-      for (int w = 0; w < kRedThreads / 32; ++w) t += wsum[0][w];
+      for (int w = 0; w < NT / 32; ++w) t += wsum[0][w];
       out[kc] = t;
     }
   }
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
+template <int NT = kRedThreads>
 __device__ __forceinline__ void reduce_epilogue(double v, double* partials, double* out,
                                                 unsigned int* ticket, int blk, int nblk, int chn,
                                                 int nch) {
   const double vv[1] = {v};
-  reduce_epilogue_k<1>(vv, partials, out, ticket, blk, nblk, chn, nch);
+  reduce_epilogue_k<1, NT>(vv, partials, out, ticket, blk, nblk, chn, nch);
 }
 
 // K1: per channel sum of (b - A u)^2 (residual_into + vec::norm^2,
@@ -186,6 +188,93 @@ __global__ void __launch_bounds__(kRedThreads)
   }
   reduce_epilogue(acc, partials, out, ticket, blockIdx.y * gridDim.x + blockIdx.x,
                   gridDim.x * gridDim.y, blockIdx.z, gridDim.z);
+}
+
+// K1 with the band tile fetched by one TMA box copy (tensor map over the
+// planar [C][H][W] iterate): 128 columns x kResBand rows per CTA, box
+// (x0 - kLead .. x0 + 127 + kLead) x (y0 - 1 .. y0 + kResBand), zero
+// outside the image.
+// Used when the row pitch is a multiple of 16 bytes (every level of an even
+// width in fp64); otherwise the cp.async kernel above runs.
+constexpr int kResTmaThreads = 128;
+// The box starts kLead = 16 / sizeof(T) columns left of the CTA's first
+// column (TMA wants 16-byte aligned inner box starts) and is 128 + 2 kLead
+// wide (a 16-byte multiple).
+template <typename T>
+__host__ __device__ constexpr int res_tma_lead() {
+  return 16 / static_cast<int>(sizeof(T));
+}
+template <typename T>
+__host__ __device__ constexpr int res_tma_box_w() {
+  return kResTmaThreads + 2 * res_tma_lead<T>();
+}
+
+template <typename T, bool INV>
+__global__ void __launch_bounds__(kResTmaThreads)
+    residual_sumsq_tma_kernel(const __grid_constant__ CUtensorMap umap,
+                              const uint8_t* __restrict__ mask, const T* __restrict__ b, int W,
+                              int H, size_t N, int row0, int row1, double* partials, double* out,
+                              unsigned int* ticket) {
+  __shared__ __align__(128) T tile[kResBand + 2][res_tma_box_w<T>()];
+  __shared__ uint64_t bar;
+  const int c = blockIdx.z;
+  const T* __restrict__ bc = b + c * N;
+  const int x0 = blockIdx.x * kResTmaThreads;
+  const int x = x0 + threadIdx.x;
+  const int y0 = row0 + static_cast<int>(blockIdx.y) * kResBand;
+  const int ny = min(kResBand, row1 - y0);
+  const bool xin = x < W;
+  const size_t Wz = static_cast<size_t>(W);
+  if (threadIdx.x == 0) {
+#ifdef SI_TMA_DEBUG
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
+      printf("tile smem %u (mod128 %u) bar %u bytes %u\n", smem_addr(&tile[0][0]),
+             smem_addr(&tile[0][0]) % 128, smem_addr(&bar), (unsigned)sizeof(tile));
+#endif
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, sizeof(tile));
+    tma_load_3d(&tile[0][0], &umap, x0 - res_tma_lead<T>(), y0 - 1, c, &bar);
+  }
+  uint8_t mk[kResBand];
+  T bv[kResBand];
+  const size_t base = xin ? static_cast<size_t>(y0) * Wz + x : 0;
+#pragma unroll
+  for (int k = 0; k < kResBand; ++k) {
+    const bool in = xin && k < ny;
+    const size_t i = in ? base + static_cast<size_t>(k) * Wz : 0;
+    const uint8_t m = __ldg(mask + i);
+    mk[k] = in ? m : uint8_t(0);
+    if (!INV) {
+      const T bb = __ldg(bc + i);
+      bv[k] = in ? bb : T(0);
+    }
+  }
+  __syncthreads();  // barrier initialised before anyone waits on it
+  mbar_wait(&bar, 0);
+  const int t = threadIdx.x + res_tma_lead<T>();
+  const int deg_x = (x > 0) + (x + 1 < W);
+  const T deg_in = T(deg_x + 2);
+  T up = tile[0][t], ctr = tile[1][t];
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < kResBand; ++k) {
+    const int y = y0 + k;
+    const T dn = tile[k + 2][t];
+    const T sum = ((tile[k + 1][t - 1] + tile[k + 1][t + 1]) + up) + dn;
+    const T deg = (y > 0 && y + 1 < H) ? deg_in : T(deg_x + (y > 0) + (y + 1 < H));
+    const T au = fma(deg, ctr, -sum);
+    T r;
+    if (INV)
+      r = mk[k] ? T(0) : au;
+    else
+      r = mk[k] ? bv[k] - ctr : bv[k] - au;
+    const double rd = (xin && k < ny) ? static_cast<double>(r) : 0.0;
+    acc = fma(rd, rd, acc);
+    up = ctr;
+    ctr = dn;
+  }
+  reduce_epilogue<kResTmaThreads>(acc, partials, out, ticket, blockIdx.y * gridDim.x + blockIdx.x,
+                                  gridDim.x * gridDim.y, blockIdx.z, gridDim.z);
 }
 
 template <typename T>

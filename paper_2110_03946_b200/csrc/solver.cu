@@ -5,6 +5,8 @@
 // outer loop's scalar decisions (rel <= tol, outer >= max_outer), exactly as
 // run_schwarz_level (schwarz.hpp:288-320) and multilevel_solve
 // (multilevel.hpp:239-310) take them.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -212,6 +214,41 @@ int grid_for(size_t n, int threads, int cap) {
 }
 
 // ---------------------------------------------------------------- launches
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 3-D map over a planar [C][H][W] buffer with a (box_w, box_h, 1) box; false
+// when TMA cannot address it (row pitch or base not 16-byte aligned).
+bool make_plane_map(CUtensorMap* m, const void* base, int W, int H, int C, int elem, int box_w,
+                    int box_h) {
+  auto enc = tensor_map_encoder();
+  if (!enc || (static_cast<size_t>(W) * elem) % 16 != 0 ||
+      reinterpret_cast<uintptr_t>(base) % 16 != 0 || (box_w * elem) % 16 != 0 || box_w > 256 ||
+      box_h > 256)
+    return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                              static_cast<cuuint64_t>(C)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(W) * elem,
+                                 static_cast<cuuint64_t>(W) * H * elem};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+             const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename T>
 void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W, int H, int C,
                      int mode, double* out, bool known_invariant = true, int row0 = 0,
@@ -226,14 +263,28 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
   // algorithmic bytes: u (or b) once per pixel per channel + the mask
   Timed t(x, K_RESIDUAL,
           static_cast<double>(W) * std::max(0, row1 - row0) * (C * sizeof(T) + (mode == 1 ? 0 : 1)));
-  if (known_invariant)
+  CUtensorMap map;
+  if (mode != 1 && !std::getenv("SI_NO_TMA") &&
+      make_plane_map(&map, u, W, H, C, sizeof(T), res_tma_box_w<T>(), kResBand + 2)) {
+    const int tx = (W + kResTmaThreads - 1) / kResTmaThreads;
+    x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(tx) * gy * C);
+    if (known_invariant)
+      residual_sumsq_tma_kernel<T, true><<<dim3(tx, gy, C), kResTmaThreads, 0, x.s>>>(
+          map, mask, b, W, H, N, row0, row1, x.c.red_partials.as<double>(), out,
+          x.c.ticket.as<unsigned int>());
+    else
+      residual_sumsq_tma_kernel<T, false><<<dim3(tx, gy, C), kResTmaThreads, 0, x.s>>>(
+          map, mask, b, W, H, N, row0, row1, x.c.red_partials.as<double>(), out,
+          x.c.ticket.as<unsigned int>());
+  } else if (known_invariant) {
     residual_sumsq_kernel<T, true><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
         mask, u, b, W, H, N, mode, row0, row1, x.c.red_partials.as<double>(), out,
         x.c.ticket.as<unsigned int>());
-  else
+  } else {
     residual_sumsq_kernel<T, false><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
         mask, u, b, W, H, N, mode, row0, row1, x.c.red_partials.as<double>(), out,
         x.c.ticket.as<unsigned int>());
+  }
   CK(cudaGetLastError());
 }
 
