@@ -228,6 +228,12 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+// SI_NO_TMA=1 forces the cooperative / cp.async staging paths (A/B runs).
+bool tma_disabled() {
+  static const bool off = std::getenv("SI_NO_TMA") != nullptr;
+  return off;
+}
+
 // 3-D map over a planar [C][H][W] buffer with a (box_w, box_h, 1) box; false
 // when TMA cannot address it (row pitch or base not 16-byte aligned).
 bool make_plane_map(CUtensorMap* m, const void* base, int W, int H, int C, int elem, int box_w,
@@ -264,7 +270,7 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
   Timed t(x, K_RESIDUAL,
           static_cast<double>(W) * std::max(0, row1 - row0) * (C * sizeof(T) + (mode == 1 ? 0 : 1)));
   CUtensorMap map;
-  if (mode != 1 && !std::getenv("SI_NO_TMA") &&
+  if (mode != 1 && !tma_disabled() &&
       make_plane_map(&map, u, W, H, C, sizeof(T), res_tma_box_w<T>(), kResBand + 2)) {
     const int tx = (W + kResTmaThreads - 1) / kResTmaThreads;
     x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(tx) * gy * C);
@@ -364,6 +370,14 @@ void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_
   a.counters = counters;
   if (by1 < 0) by1 = a.ay.count;
   a.by0 = by0;
+  // TMA tile loads need 16-byte aligned box starts x0 - 2, i.e. even block
+  // anchors (k * stride, and W - B for the last) in fp64; fp32 would need
+  // x0 = 2 mod 4, which anchor 0 never is, so fp32 stages cooperatively.
+  {
+    const bool anchors_ok = a.ax.count == 1 || (a.ax.stride % 2 == 0 && (W - a.ax.block) % 2 == 0);
+    a.use_tma = sizeof(T) == 8 && anchors_ok && !tma_disabled() &&
+                make_plane_map(&a.umap, u_old, W, H, C, sizeof(T), kTileW, kTileH);
+  }
   const int nblocks = a.ax.count * (by1 - by0);
   if (nblocks <= 0) return;
   const double bytes = static_cast<double>(a.N) * (2.0 * C * sizeof(T) + 1.0) * (by1 - by0) /

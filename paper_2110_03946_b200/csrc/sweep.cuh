@@ -29,14 +29,20 @@
 #pragma once
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace sib {
 
 // u_old tile of a block: rows y0-2 .. y0+B+1, columns x0-1 .. x0+B.
-constexpr int kTileW = kMaxBlock + 2, kTileH = kMaxBlock + 4;
+// Column j of the tile is x = x0 - 2 + j (a 16-byte aligned start for the
+// TMA box when x0 is even), so the block's columns are j = 2 .. B+1 and the
+// ring columns j = 1 and j = B+2.
+constexpr int kTileW = kMaxBlock + 4, kTileH = kMaxBlock + 4;
 
 template <typename T>
 struct SweepArgs {
+  CUtensorMap umap;    // TMA map of u_old ([C][H][W], box kTileW x kTileH) when use_tma
+  int use_tma;
   const uint8_t* mask;
   const T* b;
   const T* u_old;
@@ -75,9 +81,10 @@ __device__ __forceinline__ T robin_diag(int gx, int gy, int lx, int ly, int B, i
 
 template <typename T, int NW>
 struct SweepSmem {
+  __align__(128) T ut[kTileH][kTileW];  // u_old tile with halo (TMA destination)
+  uint64_t bar;                    // TMA completion
   T pt[kMaxBlock][kMaxBlock + 2];  // stencil operand rows, zero ghost columns 0 and B+1
   T bt[kMaxBlock][kMaxBlock];      // local right-hand side (true-residual checks)
-  T ut[kTileH][kTileW];            // u_old tile with halo (residual, write-back)
   T pub[NW][2][3][32];             // [warp][top/bottom][r,p,x][col]
   T pubt[NW][2][32];               // true-residual boundary rows
   T red[3][NW];
@@ -199,9 +206,9 @@ __device__ __forceinline__ void stage_u_tile(T (*ut)[kTileW], const T* __restric
   for (int i = 0; i < kRows; ++i) {
     const int tr = warp + i * NW;
     if (tr < kTileH) {
-      ut[tr][lane + 1] = v[i];
-      if (lane == 30) ut[tr][0] = e[i];
-      if (lane == 31) ut[tr][kTileW - 1] = e[i];
+      ut[tr][lane + 2] = v[i];
+      if (lane == 30) ut[tr][1] = e[i];
+      if (lane == 31) ut[tr][kMaxBlock + 2] = e[i];
     }
   }
 }
@@ -240,8 +247,8 @@ __device__ __forceinline__ void residual_rows(const Cell<T, R>& c, const T (*ut)
     const int ly = c.row0 - 1 + j;
     const int gy = c.y0 + ly;
     const int tr = ly + 2;
-    const T uc = ut[tr][lane + 1];
-    const T sum = ((ut[tr][lane] + ut[tr][lane + 2]) + ut[tr - 1][lane + 1]) + ut[tr + 1][lane + 1];
+    const T uc = ut[tr][lane + 2];
+    const T sum = ((ut[tr][lane + 1] + ut[tr][lane + 3]) + ut[tr - 1][lane + 2]) + ut[tr + 1][lane + 2];
     const int deg = deg_x + (gy > 0) + (gy + 1 < c.H);
     const T bj = INV ? T(0) : bv[j];
     const T ru = bj - fmaT(T(deg), uc, -sum);
@@ -317,7 +324,8 @@ struct SweepOcc {
 // wide and high with the default block size), so the Robin rows are
 // compile-time positions.
 template <typename T, int NW, bool FULL>
-__global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_kernel(SweepArgs<T> a) {
+__global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
+    oras_sweep_kernel(const __grid_constant__ SweepArgs<T> a) {
   constexpr int R = 32 / NW;  // rows per thread
   __shared__ SweepSmem<T, NW> S;
 #ifdef SI_PROBE
@@ -352,8 +360,20 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
 
   T x[R], r[R], p[R], q[R];
   uint32_t unk;
-  stage_u_tile<T, NW>(S.ut, c.u, c.x0, c.y0, B, c.W, c.H);
-  __syncthreads();
+  if (a.use_tma) {
+    // one TMA box: rows y0-2 .. y0+33, columns x0-2 .. x0+33 of this channel,
+    // zeros outside the image
+    if (tid == 0) {
+      mbar_init(&S.bar, 1);
+      mbar_expect_tx(&S.bar, sizeof(S.ut));
+      tma_load_3d(&S.ut[0][0], &a.umap, c.x0 - 2, c.y0 - 2, ch, &S.bar);
+    }
+    __syncthreads();
+    mbar_wait(&S.bar, 0);
+  } else {
+    stage_u_tile<T, NW>(S.ut, c.u, c.x0, c.y0, B, c.W, c.H);
+    __syncthreads();
+  }
 #ifdef SI_PROBE_SETUP
   const long long pr_s0 = clock64();
 #endif
@@ -586,7 +606,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value)) oras_sweep_
     const int gy = c.y0 + ly;
     const bool own = col_own && ly < B && gy >= oy0 && gy < oy1;
     const size_t pix = own ? static_cast<size_t>(gy) * c.W + c.gx : 0;
-    const T uo = S.ut[ly + 2][lane + 1];
+    const T uo = S.ut[ly + 2][lane + 2];
     T v = x[i];
     if (!c.known_invariant) {
       const T bk = c.b[pix];

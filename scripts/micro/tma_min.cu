@@ -57,5 +57,9 @@ int main(int argc, char** argv) {
   if (which == 3) run<double, 136, 18>(256, 256, -2, -1, CU_TENSOR_MAP_DATA_TYPE_FLOAT64);
   if (which == 4) run<float, 144, 18>(256, 256, -2, -1, CU_TENSOR_MAP_DATA_TYPE_UINT32);
   if (which == 5) run<float, 64, 18>(256, 256, -2, -1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+  if (which == 6) run<float, 144, 18>(256, 256, 2, 0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+  if (which == 7) run<float, 144, 18>(256, 256, -4, -1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
+  if (which == 8) run<double, 36, 36>(256, 256, 3, 5, CU_TENSOR_MAP_DATA_TYPE_FLOAT64);
+  if (which == 9) run<double, 36, 36>(256, 256, -1, -2, CU_TENSOR_MAP_DATA_TYPE_FLOAT64);
   return 0;
 }
