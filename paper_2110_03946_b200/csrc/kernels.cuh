@@ -388,27 +388,7 @@ __global__ void restrict_kernel(const uint8_t* __restrict__ fmask, const T* __re
 
 // K4: prolongate (multilevel.hpp:101-128) + snap known fine pixels to their
 // data (multilevel.hpp:294-303): cell-centred bilinear, coordinate
-// 0.5*f - 0.25 clamped to the coarse grid.  One thread per horizontal pair
-// of fine pixels (they share coarse samples); coarse reads hit L1/L2.
-template <typename T>
-__device__ __forceinline__ T prolong_px_unused(const T* __restrict__ cc, int cw, int ch, int fx, int fy) {
-  const double yc = fmin(fmax(0.5 * fy - 0.25, 0.0), static_cast<double>(ch - 1));
-  const double xc = fmin(fmax(0.5 * fx - 0.25, 0.0), static_cast<double>(cw - 1));
-  const int y0 = static_cast<int>(yc), x0 = static_cast<int>(xc);
-  const int y1 = min(y0 + 1, ch - 1), x1 = min(x0 + 1, cw - 1);
-  const T ty = static_cast<T>(yc - y0), tx = static_cast<T>(xc - x0);
-  const T v00 = __ldg(cc + static_cast<size_t>(y0) * cw + x0);
-  const T v01 = __ldg(cc + static_cast<size_t>(y0) * cw + x1);
-  const T v10 = __ldg(cc + static_cast<size_t>(y1) * cw + x0);
-  const T v11 = __ldg(cc + static_cast<size_t>(y1) * cw + x1);
-  // (1-ty)*((1-tx)*v00 + tx*v01) + ty*((1-tx)*v10 + tx*v11), with the
-  // contraction gcc -O3 applies to the reference expression
-  // (p*q + r*s -> fma(p, q, r*s); checked bitwise in the tests).
-  const T a0 = fma(T(1) - tx, v00, tx * v01);
-  const T a1 = fma(T(1) - tx, v10, tx * v11);
-  return fma(T(1) - ty, a0, ty * a1);
-}
-
+// 0.5*f - 0.25 clamped to the coarse grid.
 // Fine tile 64 x 16 per CTA (256 threads, a 2x2 quad each); the coarse
 // window it samples (34 x 10 per channel) is staged in shared memory.
 constexpr int kProX = 64, kProY = 16, kProCX = kProX / 2 + 2, kProCY = kProY / 2 + 2;
@@ -453,41 +433,53 @@ __global__ void __launch_bounds__(256, 4)
       tile[k][ly][lx] = __ldg(coarse + (c0 + k) * cn + static_cast<size_t>(gy) * cw + gx);
     }
     __syncthreads();
+    // the quad's two columns share the x interpolation across channels;
+    // each row of the quad leaves as one 16-byte (fp64) / 8-byte (fp32) store
+    double txd[2];
+    int xb0[2], xb1[2];
+#pragma unroll
+    for (int dx = 0; dx < 2; ++dx) {
+      int xa, xb;
+      prolong_axis<T>(min(fxq + dx, fw - 1), cw, txd[dx], xa, xb);
+      xb0[dx] = xa - cx0;
+      xb1[dx] = xb - cx0;
+    }
+    const bool pair_store = (fw % 2 == 0) && fxq + 1 < fw;
 #pragma unroll
     for (int dy = 0; dy < 2; ++dy) {
       const int fy = fyq + dy;
-      if (fy >= fh) continue;
+      if (fy >= fh || fxq >= fw) continue;
       double tyd;
       int ya, yb;
       prolong_axis<T>(fy, ch, tyd, ya, yb);
       const T ty = static_cast<T>(tyd);
       const int a0 = ya - cy0, a1 = yb - cy0;
+      const size_t i = static_cast<size_t>(fy) * fw + fxq;
+      for (int k = 0; k < nc; ++k) {
+        T v[2];
 #pragma unroll
-      for (int dx = 0; dx < 2; ++dx) {
-        const int fx = fxq + dx;
-        if (fx >= fw) continue;
-        double txd;
-        int xa, xb;
-        prolong_axis<T>(fx, cw, txd, xa, xb);
-        const T tx = static_cast<T>(txd);
-        const int b0 = xa - cx0, b1 = xb - cx0;
-        const size_t i = static_cast<size_t>(fy) * fw + fx;
-        const bool s = (snap >> (2 * dy + dx)) & 1u;
-        for (int k = 0; k < nc; ++k) {
-          T v;
-          if (s) {
-            v = fval[(c0 + k) * fn + i];
-          } else {
-            const T v00 = tile[k][a0][b0], v01 = tile[k][a0][b1];
-            const T v10 = tile[k][a1][b0], v11 = tile[k][a1][b1];
-            // (1-ty)*((1-tx)*v00 + tx*v01) + ty*((1-tx)*v10 + tx*v11), with the
-            // contraction gcc -O3 applies to the reference expression
-            // (p*q + r*s -> fma(p, q, r*s); checked bitwise in the tests).
-            const T p0 = fma(T(1) - tx, v00, tx * v01);
-            const T p1 = fma(T(1) - tx, v10, tx * v11);
-            v = fma(T(1) - ty, p0, ty * p1);
-          }
-          fine[(c0 + k) * fn + i] = v;
+        for (int dx = 0; dx < 2; ++dx) {
+          const T tx = static_cast<T>(txd[dx]);
+          const int b0 = xb0[dx], b1 = xb1[dx];
+          const T v00 = tile[k][a0][b0], v01 = tile[k][a0][b1];
+          const T v10 = tile[k][a1][b0], v11 = tile[k][a1][b1];
+          // (1-ty)*((1-tx)*v00 + tx*v01) + ty*((1-tx)*v10 + tx*v11), with the
+          // contraction gcc -O3 applies to the reference expression
+          // (p*q + r*s -> fma(p, q, r*s); checked bitwise in the tests).
+          const T p0 = fma(T(1) - tx, v00, tx * v01);
+          const T p1 = fma(T(1) - tx, v10, tx * v11);
+          v[dx] = fma(T(1) - ty, p0, ty * p1);
+          if ((snap >> (2 * dy + dx)) & 1u) v[dx] = fval[(c0 + k) * fn + i + dx];
+        }
+        T* dst = fine + (c0 + k) * fn + i;
+        if (pair_store) {
+          if constexpr (sizeof(T) == 8)
+            *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[1]);
+          else
+            *reinterpret_cast<float2*>(dst) = make_float2(v[0], v[1]);
+        } else {
+          dst[0] = v[0];
+          if (fxq + 1 < fw) dst[1] = v[1];
         }
       }
     }
