@@ -8,6 +8,8 @@ Bar (stated per assertion):
 Behavioural tests port schwarz_test.cpp / multilevel_test.cpp /
 acceptance_test.cpp properties to the GPU path.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -87,6 +89,16 @@ RANDOM_CASES = [
     (33, 17, 2, 0.3, si.Method.MultilevelOras, dict(averaging=si.CoarseAveraging.AllPixels,
                                                     normalizer=si.ResidualNormalizer.RhsNorm)),
     (300, 170, 3, 0.02, si.Method.MultilevelOras, dict(alpha=0.5, block_size=24, overlap=5)),
+    # degenerate shapes: clamped partitions down to 1x1 blocks
+    (1, 2, 1, 0.5, si.Method.MultilevelOras, dict()),
+    (1, 37, 2, 0.2, si.Method.MultilevelOras, dict(max_outer_iterations=60)),
+    (53, 1, 1, 0.2, si.Method.Oras, dict(block_size=8, overlap=2, max_outer_iterations=60)),
+    (2, 2, 3, 0.5, si.Method.MultilevelOras, dict(levels=3)),
+    # staging paths: odd stride / odd W - B (cooperative) vs even anchors (TMA box)
+    (777, 333, 3, 0.04, si.Method.MultilevelOras, dict()),
+    (1000, 600, 3, 0.04, si.Method.MultilevelOras, dict()),
+    (200, 150, 3, 0.05, si.Method.Oras, dict(overlap=5)),
+    (180, 90, 8, 0.05, si.Method.MultilevelOras, dict(overlap=2, levels=2)),
 ]
 
 
@@ -360,3 +372,29 @@ def test_pnm_batch_matches_decoded_pipeline(solver, oracle, w, h, c):
         ora = oracle.oracle_solve(fd.data, m.known, levels=2)
         diff = np.abs(out.astype(int) - si.quantise_pnm(si.ImageBuffer(data=ora.image)).astype(int))
         assert diff.max() <= 1 and np.count_nonzero(diff) <= max(1, diff.size // 10000)
+
+
+def test_tma_and_cooperative_staging_agree_bitwise(tmp_path):
+    """The sweep and residual kernels stage tiles by TMA where the box start is
+    16-byte aligned and cooperatively otherwise (SI_NO_TMA=1 forces the
+    latter): same arithmetic, so bit-identical results."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import paper_2110_03946_b200 as si\n"
+        "from instances import random_instance\n"
+        "f, m = random_instance(640, 480, 0.04, 3, 5)\n"
+        "r = si.Solver(0).run_method(si.Method.MultilevelOras, f, m, si.RunOptions())\n"
+        "np.save(sys.argv[1], r.image.data)\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+         os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for k, env_extra in enumerate(({}, {"SI_NO_TMA": "1"})):
+        path = str(tmp_path / f"u{k}.npy")
+        env = dict(os.environ, **env_extra)
+        run = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True,
+                             text=True, timeout=300)
+        assert run.returncode == 0, run.stderr
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
