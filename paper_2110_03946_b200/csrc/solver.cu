@@ -174,7 +174,6 @@ struct Timed {
   double bytes;
   cudaEvent_t a = nullptr, b = nullptr;
   Timed(Ctx& x_, int k, double by) : x(x_), kind(k), bytes(by) {
-    x.c.launch_count += 1;
     if (x.c.profiling) {
       a = take_event(x.c);
       b = take_event(x.c);
@@ -274,19 +273,24 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
       make_plane_map(&map, u, W, H, C, sizeof(T), res_tma_box_w<T>(), kResBand + 2)) {
     const int tx = (W + kResTmaThreads - 1) / kResTmaThreads;
     x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(tx) * gy * C);
-    if (known_invariant)
+    if (known_invariant) {
+      ++x.c.launch_count;
       residual_sumsq_tma_kernel<T, true><<<dim3(tx, gy, C), kResTmaThreads, 0, x.s>>>(
           map, mask, b, W, H, N, row0, row1, x.c.red_partials.as<double>(), out,
           x.c.ticket.as<unsigned int>());
-    else
+    } else {
+      ++x.c.launch_count;
       residual_sumsq_tma_kernel<T, false><<<dim3(tx, gy, C), kResTmaThreads, 0, x.s>>>(
           map, mask, b, W, H, N, row0, row1, x.c.red_partials.as<double>(), out,
           x.c.ticket.as<unsigned int>());
+    }
   } else if (known_invariant) {
+    ++x.c.launch_count;
     residual_sumsq_kernel<T, true><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
         mask, u, b, W, H, N, mode, row0, row1, x.c.red_partials.as<double>(), out,
         x.c.ticket.as<unsigned int>());
   } else {
+    ++x.c.launch_count;
     residual_sumsq_kernel<T, false><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
         mask, u, b, W, H, N, mode, row0, row1, x.c.red_partials.as<double>(), out,
         x.c.ticket.as<unsigned int>());
@@ -300,6 +304,7 @@ void launch_sq_error(Ctx& x, const T* u, const double* f, size_t N, int C, doubl
   x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(g) * C);
   x.c.ticket.ensure(sizeof(unsigned int) * 4);
   Timed t(x, K_METRIC, static_cast<double>(N) * C * (sizeof(T) + 8.0));
+  ++x.c.launch_count;
   sq_error_kernel<T><<<dim3(g, C), kRedThreads, 0, x.s>>>(
       u, f, N, x.c.red_partials.as<double>(), out, x.c.ticket.as<unsigned int>());
   CK(cudaGetLastError());
@@ -310,10 +315,13 @@ void launch_restrict(Ctx& x, const uint8_t* fmask, const T* fval, int fw, int fh
                      int averaging, uint8_t* cmask, T* cval) {
   const int cw = (fw + 1) / 2, ch = (fh + 1) / 2;
   const dim3 grid((cw + 127) / 128, ch);
-  if (fw % 2 == 0 && reinterpret_cast<uintptr_t>(fval) % 16 == 0)
+  if (fw % 2 == 0 && reinterpret_cast<uintptr_t>(fval) % 16 == 0) {
+    ++x.c.launch_count;
     restrict_kernel<T, true><<<grid, 128, 0, x.s>>>(fmask, fval, fw, fh, C, averaging, cmask, cval);
-  else
+  } else {
+    ++x.c.launch_count;
     restrict_kernel<T, false><<<grid, 128, 0, x.s>>>(fmask, fval, fw, fh, C, averaging, cmask, cval);
+  }
   CK(cudaGetLastError());
 }
 
@@ -321,6 +329,7 @@ template <typename T>
 void launch_prolong(Ctx& x, const T* coarse, int cw, int ch, int fw, int fh, int C,
                     const uint8_t* fmask, const T* fval, T* fine) {
   const dim3 grid((fw + kProX - 1) / kProX, (fh + kProY - 1) / kProY);
+  ++x.c.launch_count;
   prolong_snap_kernel<T><<<grid, 256, 0, x.s>>>(coarse, cw, ch, fw, fh, C, fmask, fval, fine);
   CK(cudaGetLastError());
 }
@@ -337,11 +346,15 @@ void launch_sweep_nw(Ctx& x, const SweepArgs<T>& a, int nblocks, int C) {
     x.c.scratch.ensure(sizeof(T) * kMaxBlock * kMaxBlock * static_cast<size_t>(nblocks) * C);
     SweepArgs<T> aw = a;
     aw.scratch = x.c.scratch.as<T>();
+    ++x.c.launch_count;
     oras_sweep_warp_kernel<T><<<dim3(nblocks, C), 32, 0, x.s>>>(aw);
-  } else if (a.ax.block == kMaxBlock)
+  } else if (a.ax.block == kMaxBlock) {
+    ++x.c.launch_count;
     oras_sweep_kernel<T, NW, true><<<dim3(nblocks, C), NW * 32, 0, x.s>>>(a);
-  else
+  } else {
+    ++x.c.launch_count;
     oras_sweep_kernel<T, NW, false><<<dim3(nblocks, C), NW * 32, 0, x.s>>>(a);
+  }
   CK(cudaGetLastError());
 }
 
@@ -542,12 +555,14 @@ __global__ void copy_u64_kernel(const unsigned long long* src, unsigned long lon
 
 void begin_counters(Ctx& x) {
   x.c.counters.ensure(sizeof(unsigned long long) * 8);
+  ++x.c.launch_count;
   copy_u64_kernel<<<1, 32, 0, x.s>>>(x.c.counters.as<unsigned long long>(), nullptr, 8, true);
   CK(cudaGetLastError());
 }
 
 // device counters -> mapped host memory, then wait
 void publish_counters(Ctx& x, int n) {
+  ++x.c.launch_count;
   copy_u64_kernel<<<1, 32, 0, x.s>>>(x.c.counters.as<unsigned long long>(), x.c.dev_cnt, n, false);
   CK(cudaGetLastError());
   sync(x);
@@ -595,6 +610,7 @@ LevelOutcome run_cg_level(Ctx& x, LevelView<T>& V, int C, double tol, const si_o
 
   {
     Timed t(x, K_RESIDUAL, 6 * vec_bytes);
+    ++x.c.launch_count;
     cg_init_kernel<T><<<grid, kRedThreads, 0, x.s>>>(V.mask, V.b, V.u[V.cur], rhs, xv, r, p, W, H,
                                                      N, P(), red, tk());
     CK(cudaGetLastError());
@@ -607,6 +623,7 @@ LevelOutcome run_cg_level(Ctx& x, LevelView<T>& V, int C, double tol, const si_o
     if (!sink || !tr.fn) return;
     double qv = std::numeric_limits<double>::quiet_NaN();
     if (d_ref) {
+      ++x.c.launch_count;
       cg_embed_kernel<T><<<grid, kRedThreads, 0, x.s>>>(V.mask, V.b, xv, V.u[V.cur ^ 1], W, H, N);
       launch_sq_error<T>(x, V.u[V.cur ^ 1], d_ref, N, C, x.c.dev_red + 3 * C);
       sync(x);
@@ -647,6 +664,7 @@ LevelOutcome run_cg_level(Ctx& x, LevelView<T>& V, int C, double tol, const si_o
       }
       if (active) {
         Timed t(x, K_SWEEP, 2 * vec_bytes);
+        ++x.c.launch_count;
         cg_apply_dot_kernel<T><<<grid, kRedThreads, 0, x.s>>>(V.mask, p, q, W, H, N, active, P(),
                                                               red, tk());
         CK(cudaGetLastError());
@@ -667,6 +685,7 @@ LevelOutcome run_cg_level(Ctx& x, LevelView<T>& V, int C, double tol, const si_o
       }
       if (upd) {
         Timed t(x, K_SWEEP, 5 * vec_bytes);
+        ++x.c.launch_count;
         cg_update_kernel<T><<<grid, kRedThreads, 0, x.s>>>(xv, p, r, q, W, H, N, upd, alpha, P(),
                                                            red, tk());
         CK(cudaGetLastError());
@@ -692,6 +711,7 @@ LevelOutcome run_cg_level(Ctx& x, LevelView<T>& V, int C, double tol, const si_o
           if (!frozen[c]) replace |= 1u << c;
         {
           Timed t(x, K_RESIDUAL, 3 * vec_bytes);
+          ++x.c.launch_count;
           cg_true_residual_kernel<T><<<grid, kRedThreads, 0, x.s>>>(V.mask, rhs, xv, r, W, H, N,
                                                                     replace, P(), red, tk());
           CK(cudaGetLastError());
@@ -721,6 +741,7 @@ LevelOutcome run_cg_level(Ctx& x, LevelView<T>& V, int C, double tol, const si_o
         pa |= 1u << c;
       }
       if (pa) {
+        ++x.c.launch_count;
         cg_pupdate_kernel<T><<<grid, kRedThreads, 0, x.s>>>(p, r, W, H, N, pa, beta);
         CK(cudaGetLastError());
       }
@@ -728,6 +749,7 @@ LevelOutcome run_cg_level(Ctx& x, LevelView<T>& V, int C, double tol, const si_o
     if (!done) out.iterations = maxit;
   }
   // embed_solution (reduction.hpp:138-145) into the level's iterate
+  ++x.c.launch_count;
   cg_embed_kernel<T><<<grid, kRedThreads, 0, x.s>>>(V.mask, V.b, xv, V.u[V.cur ^ 1], W, H, N);
   CK(cudaGetLastError());
   V.cur ^= 1;
@@ -769,6 +791,7 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
   const size_t n0 = static_cast<size_t>(w) * h;
   {
     Timed t(x, K_INGEST, static_cast<double>(n0) * (C * (8.0 + sizeof(T)) + 1.0));
+    ++x.c.launch_count;
     ingest_kernel<T><<<grid_for(n0, 256, 148 * 16), 256, 0, x.s>>>(
         d_f, d_mask, n0, C, x.c.levels[0].b.as<T>(), x.c.counters.as<unsigned long long>() + 2);
     CK(cudaGetLastError());
@@ -787,6 +810,7 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
     const size_t n = static_cast<size_t>(V.w) * V.h;
     if (level == depth - 1) {
       // canonical start u0 = b on the coarsest level (multilevel.hpp:267-273)
+      ++x.c.launch_count;
       convert_kernel<T, T><<<grid_for(n * C, 256, 148 * 16), 256, 0, x.s>>>(V.b, V.u[0], n * C);
       CK(cudaGetLastError());
       V.cur = 0;
@@ -850,6 +874,7 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
   // Export the finest u (T -> double).
   {
     Timed t(x, K_INGEST, static_cast<double>(n0) * C * (8.0 + sizeof(T)));
+    ++x.c.launch_count;
     convert_kernel<T, double><<<grid_for(n0 * C, 256, 148 * 16), 256, 0, x.s>>>(
         L[0].u[L[0].cur], d_out, n0 * C);
     CK(cudaGetLastError());
@@ -978,6 +1003,7 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
     const auto t0 = Clock::now();
     if (pnm) {
       // read_pnm / read_mask_pbm (pnm.hpp:98-188) on device
+      ++ctx->launch_count;
       unpack_pnm_kernel<<<dim3((w + 255) / 256, std::min(h, 65535)), 256, 0, cs>>>(
           raw_in(s), raw_mask(s), w, h, c, ctx->slot_f[s].as<double>(),
           ctx->slot_mask[s].as<uint8_t>());
@@ -987,6 +1013,7 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
                o, nullptr, ctx->slot_out[s].as<double>(), rep, nullptr, nullptr, cs, t0);
     if (pnm) {
       // write_pnm's quantise (pnm.hpp:82-85, 130-147)
+      ++ctx->launch_count;
       quantise_kernel<<<grid_for(n_px, 256, 148 * 16), 256, 0, cs>>>(
           ctx->slot_out[s].as<double>(), n_px, c, raw_out(s));
       CK(cudaGetLastError());
@@ -1028,11 +1055,13 @@ int assign_device(Ctx& x, const uint8_t* d_mask, int W, int H) {
   int m = 0;
   {
     Timed t(x, K_VORONOI, static_cast<double>(n) * 13.0);
+    ++x.c.launch_count;
     site_flags_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, x.s>>>(d_mask, n, flag);
     CK(cudaGetLastError());
     cub_call(x, [&](void* tmp, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(tmp, b, flag, rank, ni, x.s);
     });
+    ++x.c.launch_count;
     sites_scatter_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, x.s>>>(d_mask, rank, n,
                                                                      z.sites.as<int32_t>());
     CK(cudaGetLastError());
@@ -1054,6 +1083,7 @@ int assign_device(Ctx& x, const uint8_t* d_mask, int W, int H) {
   {
     Timed t(x, K_VORONOI, static_cast<double>(m) * 24.0 + nb * 12.0);
     CK(cudaMemsetAsync(cursor, 0, (nb + 1) * 4, x.s));
+    ++x.c.launch_count;
     bucket_count_kernel<<<grid_for(m, 256, 148 * 8), 256, 0, x.s>>>(z.sites.as<int32_t>(), m, W,
                                                                     cell, gw, cursor);
     CK(cudaGetLastError());
@@ -1061,12 +1091,14 @@ int assign_device(Ctx& x, const uint8_t* d_mask, int W, int H) {
       return cub::DeviceScan::ExclusiveSum(tmp, b, cursor, start, static_cast<int>(nb + 1), x.s);
     });
     CK(cudaMemcpyAsync(cursor, start, nb * 4, cudaMemcpyDeviceToDevice, x.s));
+    ++x.c.launch_count;
     bucket_fill_kernel<<<grid_for(m, 256, 148 * 8), 256, 0, x.s>>>(
         z.sites.as<int32_t>(), m, W, cell, gw, cursor, z.members.as<int32_t>());
     CK(cudaGetLastError());
   }
   {
     Timed t(x, K_VORONOI, static_cast<double>(n) * 4.0);
+    ++x.c.launch_count;
     assign_sites_kernel<<<dim3((W + 31) / 32, (H + 7) / 8), 256, 0, x.s>>>(
         z.sites.as<int32_t>(), start, z.members.as<int32_t>(), W, H, cell, gw, gh,
         z.site_of.as<int32_t>());
@@ -1105,6 +1137,7 @@ long long densify_plant(Ctx& x, const uint8_t* mask_view, uint8_t* d_mask, const
     Timed t(x, K_VORONOI, static_cast<double>(n) * (C * 16.0 + 1 + 4 + 12));
     CK(cudaMemsetAsync(area, 0, (static_cast<size_t>(m) + 1) * 4, x.s));
     CK(cudaMemsetAsync(nonempty, 0, 4, x.s));
+    ++x.c.launch_count;
     cell_keys_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, x.s>>>(
         mask_view, z.site_of.as<int32_t>(), d_u, d_f, n, C, m, z.key.as<int32_t>(),
         z.pix.as<int32_t>(), z.err.as<double>(), area);
@@ -1123,6 +1156,7 @@ long long densify_plant(Ctx& x, const uint8_t* mask_view, uint8_t* d_mask, const
   }
   {
     Timed t(x, K_VORONOI, static_cast<double>(n) * 12.0 + m * 24.0);
+    ++x.c.launch_count;
     cell_reduce_kernel<<<grid_for(m, 128, 148 * 16), 128, 0, x.s>>>(
         z.seg.as<int32_t>(), z.pix2.as<int32_t>(), z.err.as<double>(), m,
         z.bits.as<unsigned long long>(), z.worst.as<int32_t>(), z.order.as<int32_t>(), nonempty);
@@ -1136,6 +1170,7 @@ long long densify_plant(Ctx& x, const uint8_t* mask_view, uint8_t* d_mask, const
                                                        z.order.as<int32_t>(),
                                                        z.order2.as<int32_t>(), m, 0, 32, x.s);
     });
+    ++x.c.launch_count;
     gather_bits_kernel<<<grid_for(m, 256, 148 * 8), 256, 0, x.s>>>(
         z.bits.as<unsigned long long>(), z.order2.as<int32_t>(), m,
         z.bits2.as<unsigned long long>());
@@ -1153,6 +1188,7 @@ long long densify_plant(Ctx& x, const uint8_t* mask_view, uint8_t* d_mask, const
   quota = std::min<long long>({quota, static_cast<long long>(used), remaining});
   if (quota > 0) {
     Timed t(x, K_VORONOI, static_cast<double>(quota) * 9.0);
+    ++x.c.launch_count;
     plant_kernel<<<grid_for(quota, 256, 148 * 8), 256, 0, x.s>>>(
         z.order.as<int32_t>(), z.worst.as<int32_t>(), static_cast<int>(quota), d_mask);
     CK(cudaGetLastError());
@@ -1708,6 +1744,7 @@ si_status si_local_operator_apply(si_ctx* ctx, const uint8_t* mask, int w, int h
     const double* d_v = upload(x, ctx->in_f, v, cells);
     ctx->out_img.ensure(cells * sizeof(double));
     const int bx = index % ax.count, by = index / ax.count;
+    ++x.c.launch_count;
     local_operator_kernel<<<grid_for(cells, 256, 1 << 20), 256, 0, x.s>>>(
         d_m, w, h, ax.anchor(bx), ay.anchor(by), B, flavour == SI_FLAVOUR_RAS, alpha - 1.0, d_v,
         ctx->out_img.as<double>());
@@ -1773,12 +1810,15 @@ si_status si_device_ingest(si_ctx* ctx, const double* d_f, const uint8_t* d_mask
     Ctx x{*ctx, pick_stream(ctx, stream)};
     begin_counters(x);
     const size_t n = static_cast<size_t>(w) * h;
-    if (precision == SI_PRECISION_FP32)
+    if (precision == SI_PRECISION_FP32) {
+      ++x.c.launch_count;
       ingest_kernel<float><<<grid_for(n, 256, 148 * 16), 256, 0, x.s>>>(
           d_f, d_mask, n, c, static_cast<float*>(d_b), ctx->counters.as<unsigned long long>() + 2);
-    else
+    } else {
+      ++x.c.launch_count;
       ingest_kernel<double><<<grid_for(n, 256, 148 * 16), 256, 0, x.s>>>(
           d_f, d_mask, n, c, static_cast<double*>(d_b), ctx->counters.as<unsigned long long>() + 2);
+    }
     CK(cudaGetLastError());
     publish_counters(x, 3);
     if (known) *known = static_cast<long long>(ctx->host_cnt[2]);
@@ -1930,6 +1970,7 @@ si_status si_selftest(si_ctx* ctx, int which, long long n, long long* failures) 
     set_device(ctx);
     Ctx x{*ctx, ctx->own_stream};
     begin_counters(x);
+    ++x.c.launch_count;
     selftest_division_kernel<<<148 * 8, 256, 0, x.s>>>(n, 0x5eedull,
                                                       ctx->counters.as<unsigned long long>());
     CK(cudaGetLastError());
