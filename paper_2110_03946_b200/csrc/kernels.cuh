@@ -197,6 +197,10 @@ __global__ void __launch_bounds__(kRedThreads)
 // Used when the row pitch is a multiple of 16 bytes (every level of an even
 // width in fp64); otherwise the cp.async kernel above runs.
 constexpr int kResTmaThreads = 128;
+#ifndef SI_RES_BAND
+#define SI_RES_BAND 16
+#endif
+constexpr int kResTmaBand = SI_RES_BAND;  // rows per CTA of the TMA variant
 // The box starts kLead = 16 / sizeof(T) columns left of the CTA's first
 // column (TMA wants 16-byte aligned inner box starts) and is 128 + 2 kLead
 // wide (a 16-byte multiple).
@@ -215,14 +219,14 @@ __global__ void __launch_bounds__(kResTmaThreads)
                               const uint8_t* __restrict__ mask, const T* __restrict__ b, int W,
                               int H, size_t N, int row0, int row1, double* partials, double* out,
                               unsigned int* ticket) {
-  __shared__ __align__(128) T tile[kResBand + 2][res_tma_box_w<T>()];
+  __shared__ __align__(128) T tile[kResTmaBand + 2][res_tma_box_w<T>()];
   __shared__ uint64_t bar;
   const int c = blockIdx.z;
   const T* __restrict__ bc = b + c * N;
   const int x0 = blockIdx.x * kResTmaThreads;
   const int x = x0 + threadIdx.x;
-  const int y0 = row0 + static_cast<int>(blockIdx.y) * kResBand;
-  const int ny = min(kResBand, row1 - y0);
+  const int y0 = row0 + static_cast<int>(blockIdx.y) * kResTmaBand;
+  const int ny = min(kResTmaBand, row1 - y0);
   const bool xin = x < W;
   const size_t Wz = static_cast<size_t>(W);
   if (threadIdx.x == 0) {
@@ -235,11 +239,11 @@ __global__ void __launch_bounds__(kResTmaThreads)
     mbar_expect_tx(&bar, sizeof(tile));
     tma_load_3d(&tile[0][0], &umap, x0 - res_tma_lead<T>(), y0 - 1, c, &bar);
   }
-  uint8_t mk[kResBand];
-  T bv[kResBand];
+  uint8_t mk[kResTmaBand];
+  T bv[kResTmaBand];
   const size_t base = xin ? static_cast<size_t>(y0) * Wz + x : 0;
 #pragma unroll
-  for (int k = 0; k < kResBand; ++k) {
+  for (int k = 0; k < kResTmaBand; ++k) {
     const bool in = xin && k < ny;
     const size_t i = in ? base + static_cast<size_t>(k) * Wz : 0;
     const uint8_t m = __ldg(mask + i);
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(kResTmaThreads)
   T up = tile[0][t], ctr = tile[1][t];
   double acc = 0.0;
 #pragma unroll
-  for (int k = 0; k < kResBand; ++k) {
+  for (int k = 0; k < kResTmaBand; ++k) {
     const int y = y0 + k;
     const T dn = tile[k + 2][t];
     const T sum = ((tile[k + 1][t - 1] + tile[k + 1][t + 1]) + up) + dn;

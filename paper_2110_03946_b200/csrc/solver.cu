@@ -270,8 +270,9 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
           static_cast<double>(W) * std::max(0, row1 - row0) * (C * sizeof(T) + (mode == 1 ? 0 : 1)));
   CUtensorMap map;
   if (mode != 1 && !tma_disabled() &&
-      make_plane_map(&map, u, W, H, C, sizeof(T), res_tma_box_w<T>(), kResBand + 2)) {
+      make_plane_map(&map, u, W, H, C, sizeof(T), res_tma_box_w<T>(), kResTmaBand + 2)) {
     const int tx = (W + kResTmaThreads - 1) / kResTmaThreads;
+    const int gy = (rows + kResTmaBand - 1) / kResTmaBand;
     x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(tx) * gy * C);
     if (known_invariant) {
       ++x.c.launch_count;
