@@ -137,7 +137,7 @@ struct si_ctx {
   std::vector<PendingEvent> pending;
   std::vector<cudaEvent_t> event_pool;
   si_kernel_stats stats{};
-  int sweep_nw64 = 4, sweep_nw32 = 4;           // warps per sweep CTA
+  int sweep_nw64 = 2, sweep_nw32 = 2;           // warps per sweep CTA (measured best)
   long long launch_count = 0;                   // kernels launched (always counted)
   int sweep_warp = 0;                           // 1: full blocks on the one-warp variant
   // batch pipeline: two staging slots, one stream per copy direction

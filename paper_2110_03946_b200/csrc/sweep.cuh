@@ -307,6 +307,12 @@ __device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, const T (*ut)
 #ifndef SI_OCC32
 #define SI_OCC32 6
 #endif
+#ifndef SI_OCC64_2
+#define SI_OCC64_2 6
+#endif
+#ifndef SI_OCC32_2
+#define SI_OCC32_2 8
+#endif
 #ifndef SI_OCC64_8
 #define SI_OCC64_8 3
 #endif
@@ -316,8 +322,8 @@ __device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, const T (*ut)
 template <typename T, int NW>
 struct SweepOcc {
   static constexpr int value =
-      sizeof(T) == 8 ? (NW == 8 ? SI_OCC64_8 : NW == 4 ? SI_OCC64 : (NW == 2 ? 3 : 1))
-                     : (NW == 8 ? SI_OCC32_8 : NW == 4 ? SI_OCC32 : (NW == 2 ? 4 : 2));
+      sizeof(T) == 8 ? (NW == 8 ? SI_OCC64_8 : NW == 4 ? SI_OCC64 : (NW == 2 ? SI_OCC64_2 : 1))
+                     : (NW == 8 ? SI_OCC32_8 : NW == 4 ? SI_OCC32 : (NW == 2 ? SI_OCC32_2 : 2));
 };
 
 // FULL: the block is exactly 32x32 (every level of any image >= 32 pixels
