@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
   if (any_unknown) {
 #pragma unroll
     for (int i = 0; i < R; ++i) p[i] = r[i];  // r = b - A*0 = b exactly
-    T nb_p[2] = {T(0), T(0)}, nb_r[2] = {T(0), T(0)}, nb_x[2] = {T(0), T(0)};
+    T nb_p[2] = {T(0), T(0)}, nb_r[2] = {T(0), T(0)};
 
     auto publish = [&]() {
       if (NW > 1) {
@@ -459,12 +459,10 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
         if (warp > 0) {
           nb_r[0] = S.pub[warp - 1][1][0][lane];
           nb_p[0] = S.pub[warp - 1][1][1][lane];
-          nb_x[0] = S.pub[warp - 1][1][2][lane];
         }
         if (warp + 1 < NW) {
           nb_r[1] = S.pub[warp + 1][0][0][lane];
           nb_p[1] = S.pub[warp + 1][0][1][lane];
-          nb_x[1] = S.pub[warp + 1][0][2][lane];
         }
       }
     };
@@ -555,7 +553,11 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
         if (cadence || maybe_done) {
           // True residual b - A x, then confirm or replace (cg.hpp:131-146).
           stage(x);
-          apply(x, nb_x[0], nb_x[1], q);
+          // the neighbours' boundary rows of x were published before the rr
+          // barrier of this iteration
+          const T nx0 = (NW > 1 && warp > 0) ? S.pub[warp - 1][1][2][lane] : T(0);
+          const T nx1 = (NW > 1 && warp + 1 < NW) ? S.pub[warp + 1][0][2][lane] : T(0);
+          apply(x, nx0, nx1, q);
 #pragma unroll
           for (int i = 0; i < R; ++i) q[i] = S.bt[c.row0 + i][lane] - q[i];
           const T part = dot2<T, R>(q, q);
