@@ -28,6 +28,8 @@
 // pixel is written exactly once and no CTA reads what another writes.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "tma.cuh"
 
@@ -221,12 +223,12 @@ __device__ __forceinline__ void stage_u_tile(T (*ut)[kTileW], const T* __restric
 // out-of-image neighbours are zeros of the tile, i.e. the reference's skipped
 // term (x + 0 == x), deg counts the in-image ones.  Branch-free, so the rows
 // overlap.  INV: the multilevel invariant (b never read).
+// Mask bits (and b where the invariant does not hold) of the rows
+// row0-1 .. row0+R at my column: every load issued at once, before the u tile
+// is waited for, so their latency overlaps the tile copy.
 template <typename T, int R, bool INV>
-__device__ __forceinline__ void residual_rows(const Cell<T, R>& c, const T (*ut)[kTileW],
-                                              T (&r)[R + 2], uint64_t& kbits) {
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void load_rows(const Cell<T, R>& c, uint64_t& kbits, T (&bv)[R + 2]) {
   const size_t W = static_cast<size_t>(c.W);
-  T bv[R + 2];
   kbits = 0;
 #pragma unroll
   for (int j = 0; j < R + 2; ++j) {
@@ -241,6 +243,13 @@ __device__ __forceinline__ void residual_rows(const Cell<T, R>& c, const T (*ut)
       bv[j] = in_blk ? bb : T(0);
     }
   }
+}
+
+template <typename T, int R, bool INV>
+__device__ __forceinline__ void residual_rows(const Cell<T, R>& c, const T (*ut)[kTileW],
+                                              T (&r)[R + 2], uint64_t kbits,
+                                              const T (&bv)[R + 2]) {
+  const int lane = threadIdx.x & 31;
   const int deg_x = (c.gx > 0) + (c.gx + 1 < c.W);
 #pragma unroll
   for (int j = 0; j < R + 2; ++j) {
@@ -261,16 +270,12 @@ __device__ __forceinline__ void residual_rows(const Cell<T, R>& c, const T (*ut)
 // Local right-hand side of my rows (solve_local_block, schwarz.hpp:219-230):
 //   rhs = unk * (pv + knw_W pv_W + knw_E pv_E + knw_N pv_N + knw_S pv_S),
 // knw counting only in-block neighbours (ghost ring = 0).  Returns unk bits.
-template <typename T, int R>
+template <typename T, int R, bool INV>
 __device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, const T (*ut)[kTileW],
-                                              T (&rhs)[R], uint64_t* kbits_out = nullptr) {
+                                              T (&rhs)[R], uint64_t kb, const T (&bv)[R + 2]) {
   const int lane = threadIdx.x & 31;
   T r[R + 2];
-  uint64_t kb;
-  if (c.known_invariant)
-    residual_rows<T, R, true>(c, ut, r, kb);
-  else
-    residual_rows<T, R, false>(c, ut, r, kb);
+  residual_rows<T, R, INV>(c, ut, r, kb, bv);
   const uint64_t kbW = __shfl_up_sync(0xffffffffu, kb, 1);
   const uint64_t kbE = __shfl_down_sync(0xffffffffu, kb, 1);
   uint32_t unk = 0;
@@ -286,7 +291,7 @@ __device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, const T (*ut)
     // neighbour terms vanish; otherwise add each known in-block neighbour's r
     // (+0 for the others: the reference's skipped term).
     T t = r[j];
-    if (!c.known_invariant) {
+    if (!INV) {
       t += (lane > 0 && ((kbW >> j) & 1ull)) ? rW : T(0);
       t += (lane + 1 < c.B && ((kbE >> j) & 1ull)) ? rE : T(0);
       t += (ly > 0 && ((kb >> (j - 1)) & 1ull)) ? r[j - 1] : T(0);
@@ -295,7 +300,6 @@ __device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, const T (*ut)
     t = unk_i ? t : T(0);
     rhs[i] = t;
   }
-  if (kbits_out) *kbits_out = kb;
   return unk;
 }
 
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
   long long pr_k1 = pr_k0, pr_k2 = pr_k0;
 #endif
 #ifdef SI_PROBE_SETUP
-  long long pr_s1 = 0, pr_s2 = 0;
+  long long pr_s0 = 0, pr_s1 = 0, pr_s2 = 0;
 #endif
 
   const int bx = blockIdx.x % a.ax.count;
@@ -366,30 +370,41 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
 
   T x[R], r[R], p[R], q[R];
   uint32_t unk;
-  if (a.use_tma) {
-    // one TMA box: rows y0-2 .. y0+33, columns x0-2 .. x0+33 of this channel,
-    // zeros outside the image
-    if (tid == 0) {
-      mbar_init(&S.bar, 1);
-      mbar_expect_tx(&S.bar, sizeof(S.ut));
-      tma_load_3d(&S.ut[0][0], &a.umap, c.x0 - 2, c.y0 - 2, ch, &S.bar);
+  // u tile (TMA box or cooperative copy) and the mask bits of my rows, the
+  // latter in flight while the tile arrives; then residual and right-hand side
+  auto setup = [&](auto inv_tag) {
+    constexpr bool INV = decltype(inv_tag)::value;
+    uint64_t kb;
+    T bv[R + 2];
+    if (a.use_tma) {
+      // one TMA box: rows y0-2 .. y0+33, columns x0-2 .. x0+33 of this
+      // channel, zeros outside the image
+      if (tid == 0) {
+        mbar_init(&S.bar, 1);
+        mbar_expect_tx(&S.bar, sizeof(S.ut));
+        tma_load_3d(&S.ut[0][0], &a.umap, c.x0 - 2, c.y0 - 2, ch, &S.bar);
+      }
+      load_rows<T, R, INV>(c, kb, bv);
+      __syncthreads();
+      mbar_wait(&S.bar, 0);
+    } else {
+      load_rows<T, R, INV>(c, kb, bv);
+      stage_u_tile<T, NW>(S.ut, c.u, c.x0, c.y0, B, c.W, c.H);
+      __syncthreads();
     }
-    __syncthreads();
-    mbar_wait(&S.bar, 0);
-  } else {
-    stage_u_tile<T, NW>(S.ut, c.u, c.x0, c.y0, B, c.W, c.H);
-    __syncthreads();
-  }
 #ifdef SI_PROBE_SETUP
-  const long long pr_s0 = clock64();
+    pr_s0 = clock64();
 #endif
-  {
-    unk = local_rhs<T, R>(c, S.ut, r);
+    unk = local_rhs<T, R, INV>(c, S.ut, r, kb, bv);
 #ifdef SI_PROBE_SETUP
     if (unk == 0xdeadbeefu) a.u_new[0] = r[0];  // forces r complete before the stamp
     pr_s1 = clock64();
 #endif
-  }
+  };
+  if (a.known_invariant)
+    setup(std::true_type{});
+  else
+    setup(std::false_type{});
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     x[i] = T(0);
