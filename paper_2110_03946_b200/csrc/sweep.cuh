@@ -6,23 +6,26 @@
 //   solve_local_block + cg_solve (schwarz.hpp:202-250, cg.hpp:90-154),
 //   accumulate_owned (partition.hpp:148-156).
 //
-// One CTA = one (subdomain, channel), NW warps.  Layout: lane = block column,
-// warp w owns rows [w*R, (w+1)*R), R = 32/NW, so every CG vector lives in
-// registers (R values per thread per vector):
-//   * horizontal stencil neighbours come from __shfl_up/down, vertical ones
-//     from the thread's own registers;
-//   * the rows at warp boundaries are exchanged through shared memory with no
-//     dedicated barrier: before each reduction barrier every warp publishes
-//     the *components* of its boundary rows (r, old p, x) and its neighbours
-//     rebuild p_new = r + beta*p with the identical fma afterwards.  One CG
-//     iteration costs 2 CTA barriers (3 on a true-residual check);
-//   * dot products: warp butterfly + fixed-order cross-warp sum, so every
-//     thread holds the same value and all control flow is CTA-uniform.
-// Nothing is staged in shared memory besides those boundary rows: the
-// residual slice and the local right-hand side are rebuilt from global memory
-// (u_old, mask, b are read-only during the sweep) whenever they are needed —
-// at setup, at the rare true-residual checks and at write-back — which keeps
-// shared memory at ~4 KB per CTA and occupancy register-bound.
+// One CTA = one (subdomain, channel), NW warps (2 by default, chosen by
+// measurement).  Layout: lane = block column, warp w owns rows
+// [w*R, (w+1)*R), R = 32/NW, so every CG vector lives in registers (R values
+// per thread per vector):
+//   * setup: the block's u_old with a 2-pixel halo arrives in shared memory by
+//     one TMA box copy (zero fill outside the image) where the box start is
+//     16-byte aligned, else by one cooperative all-loads-first pass; the mask
+//     bits of the thread's rows are loaded while the tile is in flight; the
+//     residual slice and the local right-hand side are then evaluated
+//     branch-free from the tile;
+//   * stencil: W/E neighbours from a per-warp staged row buffer in shared
+//     memory (warp-local __syncwarp only), N/S from the thread's registers;
+//   * rows at warp boundaries are exchanged with no dedicated barrier: before
+//     each reduction barrier every warp publishes the *components* of its
+//     boundary rows (r, old p, x) and its neighbours rebuild p_new = r + beta*p
+//     with the identical fma afterwards.  One CG iteration costs 2 CTA
+//     barriers (3 on a true-residual check);
+//   * dot products: 4-accumulator tree per thread, warp total on the FP64
+//     tensor core (DMMA), pairwise tree over the warps, so every thread holds
+//     the same value and all control flow is CTA-uniform.
 // u_new = u_old + v is written only on the block's owned rectangle into a
 // separate buffer (ping-pong): owned rectangles tile the image, so every
 // pixel is written exactly once and no CTA reads what another writes.
