@@ -384,14 +384,11 @@ void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_
   a.counters = counters;
   if (by1 < 0) by1 = a.ay.count;
   a.by0 = by0;
-  // TMA tile loads need 16-byte aligned box starts x0 - 2, i.e. even block
-  // anchors (k * stride, and W - B for the last) in fp64; fp32 would need
-  // x0 = 2 mod 4, which anchor 0 never is, so fp32 stages cooperatively.
-  {
-    const bool anchors_ok = a.ax.count == 1 || (a.ax.stride % 2 == 0 && (W - a.ax.block) % 2 == 0);
-    a.use_tma = sizeof(T) == 8 && anchors_ok && !tma_disabled() &&
-                make_plane_map(&a.umap, u_old, W, H, C, sizeof(T), kTileW, kTileH);
-  }
+  // TMA tile loads: the box starts at the 16-byte aligned column left of each
+  // block (tile_lead), so any anchor works; the row pitch must be a multiple
+  // of 16 bytes (checked by make_plane_map)
+  a.use_tma = !tma_disabled() &&
+              make_plane_map(&a.umap, u_old, W, H, C, sizeof(T), tile_w<T>(), kTileH);
   const int nblocks = a.ax.count * (by1 - by0);
   if (nblocks <= 0) return;
   const double bytes = static_cast<double>(a.N) * (2.0 * C * sizeof(T) + 1.0) * (by1 - by0) /

@@ -39,14 +39,25 @@
 namespace sib {
 
 // u_old tile of a block: rows y0-2 .. y0+B+1, columns x0-1 .. x0+B.
-// Column j of the tile is x = x0 - 2 + j (a 16-byte aligned start for the
-// TMA box when x0 is even), so the block's columns are j = 2 .. B+1 and the
-// ring columns j = 1 and j = B+2.
-constexpr int kTileW = kMaxBlock + 4, kTileH = kMaxBlock + 4;
+// Column j of the tile is x = x0 - lead + j: the block's columns are
+// j = lead .. lead+B-1, the ring columns lead-1 and lead+B.  The cooperative
+// copy uses lead 2; the TMA box starts at the 16-byte aligned column
+// x0 - lead with lead = ((x0 - 1) mod q) + 1, q = 16 / sizeof(T), so the
+// tile is 32 + q + 2 columns rounded to a 16-byte row (fp64 36, fp32 40).
+constexpr int kTileH = kMaxBlock + 4;
+template <typename T>
+__host__ __device__ constexpr int tile_w() {
+  return sizeof(T) == 8 ? kMaxBlock + 4 : kMaxBlock + 8;
+}
+template <typename T>
+__host__ __device__ inline int tile_lead(int x0) {
+  constexpr int q = 16 / static_cast<int>(sizeof(T));
+  return ((x0 - 1) % q + q) % q + 1;
+}
 
 template <typename T>
 struct SweepArgs {
-  CUtensorMap umap;    // TMA map of u_old ([C][H][W], box kTileW x kTileH) when use_tma
+  CUtensorMap umap;    // TMA map of u_old ([C][H][W], box tile_w x kTileH) when use_tma
   int use_tma;
   const uint8_t* mask;
   const T* b;
@@ -86,7 +97,7 @@ __device__ __forceinline__ T robin_diag(int gx, int gy, int lx, int ly, int B, i
 
 template <typename T, int NW>
 struct SweepSmem {
-  __align__(128) T ut[kTileH][kTileW];  // u_old tile with halo (TMA destination)
+  __align__(128) T ut[kTileH][tile_w<T>()];  // u_old tile with halo (TMA destination)
   uint64_t bar;                    // TMA completion
   T pt[kMaxBlock][kMaxBlock + 2];  // stencil operand rows, zero ghost columns 0 and B+1
   T bt[kMaxBlock][kMaxBlock];      // local right-hand side (true-residual checks)
@@ -174,6 +185,7 @@ __device__ __noinline__ bool band_sqrt_le(T v, T thr) {
 template <typename T, int R>
 struct Cell {
   int lx, gx, row0, x0, y0, B, W, H;
+  int tl;  // tile column of pixel x0 (see tile_lead)
   bool col_ok;
   const uint8_t* __restrict__ mask;
   const T* __restrict__ u;
@@ -186,7 +198,7 @@ struct Cell {
 // the whole CTA (consecutive threads -> consecutive columns of a row: 272-byte
 // coalesced row segments, every load independent and issued up front).
 template <typename T, int NW>
-__device__ __forceinline__ void stage_u_tile(T (*ut)[kTileW], const T* __restrict__ u, int x0,
+__device__ __forceinline__ void stage_u_tile(T (*ut)[tile_w<T>()], const T* __restrict__ u, int x0,
                                              int y0, int B, int W, int H) {
   // Warp w stages tile rows w, w+NW, ...: lanes 0..B load columns x0..x0+B
   // (one coalesced row segment), lanes 30/31 the ring columns x0-1 and x0+32.
@@ -249,7 +261,7 @@ __device__ __forceinline__ void load_rows(const Cell<T, R>& c, uint64_t& kbits, 
 }
 
 template <typename T, int R, bool INV>
-__device__ __forceinline__ void residual_rows(const Cell<T, R>& c, const T (*ut)[kTileW],
+__device__ __forceinline__ void residual_rows(const Cell<T, R>& c, const T (*ut)[tile_w<T>()],
                                               T (&r)[R + 2], uint64_t kbits,
                                               const T (&bv)[R + 2]) {
   const int lane = threadIdx.x & 31;
@@ -259,8 +271,9 @@ __device__ __forceinline__ void residual_rows(const Cell<T, R>& c, const T (*ut)
     const int ly = c.row0 - 1 + j;
     const int gy = c.y0 + ly;
     const int tr = ly + 2;
-    const T uc = ut[tr][lane + 2];
-    const T sum = ((ut[tr][lane + 1] + ut[tr][lane + 3]) + ut[tr - 1][lane + 2]) + ut[tr + 1][lane + 2];
+    const int tc = lane + c.tl;
+    const T uc = ut[tr][tc];
+    const T sum = ((ut[tr][tc - 1] + ut[tr][tc + 1]) + ut[tr - 1][tc]) + ut[tr + 1][tc];
     const int deg = deg_x + (gy > 0) + (gy + 1 < c.H);
     const T bj = INV ? T(0) : bv[j];
     const T ru = bj - fmaT(T(deg), uc, -sum);
@@ -274,7 +287,7 @@ __device__ __forceinline__ void residual_rows(const Cell<T, R>& c, const T (*ut)
 //   rhs = unk * (pv + knw_W pv_W + knw_E pv_E + knw_N pv_N + knw_S pv_S),
 // knw counting only in-block neighbours (ghost ring = 0).  Returns unk bits.
 template <typename T, int R, bool INV>
-__device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, const T (*ut)[kTileW],
+__device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, const T (*ut)[tile_w<T>()],
                                               T (&rhs)[R], uint64_t kb, const T (&bv)[R + 2]) {
   const int lane = threadIdx.x & 31;
   T r[R + 2];
@@ -370,6 +383,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
   c.u = a.u_old + plane;
   c.b = a.b + plane;
   c.known_invariant = a.known_invariant;
+  c.tl = a.use_tma ? tile_lead<T>(c.x0) : 2;
 
   T x[R], r[R], p[R], q[R];
   uint32_t unk;
@@ -385,7 +399,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
       if (tid == 0) {
         mbar_init(&S.bar, 1);
         mbar_expect_tx(&S.bar, sizeof(S.ut));
-        tma_load_3d(&S.ut[0][0], &a.umap, c.x0 - 2, c.y0 - 2, ch, &S.bar);
+        tma_load_3d(&S.ut[0][0], &a.umap, c.x0 - c.tl, c.y0 - 2, ch, &S.bar);
       }
       load_rows<T, R, INV>(c, kb, bv);
       __syncthreads();
@@ -632,7 +646,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
     const int gy = c.y0 + ly;
     const bool own = col_own && ly < B && gy >= oy0 && gy < oy1;
     const size_t pix = own ? static_cast<size_t>(gy) * c.W + c.gx : 0;
-    const T uo = S.ut[ly + 2][lane + 2];
+    const T uo = S.ut[ly + 2][lane + c.tl];
     T v = x[i];
     if (!c.known_invariant) {
       const T bk = c.b[pix];

@@ -374,10 +374,12 @@ def test_pnm_batch_matches_decoded_pipeline(solver, oracle, w, h, c):
         assert diff.max() <= 1 and np.count_nonzero(diff) <= max(1, diff.size // 10000)
 
 
-def test_tma_and_cooperative_staging_agree_bitwise(tmp_path):
-    """The sweep and residual kernels stage tiles by TMA where the box start is
-    16-byte aligned and cooperatively otherwise (SI_NO_TMA=1 forces the
-    latter): same arithmetic, so bit-identical results."""
+@pytest.mark.parametrize("precision,overlap", [(0, 6), (1, 6), (0, 5), (1, 3)])
+def test_tma_and_cooperative_staging_agree_bitwise(tmp_path, precision, overlap):
+    """The sweep and residual kernels stage tiles by TMA (box start aligned
+    down to 16 bytes left of each block, any anchor) and cooperatively
+    otherwise (SI_NO_TMA=1 forces the latter): same arithmetic, so
+    bit-identical results, fp64 and fp32, even and odd block strides."""
     import subprocess
     import sys
     code = (
@@ -385,10 +387,11 @@ def test_tma_and_cooperative_staging_agree_bitwise(tmp_path):
         "import paper_2110_03946_b200 as si\n"
         "from instances import random_instance\n"
         "f, m = random_instance(640, 480, 0.04, 3, 5)\n"
-        "r = si.Solver(0).run_method(si.Method.MultilevelOras, f, m, si.RunOptions())\n"
+        "o = si.RunOptions(overlap=%d, precision=si.Precision(%d))\n"
+        "r = si.Solver(0).run_method(si.Method.MultilevelOras, f, m, o)\n"
         "np.save(sys.argv[1], r.image.data)\n"
     ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-         os.path.dirname(os.path.abspath(__file__)))
+         os.path.dirname(os.path.abspath(__file__)), overlap, precision)
     outs = []
     for k, env_extra in enumerate(({}, {"SI_NO_TMA": "1"})):
         path = str(tmp_path / f"u{k}.npy")
