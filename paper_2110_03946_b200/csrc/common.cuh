@@ -7,7 +7,6 @@
 namespace sib {
 
 constexpr int kMaxBlock = 32;   // subdomain edge handled by the sweep kernel
-constexpr int kTile = kMaxBlock + 2;
 
 // Partition of one axis, computed arithmetically so no per-block tables are
 // needed on device.  partition_axis / owned_end (partition.hpp:46-63):

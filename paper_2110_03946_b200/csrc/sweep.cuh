@@ -126,9 +126,6 @@ template <typename T, int NW>
 __device__ __forceinline__ T cta_sum(T v, T (*red)[NW], int slot, int warp, int lane) {
   v = warp_total(v);
   if (NW == 1) return v;
-#ifdef SI_ABL_NORED
-  return v;
-#endif
   if (lane == 0) red[slot][warp] = v;
   __syncthreads();
   T t[NW];
@@ -524,11 +521,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
         // d*v - (vW + vE) - (vN + vS): dependent depth 3 (the reference's
         // left-to-right chain is 4; the values agree to rounding)
         const T t = fmaT(d, v[i], -(vW + vE)) - (vN + vS);
-#ifdef SI_ABL_NOMASK
-        o[i] = t;
-#else
         o[i] = ((unk >> i) & 1u) ? t : T(0);
-#endif
       }
     };
 
@@ -557,18 +550,12 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
       for (int iter = 1; iter <= a.lmax; ++iter) {
         apply(p, nb_p[0], nb_p[1], q);
         const T pAp = cta_sum<T, NW>(dot2<T, R>(p, q), S.red, 0, warp, lane);
-#ifndef SI_ABL_NOBREAK
         if (!(pAp > T(0)) || !isfinite(pAp)) {  // breakdown (cg.hpp:120-125)
           iters = iter - 1;
           break;
         }
-#endif
         SI_PROBE_MARK(0);
-#ifdef SI_ABL_NODIV
-        const T alpha = rr * T(0.5);
-#else
         const T alpha = rr / pAp;
-#endif
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           x[i] = fmaT(alpha, p[i], x[i]);
@@ -612,11 +599,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
           }
           rr_new = tt;
         }
-#ifdef SI_ABL_NODIV
-        const T beta = rr_new * T(0.25);
-#else
         const T beta = div_by_recip(rr_new, rr, rr_rcp);  // == rr_new / rr
-#endif
 #pragma unroll
         for (int i = 0; i < R; ++i) p[i] = fmaT(beta, p[i], r[i]);
         stage(p);
