@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 #include <functional>
+#include <memory>
 
 #include "../../include/schwarz_b200.h"
 #include "common.cuh"
@@ -28,6 +29,7 @@
 #include "sweep_warp.cuh"
 #include "cg_level.cuh"
 #include "densify.cuh"
+#include "host_copy.h"
 
 #include <cub/cub.cuh>
 
@@ -144,6 +146,7 @@ struct si_ctx {
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   DevBuf slot_f[2], slot_mask[2], slot_out[2];
   VoronoiBufs vz;                               // densification
+  std::unique_ptr<sib::Stager> stager;          // pageable host <-> device copies
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_solved[2] = {nullptr, nullptr},
               ev_d2h[2] = {nullptr, nullptr};
 };
@@ -204,6 +207,21 @@ void resolve_events(si_ctx& c) {
 
 void sync(Ctx& x) {
   CK(cudaStreamSynchronize(x.s));
+  if (!x.c.pending.empty()) resolve_events(x.c);
+}
+
+// Caller host buffers (pageable or pinned) <-> device, see host_copy.h.
+sib::Stager& stager(si_ctx& c) {
+  if (!c.stager)
+    c.stager = std::make_unique<sib::Stager>([](cudaError_t e, const char* what) {
+      cuda_check(e, what);
+    });
+  return *c.stager;
+}
+void h2d(Ctx& x, void* dst, const void* src, size_t n) { stager(x.c).h2d(dst, src, n, x.s); }
+// returns with the data in dst (everything queued on x.s before has finished)
+void d2h(Ctx& x, void* dst, const void* src, size_t n) {
+  stager(x.c).d2h(dst, src, n, x.s);
   if (!x.c.pending.empty()) resolve_events(x.c);
 }
 
@@ -1225,8 +1243,8 @@ void voronoi_densify(si_ctx* ctx, const double* f, int w, int h, int c, double t
   z.f.ensure(n * c * 8);
   z.mask.ensure(n);
   z.u.ensure(n * c * 8);
-  CK(cudaMemcpyAsync(z.f.ptr, f, n * c * 8, cudaMemcpyHostToDevice, x.s));
-  CK(cudaMemcpyAsync(z.mask.ptr, seed_mask.data(), n, cudaMemcpyHostToDevice, x.s));
+  h2d(x, z.f.ptr, f, n * c * 8);
+  h2d(x, z.mask.ptr, seed_mask.data(), n);
   int sw = 0;
   while (known < target_k && sw < d.max_sweeps) {
     si_report rep;
@@ -1238,8 +1256,7 @@ void voronoi_densify(si_ctx* ctx, const double* f, int w, int h, int c, double t
                            z.f.as<double>(), w, h, c, m, d.cell_fraction, target_k - known);
     ++sw;
   }
-  CK(cudaMemcpyAsync(mask_out, z.mask.ptr, n, cudaMemcpyDeviceToHost, x.s));
-  sync(x);
+  d2h(x, mask_out, z.mask.ptr, n);
   *sweeps = sw;
   *reached = known >= target_k;
 }
@@ -1341,6 +1358,7 @@ void si_destroy(si_ctx* c) {
                     &c->cg_r, &c->cg_p, &c->cg_q})
     b->release();
   c->vz.release();
+  c->stager.reset();
   for (auto& p : c->pending) {
     cudaEventDestroy(p.start);
     cudaEventDestroy(p.stop);
@@ -1415,19 +1433,17 @@ si_status si_run_method(si_ctx* ctx, int method, const double* f, const uint8_t*
     ctx->in_f.ensure(n * c * sizeof(double));
     ctx->in_mask.ensure(n);
     ctx->out_img.ensure(n * c * sizeof(double));
-    CK(cudaMemcpyAsync(ctx->in_f.ptr, f, n * c * sizeof(double), cudaMemcpyHostToDevice, x.s));
-    CK(cudaMemcpyAsync(ctx->in_mask.ptr, mask, n, cudaMemcpyHostToDevice, x.s));
+    h2d(x, ctx->in_f.ptr, f, n * c * sizeof(double));
+    h2d(x, ctx->in_mask.ptr, mask, n);
     const double* d_ref = nullptr;
     if (reference) {
       ctx->in_ref.ensure(n * c * sizeof(double));
-      CK(cudaMemcpyAsync(ctx->in_ref.ptr, reference, n * c * sizeof(double),
-                         cudaMemcpyHostToDevice, x.s));
+      h2d(x, ctx->in_ref.ptr, reference, n * c * sizeof(double));
       d_ref = ctx->in_ref.as<double>();
     }
     run_device(ctx, method, ctx->in_f.as<double>(), ctx->in_mask.as<uint8_t>(), w, h, c, o, d_ref,
                ctx->out_img.as<double>(), rep, trace, user, x.s, t0);
-    CK(cudaMemcpyAsync(out, ctx->out_img.ptr, n * c * sizeof(double), cudaMemcpyDeviceToHost, x.s));
-    sync(x);
+    d2h(x, out, ctx->out_img.ptr, n * c * sizeof(double));
   });
   rep->elapsed_ms = ms_since(t0);
   return st;
@@ -1512,14 +1528,13 @@ __global__ void local_operator_kernel(const uint8_t* mask, int W, int H, int x0,
 template <typename T>
 T* upload(Ctx& x, DevBuf& buf, const T* host, size_t count) {
   buf.ensure(count * sizeof(T) + 16);
-  CK(cudaMemcpyAsync(buf.ptr, host, count * sizeof(T), cudaMemcpyHostToDevice, x.s));
+  h2d(x, buf.ptr, host, count * sizeof(T));
   return buf.as<T>();
 }
 
 template <typename T>
 void download(Ctx& x, T* host, const void* dev, size_t count) {
-  CK(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, x.s));
-  sync(x);
+  d2h(x, host, dev, count * sizeof(T));
 }
 
 si_options opts_or_default(const si_options* opt) {
