@@ -239,6 +239,60 @@ inline InpaintingMask random_mask(int w, int h, double density, uint64_t seed) {
   return m;
 }
 
+// VoronoiAssignment / assign_nearest_site (masks.hpp:45-139).
+struct VoronoiAssignment {
+  std::vector<std::int32_t> sites;    // known pixel indices, ascending
+  std::vector<std::int32_t> site_of;  // pixel -> index into sites
+};
+
+inline VoronoiAssignment assign_nearest_site(const InpaintingMask& mask,
+                                             Context& ctx = Context::thread_default()) {
+  VoronoiAssignment a;
+  const size_t n = static_cast<size_t>(mask.width) * mask.height;
+  a.sites.resize(n);
+  a.site_of.resize(n);
+  int m = 0;
+  detail::throw_status(si_assign_nearest_site(ctx.get(), mask.known.data(), mask.width,
+                                              mask.height, a.sites.data(), a.site_of.data(), &m));
+  a.sites.resize(static_cast<size_t>(m));
+  return a;
+}
+
+// DensifyOptions / DensifyResult / voronoi_densify (masks.hpp:145-212).
+struct DensifyOptions {
+  double initial_density = 0.0;   // <= 0: start at a quarter of the target
+  double cell_fraction = 0.20;    // share of cells refined per sweep
+  double inner_tolerance = 1e-3;  // tolerance of the guiding inpainting runs
+  int max_sweeps = 100;
+  RunOptions solve;               // guide solver (multilevel ORAS); tolerance := inner_tolerance
+};
+
+struct DensifyResult {
+  InpaintingMask mask;
+  int sweeps = 0;
+  bool reached_target = false;
+};
+
+inline DensifyResult voronoi_densify(const ImageBuffer& f, double target_density, uint64_t seed,
+                                     const DensifyOptions& options = {},
+                                     Context& ctx = Context::thread_default()) {
+  si_densify_options d;
+  si_default_densify_options(&d);
+  d.initial_density = options.initial_density;
+  d.cell_fraction = options.cell_fraction;
+  d.inner_tolerance = options.inner_tolerance;
+  d.max_sweeps = options.max_sweeps;
+  d.solve = options.solve.to_c();
+  DensifyResult r;
+  r.mask = InpaintingMask(f.width, f.height);
+  int reached = 0;
+  detail::throw_status(si_voronoi_densify(ctx.get(), f.data.data(), f.width, f.height, f.channels,
+                                          target_density, seed, &d, r.mask.known.data(),
+                                          &r.sweeps, &reached));
+  r.reached_target = reached != 0;
+  return r;
+}
+
 inline double psnr(const ImageBuffer& u, const ImageBuffer& f) {
   detail::check_arg(u.width == f.width && u.height == f.height && u.channels == f.channels,
                     "mse_per_channel: image dimensions differ");

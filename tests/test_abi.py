@@ -176,7 +176,12 @@ def test_cpp_wrapper_header_compiles(tmp_path):
                    'int main(){ namespace sb = schwarz_b200;\n'
                    '  auto f = sb::synthetic_test_image(16, 16, 1, 1);\n'
                    '  auto m = sb::random_mask(16, 16, 0.2, 2);\n'
-                   '  sb::RunOptions o; (void)o; (void)f; (void)m; return 0; }\n')
+                   '  sb::RunOptions o; (void)o; (void)f; (void)m;\n'
+                   '  sb::DensifyOptions d; (void)d;\n'
+                   '  auto (*dens)(const sb::ImageBuffer&, double, uint64_t, const sb::DensifyOptions&,\n'
+                   '              sb::Context&) = &sb::voronoi_densify; (void)dens;\n'
+                   '  auto (*asg)(const sb::InpaintingMask&, sb::Context&) = &sb::assign_nearest_site;\n'
+                   '  (void)asg; return 0; }\n')
     out = subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src),
                           L.lib_path(), "-o", str(tmp_path / "t"),
                           f"-Wl,-rpath,{os.path.dirname(L.lib_path())}"],

@@ -401,3 +401,46 @@ def test_tma_and_cooperative_staging_agree_bitwise(tmp_path, precision, overlap)
         assert run.returncode == 0, run.stderr
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_cpp_dropin_header_on_device(tmp_path, solver):
+    """include/schwarz_b200.hpp used the way a reference caller would
+    (run_method, voronoi_densify) gives the Python/C-ABI results."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "t.cpp"
+    src.write_text(
+        '#include <cstdio>\n#include "schwarz_b200.hpp"\n'
+        'int main() { namespace sb = schwarz_b200;\n'
+        '  auto f = sb::synthetic_test_image(256, 256, 1, 7);\n'
+        '  auto m = sb::random_mask(256, 256, 0.05, 11);\n'
+        '  sb::RunOptions o; o.levels = 2;\n'
+        '  auto r = sb::run_method(sb::Method::MultilevelOras, f, m, o);\n'
+        '  double s = 0; for (double v : r.image.data) s += v;\n'
+        '  std::printf("%d %d %.17g\\n", r.report.level_iterations[0], r.report.level_iterations[1], s);\n'
+        '  auto g = sb::synthetic_test_image(64, 64, 1, 3);\n'
+        '  sb::DensifyOptions d; d.max_sweeps = 50;\n'
+        '  auto res = sb::voronoi_densify(g, 0.08, 17, d);\n'
+        '  size_t k = 0; for (auto b : res.mask.known) k += b != 0;\n'
+        '  std::printf("%d %d %zu\\n", res.sweeps, (int)res.reached_target, k);\n'
+        '  return 0; }\n')
+    lib_dir = os.path.join(root, "paper_2110_03946_b200")
+    exe = str(tmp_path / "t")
+    cc = subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(root, "include"), str(src),
+                         os.path.join(lib_dir, "libschwarz_b200.so"), f"-Wl,-rpath,{lib_dir}",
+                         "-o", exe], capture_output=True, text=True)
+    assert cc.returncode == 0, cc.stderr
+    run = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert run.returncode == 0, run.stderr
+    l1, l2 = run.stdout.strip().splitlines()
+    it0, it1, checksum = l1.split()
+    f = si.synthetic_test_image(256, 256, 1, 7)
+    m = si.random_mask(256, 256, 0.05, 11)
+    ref = solver.run_method(si.Method.MultilevelOras, f, m, si.RunOptions(levels=2))
+    assert [int(it0), int(it1)] == ref.report.level_iterations
+    assert float(checksum) == pytest.approx(float(ref.image.data.sum()), rel=1e-12)
+    sweeps, reached, known = (int(v) for v in l2.split())
+    dens = solver.voronoi_densify(si.synthetic_test_image(64, 64, 1, 3), 0.08, 17,
+                                  si.DensifyOptions(max_sweeps=50))
+    assert (sweeps, bool(reached), known) == (dens.sweeps, dens.reached_target,
+                                              dens.mask.known_count())
