@@ -334,12 +334,13 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     achieved = (sw["algorithmic_bytes"] / (sw["device_ms"] / 1e3) / 1e9) if sw["device_ms"] else 0.0
-    traffic, traffic_alg = None, None
+    traffic, traffic_alg, fp64_pct = None, None, None
     tfile = os.path.join(ROOT, "profiles", "sweep_dram_traffic.json")
     if os.path.exists(tfile):  # one ncu --set full capture (scripts/summarize_profiles.py)
         try:
             tj = json.load(open(tfile))
             traffic, traffic_alg = tj.get("dram_bytes_per_launch"), tj.get("algorithmic_bytes_per_launch")
+            fp64_pct = tj.get("fp64_pipe_pct_of_peak")
         except ValueError:
             pass
     total_dev = sum(v["device_ms"] for k, v in stats.items() if isinstance(v, dict))
@@ -361,7 +362,9 @@ def main():
                      "traffic_launch": "finest-level sweep, ncu dram__bytes_read+write",
                      "traffic_algorithmic": traffic_alg,
                      "frame_hbm_frac": (frame_bytes / prof_steps) / (ms_per_step / 1e3) / 1e9 / peak,
-                     "sweep_share_of_step": sw["device_ms"] / max(total_dev, 1e-9)},
+                     "sweep_share_of_step": sw["device_ms"] / max(total_dev, 1e-9),
+                     "onchip_bound": {"pipe": "fp64", "pct_of_peak": fp64_pct,
+                                      "source": "ncu --set full, first finest-level sweep"}},
         "e2e": {"value": e2e_value, "unit": "frames/s",
                 "h2d_bytes_per_step": int(C4K * n * 8 + n),
                 "d2h_bytes_per_step": int(C4K * n * 8),

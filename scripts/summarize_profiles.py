@@ -112,6 +112,15 @@ def main(tag):
         txt += ["", "warp stall reasons (cycles per issued instruction):"]
         txt += [f"  {k:30s} {v:6.2f}" for v, k in stalls]
         open(os.path.join(OUT, f"{tag}_sweep_ncu.txt"), "w").write("\n".join(txt) + "\n")
+        # the on-chip bound of the sweep, next to its DRAM traffic (bench.py)
+        tp = os.path.join(OUT, "sweep_dram_traffic.json")
+        if os.path.exists(tp):
+            tj = json.load(open(tp))
+            fp64 = [v for k, v in pipes.items() if k.startswith("sm__pipe_fp64_cycles_active")]
+            if fp64:
+                tj["fp64_pipe_pct_of_peak"] = fp64[0]
+            tj["ncu_full_capture"] = f"profiles/{tag}_sweep_ncu.txt"
+            json.dump(tj, open(tp, "w"), indent=1)
     bench = []
     for name in ("bench.json", "bench_fp32.json"):
         p = os.path.join(RAW, name)
