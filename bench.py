@@ -40,7 +40,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
+    p.add_argument("--precision", default="fp64", choices=["fp64", "fp32", "mixed"])
     p.add_argument("--frames", type=int, default=2, help="distinct frames per rank")
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -207,7 +207,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    prec = si.Precision.FP64 if args.precision == "fp64" else si.Precision.FP32
+    prec = {"fp64": si.Precision.FP64, "fp32": si.Precision.FP32,
+            "mixed": si.Precision.MIXED}[args.precision]
     opts = si.RunOptions(levels=LEVELS, precision=prec)
     solver = si.Solver(local)
     stream = torch.cuda.current_stream()
@@ -350,7 +351,8 @@ def main():
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64" if prec == si.Precision.FP64 else "f32", "data": "synthetic",
+        "dtype": {si.Precision.FP64: "f64", si.Precision.FP32: "f32",
+                  si.Precision.MIXED: "f64 (local CG f32)"}[prec], "data": "synthetic",
         "config": {"workload": "3840x2160 RGB, 4% random mask, 3-level ORAS, tol 1e-3 "
                                "(BASELINE configs[2]); per rank independent frames (configs[3])",
                    "block": 32, "overlap": 6, "alpha": 0.25, "levels": LEVELS,

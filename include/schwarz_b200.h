@@ -54,7 +54,14 @@ typedef enum {
 typedef enum { SI_AVERAGING_KNOWN_ONLY = 0, SI_AVERAGING_ALL_PIXELS = 1 } si_averaging;    /* multilevel.hpp:25 */
 typedef enum { SI_NORMALIZER_INITIAL_GUESS = 0, SI_NORMALIZER_RHS_NORM = 1 } si_normalizer; /* schwarz.hpp:36 */
 typedef enum { SI_FLAVOUR_RAS = 0, SI_FLAVOUR_ORAS = 1 } si_flavour;                      /* schwarz.hpp:29 */
-typedef enum { SI_PRECISION_FP64 = 0, SI_PRECISION_FP32 = 1 } si_precision;
+/* FP64: the reference's arithmetic everywhere.  FP32: everything in float.
+ * MIXED: the image, residual norms and outer iteration in double, the local
+ * CG solves (tolerance 1e-2 by default) in float. */
+typedef enum {
+  SI_PRECISION_FP64 = 0,
+  SI_PRECISION_FP32 = 1,
+  SI_PRECISION_MIXED = 2
+} si_precision;
 
 /* RunOptions (methods.hpp:40-55), field for field, plus the device
  * arithmetic type.  si_default_options() fills the reference defaults. */

@@ -102,8 +102,9 @@ class LevelSolver(enum.IntEnum):
 
 
 class Precision(enum.IntEnum):
-    FP64 = 0
-    FP32 = 1
+    FP64 = 0   # the reference's arithmetic
+    FP32 = 1   # everything in float
+    MIXED = 2  # double image / residuals / outer iteration, float local CG
 
 
 kDefaultOrasAlpha = 0.25  # schwarz.hpp:34

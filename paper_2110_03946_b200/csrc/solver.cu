@@ -142,6 +142,7 @@ struct si_ctx {
   int sweep_nw64 = 2, sweep_nw32 = 2;           // warps per sweep CTA (measured best)
   long long launch_count = 0;                   // kernels launched (always counted)
   int sweep_warp = 0;                           // 1: full blocks on the one-warp variant
+  int local_fp32 = 0;                           // MIXED precision: float local CG (set per call)
   // batch pipeline: two staging slots, one stream per copy direction
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   DevBuf slot_f[2], slot_mask[2], slot_out[2];
@@ -361,6 +362,17 @@ struct LocalCfg {
 
 template <typename T, int NW>
 void launch_sweep_nw(Ctx& x, const SweepArgs<T>& a, int nblocks, int C) {
+  if constexpr (sizeof(T) == 8) {
+    if (x.c.local_fp32) {  // MIXED: double image / outer iteration, float local CG
+      ++x.c.launch_count;
+      if (a.ax.block == kMaxBlock)
+        oras_sweep_kernel<T, NW, true, float><<<dim3(nblocks, C), NW * 32, 0, x.s>>>(a);
+      else
+        oras_sweep_kernel<T, NW, false, float><<<dim3(nblocks, C), NW * 32, 0, x.s>>>(a);
+      CK(cudaGetLastError());
+      return;
+    }
+  }
   if (a.ax.block == kMaxBlock && x.c.sweep_warp) {
     x.c.scratch.ensure(sizeof(T) * kMaxBlock * kMaxBlock * static_cast<size_t>(nblocks) * C);
     SweepArgs<T> aw = a;
@@ -423,14 +435,24 @@ void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_
   }
 }
 
+// MIXED precision for the duration of one ABI call.
+struct LocalPrecision {
+  si_ctx& c;
+  LocalPrecision(si_ctx& ctx, int precision) : c(ctx) {
+    c.local_fp32 = precision == SI_PRECISION_MIXED;
+  }
+  ~LocalPrecision() { c.local_fp32 = 0; }
+};
+
 // ---------------------------------------------------------------- options
 void validate_options_common(const si_options& o) {
   check_arg(o.tolerance > 0.0 && o.coarse_tolerance > 0.0,
             "multilevel_solve: tolerances must be positive");
   check_arg(o.averaging == 0 || o.averaging == 1, "averaging must be KnownOnly or AllPixels");
   check_arg(o.normalizer == 0 || o.normalizer == 1, "normalizer must be InitialGuess or RhsNorm");
-  check_arg(o.precision == SI_PRECISION_FP64 || o.precision == SI_PRECISION_FP32,
-            "precision must be FP64 or FP32");
+  check_arg(o.precision == SI_PRECISION_FP64 || o.precision == SI_PRECISION_FP32 ||
+                o.precision == SI_PRECISION_MIXED,
+            "precision must be FP64, FP32 or MIXED");
 }
 
 // cg_solve's validate_solver_config (cg.hpp:75-80), applied to the local
@@ -955,6 +977,7 @@ void run_device(si_ctx* ctx, int method, const double* d_f, const uint8_t* d_mas
   check_dims(w, h, c);
   validate_options_common(o);
   Ctx x{*ctx, s};
+  LocalPrecision lp(*ctx, o.precision);
   begin_counters(x);
   Trace tr{trace, user, t0};
   if (o.precision == SI_PRECISION_FP32)
@@ -1572,6 +1595,7 @@ si_status si_solve_schwarz(si_ctx* ctx, const double* f, const uint8_t* mask, in
     const uint8_t* d_m = upload(x, ctx->in_mask, mask, n);
     const double* d_ref = reference ? upload(x, ctx->in_ref, reference, n * c) : nullptr;
     ctx->out_img.ensure(n * c * sizeof(double));
+    LocalPrecision lp(*ctx, oo.precision);
     begin_counters(x);
     Trace tr{trace, user, t0};
     if (oo.precision == SI_PRECISION_FP32)
@@ -1921,6 +1945,7 @@ si_status si_device_sweep_rows(si_ctx* ctx, const uint8_t* d_mask, const void* d
       check_arg(std::isfinite(o.alpha), "run_schwarz_level: alpha must be finite");
     set_device(ctx);
     Ctx x{*ctx, pick_stream(ctx, stream)};
+    LocalPrecision lp(*ctx, o.precision);
     begin_counters(x);
     const LocalCfg lc{o.local_tolerance, o.local_max_iterations, o.local_check_interval};
     if (o.precision == SI_PRECISION_FP32)

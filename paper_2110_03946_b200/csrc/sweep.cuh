@@ -95,15 +95,17 @@ __device__ __forceinline__ T robin_diag(int gx, int gy, int lx, int ly, int B, i
   return T(deg) + am1 * T(cut);
 }
 
-template <typename T, int NW>
+// T: storage / outer-iteration type of the image, L: type of the local CG
+// (L = T, or float under double storage for the mixed-precision mode).
+template <typename T, int NW, typename L = T>
 struct SweepSmem {
   __align__(128) T ut[kTileH][tile_w<T>()];  // u_old tile with halo (TMA destination)
   uint64_t bar;                    // TMA completion
-  T pt[kMaxBlock][kMaxBlock + 2];  // stencil operand rows, zero ghost columns 0 and B+1
-  T bt[kMaxBlock][kMaxBlock];      // local right-hand side (true-residual checks)
-  T pub[NW][2][3][32];             // [warp][top/bottom][r,p,x][col]
-  T pubt[NW][2][32];               // true-residual boundary rows
-  T red[3][NW];
+  L pt[kMaxBlock][kMaxBlock + 2];  // stencil operand rows, zero ghost columns 0 and B+1
+  L bt[kMaxBlock][kMaxBlock];      // local right-hand side (true-residual checks)
+  L pub[NW][2][3][32];             // [warp][top/bottom][r,p,x][col]
+  L pubt[NW][2][32];               // true-residual boundary rows
+  L red[3][NW];
 };
 
 // CTA-wide sum; identical value in every thread.  slot selects the buffer so
@@ -283,9 +285,9 @@ __device__ __forceinline__ void residual_rows(const Cell<T, R>& c, const T (*ut)
 // Local right-hand side of my rows (solve_local_block, schwarz.hpp:219-230):
 //   rhs = unk * (pv + knw_W pv_W + knw_E pv_E + knw_N pv_N + knw_S pv_S),
 // knw counting only in-block neighbours (ghost ring = 0).  Returns unk bits.
-template <typename T, int R, bool INV>
+template <typename T, int R, bool INV, typename L>
 __device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, const T (*ut)[tile_w<T>()],
-                                              T (&rhs)[R], uint64_t kb, const T (&bv)[R + 2]) {
+                                              L (&rhs)[R], uint64_t kb, const T (&bv)[R + 2]) {
   const int lane = threadIdx.x & 31;
   T r[R + 2];
   residual_rows<T, R, INV>(c, ut, r, kb, bv);
@@ -311,7 +313,7 @@ __device__ __forceinline__ uint32_t local_rhs(const Cell<T, R>& c, const T (*ut)
       t += (ly + 1 < c.B && ((kb >> (j + 1)) & 1ull)) ? r[j + 1] : T(0);
     }
     t = unk_i ? t : T(0);
-    rhs[i] = t;
+    rhs[i] = static_cast<L>(t);
   }
   return unk;
 }
@@ -346,11 +348,13 @@ struct SweepOcc {
 // FULL: the block is exactly 32x32 (every level of any image >= 32 pixels
 // wide and high with the default block size), so the Robin rows are
 // compile-time positions.
-template <typename T, int NW, bool FULL>
-__global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
+// L: the local CG's type (T, or float under double storage: the outer
+// iteration, residuals and the image stay in T).
+template <typename T, int NW, bool FULL, typename L = T>
+__global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
     oras_sweep_kernel(const __grid_constant__ SweepArgs<T> a) {
   constexpr int R = 32 / NW;  // rows per thread
-  __shared__ SweepSmem<T, NW> S;
+  __shared__ SweepSmem<T, NW, L> S;
 #ifdef SI_PROBE
   const long long pr_k0 = clock64();
   long long pr_k1 = pr_k0, pr_k2 = pr_k0;
@@ -382,7 +386,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
   c.known_invariant = a.known_invariant;
   c.tl = a.use_tma ? tile_lead<T>(c.x0) : 2;
 
-  T x[R], r[R], p[R], q[R];
+  L x[R], r[R], p[R], q[R];
   uint32_t unk;
   // u tile (TMA box or cooperative copy) and the mask bits of my rows, the
   // latter in flight while the tile arrives; then residual and right-hand side
@@ -409,7 +413,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
 #ifdef SI_PROBE_SETUP
     pr_s0 = clock64();
 #endif
-    unk = local_rhs<T, R, INV>(c, S.ut, r, kb, bv);
+    unk = local_rhs<T, R, INV, L>(c, S.ut, r, kb, bv);
 #ifdef SI_PROBE_SETUP
     if (unk == 0xdeadbeefu) a.u_new[0] = r[0];  // forces r complete before the stamp
     pr_s1 = clock64();
@@ -421,17 +425,17 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
     setup(std::false_type{});
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    x[i] = T(0);
+    x[i] = L(0);
     S.bt[c.row0 + i][lane] = r[i];
     S.pt[c.row0 + i][lane + 1] = r[i];  // p = r initially
   }
   if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < R; ++i) S.pt[c.row0 + i][0] = T(0);
+    for (int i = 0; i < R; ++i) S.pt[c.row0 + i][0] = L(0);
   }
   if (lane == B - 1 || (!FULL && lane == 31)) {
 #pragma unroll
-    for (int i = 0; i < R; ++i) S.pt[c.row0 + i][B + 1] = T(0);
+    for (int i = 0; i < R; ++i) S.pt[c.row0 + i][B + 1] = L(0);
   }
   const int any_unknown = __syncthreads_or(unk != 0);
 #ifdef SI_PROBE_SETUP
@@ -439,14 +443,15 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
 #endif
 
   // Robin diagonals of my column: interior rows, block row 0, block row B-1.
-  T dI = T(0), dT = T(0), dB = T(0);
+  L dI = L(0), dT = L(0), dB = L(0);
   if (c.col_ok) {
-    dI = robin_diag(c.gx, c.y0 + 1, lane, 1, B, c.W, c.H, a.am1, a.ras);
-    dT = robin_diag(c.gx, c.y0, lane, 0, B, c.W, c.H, a.am1, a.ras);
-    dB = robin_diag(c.gx, c.y0 + B - 1, lane, B - 1, B, c.W, c.H, a.am1, a.ras);
+    const L am1 = static_cast<L>(a.am1);
+    dI = robin_diag<L>(c.gx, c.y0 + 1, lane, 1, B, c.W, c.H, am1, a.ras);
+    dT = robin_diag<L>(c.gx, c.y0, lane, 0, B, c.W, c.H, am1, a.ras);
+    dB = robin_diag<L>(c.gx, c.y0 + B - 1, lane, B - 1, B, c.W, c.H, am1, a.ras);
   }
-  const T dFirst = (warp == 0) ? dT : dI;        // FULL: row i = 0
-  const T dLast = (warp == NW - 1) ? dB : dI;    // FULL: row i = R-1
+  const L dFirst = (warp == 0) ? dT : dI;        // FULL: row i = 0
+  const L dLast = (warp == NW - 1) ? dB : dI;    // FULL: row i = R-1
   const int iT = -c.row0;            // generic: local index of block row 0
   const int iB = (B - 1) - c.row0;   // generic: local index of block row B-1
 
@@ -471,7 +476,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
   if (any_unknown) {
 #pragma unroll
     for (int i = 0; i < R; ++i) p[i] = r[i];  // r = b - A*0 = b exactly
-    T nb_p[2] = {T(0), T(0)}, nb_r[2] = {T(0), T(0)};
+    L nb_p[2] = {L(0), L(0)}, nb_r[2] = {L(0), L(0)};
 
     auto publish = [&]() {
       if (NW > 1) {
@@ -497,7 +502,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
     };
     // Stage my rows of v as stencil operand (the warp owns whole rows, so a
     // warp barrier suffices; the ghost columns stay zero).
-    auto stage = [&](const T(&v)[R]) {
+    auto stage = [&](const L(&v)[R]) {
       __syncwarp();
 #pragma unroll
       for (int i = 0; i < R; ++i) S.pt[c.row0 + i][lane + 1] = v[i];
@@ -506,40 +511,40 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
     // o = A v on my cells (LocalStencilOperator::apply, schwarz.hpp:146-159):
     // o = unk * (d*v - vW - vE - vN - vS); block-external neighbours are
     // ghost zeros.  v must have been staged.
-    auto apply = [&](const T(&v)[R], T vN0, T vS1, T(&o)[R]) {
+    auto apply = [&](const L(&v)[R], L vN0, L vS1, L(&o)[R]) {
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        const T vW = S.pt[c.row0 + i][lane];
-        const T vE = S.pt[c.row0 + i][lane + 2];
-        const T vN = i > 0 ? v[i - 1] : vN0;
-        const T vS = i + 1 < R ? v[i + 1] : vS1;
-        T d;
+        const L vW = S.pt[c.row0 + i][lane];
+        const L vE = S.pt[c.row0 + i][lane + 2];
+        const L vN = i > 0 ? v[i - 1] : vN0;
+        const L vS = i + 1 < R ? v[i + 1] : vS1;
+        L d;
         if (FULL)
           d = (i == 0) ? dFirst : ((i == R - 1) ? dLast : dI);
         else
           d = (i == iT) ? dT : ((i == iB) ? dB : dI);
         // d*v - (vW + vE) - (vN + vS): dependent depth 3 (the reference's
         // left-to-right chain is 4; the values agree to rounding)
-        const T t = fmaT(d, v[i], -(vW + vE)) - (vN + vS);
-        o[i] = ((unk >> i) & 1u) ? t : T(0);
+        const L t = fmaT(d, v[i], -(vW + vE)) - (vN + vS);
+        o[i] = ((unk >> i) & 1u) ? t : L(0);
       }
     };
 
     publish();
-    T rr = cta_sum<T, NW>(dot2<T, R>(r, r), S.red, 1, warp, lane);  // also orders the pt staging
-    T rr_rcp = recip_rn(rr);
+    L rr = cta_sum<L, NW>(dot2<L, R>(r, r), S.red, 1, warp, lane);  // also orders the pt staging
+    L rr_rcp = recip_rn(rr);
     collect();
     nb_p[0] = nb_r[0];  // p = r initially
     nb_p[1] = nb_r[1];
-    const T r0 = sqrt(rr);
+    const L r0 = sqrt(rr);
     // maybe_done = sqrt(rr_new) <= tol*r0 (cg.hpp:132); the sqrt is only
     // evaluated inside a 1e-12 band around the threshold, outside it the
     // squared comparison decides identically.
-    const T thr = a.ltol * r0;
-    const T thr2 = thr * thr;
-    const T thr2_lo = thr2 * T(1.0 - 1e-6), thr2_hi = thr2 * T(1.0 + 1e-6);
+    const L thr = a.ltol * r0;
+    const L thr2 = thr * thr;
+    const L thr2_lo = thr2 * L(1.0 - 1e-6), thr2_hi = thr2 * L(1.0 + 1e-6);
     converged = false;
-    if (r0 == T(0)) {
+    if (r0 == L(0)) {
       converged = true;
     } else {
       int until_check = a.lcheck;  // iter % lcheck == 0  <=>  countdown hits 0
@@ -549,20 +554,20 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
 #endif
       for (int iter = 1; iter <= a.lmax; ++iter) {
         apply(p, nb_p[0], nb_p[1], q);
-        const T pAp = cta_sum<T, NW>(dot2<T, R>(p, q), S.red, 0, warp, lane);
-        if (!(pAp > T(0)) || !isfinite(pAp)) {  // breakdown (cg.hpp:120-125)
+        const L pAp = cta_sum<L, NW>(dot2<L, R>(p, q), S.red, 0, warp, lane);
+        if (!(pAp > L(0)) || !isfinite(pAp)) {  // breakdown (cg.hpp:120-125)
           iters = iter - 1;
           break;
         }
         SI_PROBE_MARK(0);
-        const T alpha = rr / pAp;
+        const L alpha = rr / pAp;
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           x[i] = fmaT(alpha, p[i], x[i]);
           r[i] = fmaT(-alpha, q[i], r[i]);
         }
         publish();
-        T rr_new = cta_sum<T, NW>(dot2<T, R>(r, r), S.red, 1, warp, lane);
+        L rr_new = cta_sum<L, NW>(dot2<L, R>(r, r), S.red, 1, warp, lane);
         collect();
         if (--until_check == 0) until_check = a.lcheck;
         const bool cadence = until_check == a.lcheck || iter == a.lmax;
@@ -574,18 +579,18 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
           stage(x);
           // the neighbours' boundary rows of x were published before the rr
           // barrier of this iteration
-          const T nx0 = (NW > 1 && warp > 0) ? S.pub[warp - 1][1][2][lane] : T(0);
-          const T nx1 = (NW > 1 && warp + 1 < NW) ? S.pub[warp + 1][0][2][lane] : T(0);
+          const L nx0 = (NW > 1 && warp > 0) ? S.pub[warp - 1][1][2][lane] : L(0);
+          const L nx1 = (NW > 1 && warp + 1 < NW) ? S.pub[warp + 1][0][2][lane] : L(0);
           apply(x, nx0, nx1, q);
 #pragma unroll
           for (int i = 0; i < R; ++i) q[i] = S.bt[c.row0 + i][lane] - q[i];
-          const T part = dot2<T, R>(q, q);
+          const L part = dot2<L, R>(q, q);
           if (NW > 1) {
             S.pubt[warp][0][lane] = q[0];
             S.pubt[warp][1][lane] = q[R - 1];
           }
-          const T tt = cta_sum<T, NW>(part, S.red, 2, warp, lane);
-          const T rel = sqrt(tt) / r0;
+          const L tt = cta_sum<L, NW>(part, S.red, 2, warp, lane);
+          const L rel = sqrt(tt) / r0;
           if (rel <= a.ltol) {
             iters = iter;
             converged = true;
@@ -599,7 +604,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
           }
           rr_new = tt;
         }
-        const T beta = div_by_recip(rr_new, rr, rr_rcp);  // == rr_new / rr
+        const L beta = div_by_recip(rr_new, rr, rr_rcp);  // == rr_new / rr
 #pragma unroll
         for (int i = 0; i < R; ++i) p[i] = fmaT(beta, p[i], r[i]);
         stage(p);
@@ -630,7 +635,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<T, NW>::value))
     const bool own = col_own && ly < B && gy >= oy0 && gy < oy1;
     const size_t pix = own ? static_cast<size_t>(gy) * c.W + c.gx : 0;
     const T uo = S.ut[ly + 2][lane + c.tl];
-    T v = x[i];
+    T v = static_cast<T>(x[i]);
     if (!c.known_invariant) {
       const T bk = c.b[pix];
       if (!((unk >> i) & 1u)) v = bk - uo;

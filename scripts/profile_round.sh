@@ -4,6 +4,7 @@ set -u
 python bench.py --steps 20 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
 echo "bench rc=$?"; tail -c 2000 gpurun_out/bench.json
 python bench.py --steps 20 --warmup 3 --precision fp32 --no-cpu-baseline > gpurun_out/bench_fp32.json 2>&1
+python bench.py --steps 20 --warmup 3 --precision mixed --no-cpu-baseline > gpurun_out/bench_mixed.json 2>&1
 python scripts/profile_frame.py --frames 2 > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file gpurun_out/launches.csv python scripts/profile_frame.py --frames 2 > gpurun_out/ncu_launches.log 2>&1

@@ -122,7 +122,7 @@ def main(tag):
             tj["ncu_full_capture"] = f"profiles/{tag}_sweep_ncu.txt"
             json.dump(tj, open(tp, "w"), indent=1)
     bench = []
-    for name in ("bench.json", "bench_fp32.json"):
+    for name in ("bench.json", "bench_fp32.json", "bench_mixed.json"):
         p = os.path.join(RAW, name)
         if os.path.exists(p):
             for line in open(p):

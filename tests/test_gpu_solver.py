@@ -5,6 +5,8 @@ Bar (stated per assertion):
         1e-9 relative; output max-abs <= 1e-9 and MSE <= 1e-18.
   fp32: equal counts; trace rows within 1e-4 relative; output max-abs <= 5e-4
         and MSE <= 1e-10.
+  mixed (double outer iteration, float local CG): equal counts; trace rows
+        within 1e-5 relative; output max-abs <= 1e-4 and MSE <= 1e-12.
 Behavioural tests port schwarz_test.cpp / multilevel_test.cpp /
 acceptance_test.cpp properties to the GPU path.
 """
@@ -20,6 +22,9 @@ pytestmark = pytest.mark.gpu
 
 FP64 = dict(trace=1e-9, maxabs=1e-9, mse=1e-18)
 FP32 = dict(trace=1e-4, maxabs=5e-4, mse=1e-10)
+# double image / outer iteration, float local CG: the local solves stop at
+# 1e-2, so float changes them at ~1e-7 relative
+MIXED = dict(trace=1e-5, maxabs=1e-4, mse=1e-12)
 
 
 def compare(res, ora, bar, levels=True):
@@ -52,7 +57,8 @@ def opts_dict(o: si.RunOptions, method):
                 cg_max_iterations=o.cg_max_iterations, cg_check_interval=o.cg_check_interval)
 
 
-@pytest.mark.parametrize("precision,bar", [(si.Precision.FP64, FP64), (si.Precision.FP32, FP32)])
+@pytest.mark.parametrize("precision,bar", [(si.Precision.FP64, FP64), (si.Precision.FP32, FP32),
+                                           (si.Precision.MIXED, MIXED)])
 def test_c1_mloras_matches_oracle(solver, oracle, precision, bar):
     """BASELINE config 1: 256x256 grey, 5%, 2 levels (the CPU reference case)."""
     f, m = config_instance(C1)
@@ -65,7 +71,8 @@ def test_c1_mloras_matches_oracle(solver, oracle, precision, bar):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("precision,bar", [(si.Precision.FP64, FP64), (si.Precision.FP32, FP32)])
+@pytest.mark.parametrize("precision,bar", [(si.Precision.FP64, FP64), (si.Precision.FP32, FP32),
+                                           (si.Precision.MIXED, MIXED)])
 def test_c2_mloras_matches_oracle(solver, oracle, precision, bar):
     """BASELINE config 2: 1920x1080 RGB, 4%, 2 levels."""
     f, m = config_instance(C2)
@@ -109,6 +116,16 @@ def test_random_instances_match_oracle(solver, oracle, w, h, c, d, method, kw):
     res = solver.run_method(method, f, m, o)
     ora = oracle.oracle_solve(f.data, m.known, **opts_dict(o, method))
     compare(res, ora, FP64)
+
+
+@pytest.mark.parametrize("w,h,c,d,method,kw", [RANDOM_CASES[i] for i in (0, 3, 6, 9, 14, 16)])
+def test_random_instances_mixed_precision(solver, oracle, w, h, c, d, method, kw):
+    """MIXED: double image and outer iteration, float local CG."""
+    f, m = random_instance(w, h, d, c, 1000 + w + h)
+    o = si.RunOptions(precision=si.Precision.MIXED, **kw)
+    res = solver.run_method(method, f, m, o)
+    ora = oracle.oracle_solve(f.data, m.known, **opts_dict(o, method))
+    compare(res, ora, MIXED)
 
 
 def test_acceptance_oracle_equivalence_dense(solver):
