@@ -66,7 +66,7 @@ struct InpaintingMask {
 enum class Method { Cg = 0, MultilevelCg = 1, Ras = 2, Oras = 3, MultilevelOras = 4 };
 enum class CoarseAveraging { KnownOnly = 0, AllPixels = 1 };
 enum class ResidualNormalizer { InitialGuess = 0, RhsNorm = 1 };
-enum class Precision { FP64 = 0, FP32 = 1 };
+enum class Precision { FP64 = 0, FP32 = 1, MIXED = 2 };  // MIXED: float local CG, double outer iteration
 
 inline constexpr double kDefaultOrasAlpha = 0.25;
 
