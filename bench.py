@@ -337,7 +337,7 @@ def main():
     achieved = (sw["algorithmic_bytes"] / (sw["device_ms"] / 1e3) / 1e9) if sw["device_ms"] else 0.0
     traffic, traffic_alg, fp64_pct = None, None, None
     tfile = os.path.join(ROOT, "profiles", "sweep_dram_traffic.json")
-    if os.path.exists(tfile):  # one ncu --set full capture (scripts/summarize_profiles.py)
+    if os.path.exists(tfile) and prec == si.Precision.FP64:  # ncu capture of the fp64 sweep
         try:
             tj = json.load(open(tfile))
             traffic, traffic_alg = tj.get("dram_bytes_per_launch"), tj.get("algorithmic_bytes_per_launch")
