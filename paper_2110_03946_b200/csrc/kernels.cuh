@@ -406,11 +406,14 @@ __device__ __forceinline__ void prolong_axis(int f, int cn, double& t, int& i0, 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256, 4)
+#ifndef SI_PRO_OCC
+#define SI_PRO_OCC 4
+#endif
+__global__ void __launch_bounds__(256, SI_PRO_OCC)
     prolong_snap_kernel(const T* __restrict__ coarse, int cw, int ch, int fw, int fh, int C,
                         const uint8_t* __restrict__ fmask, const T* __restrict__ fval,
                         T* __restrict__ fine) {
-  constexpr int kCh = 4;  // channels staged per pass
+  constexpr int kCh = 3;  // channels staged per pass
   __shared__ T tile[kCh][kProCY][kProCX];
   const size_t fn = static_cast<size_t>(fw) * fh, cn = static_cast<size_t>(cw) * ch;
   const int fx0 = blockIdx.x * kProX, fy0 = blockIdx.y * kProY;
@@ -436,6 +439,16 @@ __global__ void __launch_bounds__(256, 4)
       const int gy = min(max(cy0 + ly, 0), ch - 1), gx = min(max(cx0 + lx, 0), cw - 1);
       tile[k][ly][lx] = __ldg(coarse + (c0 + k) * cn + static_cast<size_t>(gy) * cw + gx);
     }
+    // the known pixels' data of my quad, in flight across the barrier
+    T sv[kCh][4];
+#pragma unroll
+    for (int k = 0; k < kCh; ++k)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool on = k < nc && ((snap >> q) & 1u);
+        const size_t i = on ? static_cast<size_t>(fyq + (q >> 1)) * fw + fxq + (q & 1) : 0;
+        sv[k][q] = on ? __ldg(fval + (c0 + k) * fn + i) : T(0);
+      }
     __syncthreads();
     // the quad's two columns share the x interpolation across channels;
     // each row of the quad leaves as one 16-byte (fp64) / 8-byte (fp32) store
@@ -459,7 +472,9 @@ __global__ void __launch_bounds__(256, 4)
       const T ty = static_cast<T>(tyd);
       const int a0 = ya - cy0, a1 = yb - cy0;
       const size_t i = static_cast<size_t>(fy) * fw + fxq;
-      for (int k = 0; k < nc; ++k) {
+#pragma unroll
+      for (int k = 0; k < kCh; ++k) {
+        if (k >= nc) break;
         T v[2];
 #pragma unroll
         for (int dx = 0; dx < 2; ++dx) {
@@ -473,7 +488,7 @@ __global__ void __launch_bounds__(256, 4)
           const T p0 = fma(T(1) - tx, v00, tx * v01);
           const T p1 = fma(T(1) - tx, v10, tx * v11);
           v[dx] = fma(T(1) - ty, p0, ty * p1);
-          if ((snap >> (2 * dy + dx)) & 1u) v[dx] = fval[(c0 + k) * fn + i + dx];
+          if ((snap >> (2 * dy + dx)) & 1u) v[dx] = sv[k][2 * dy + dx];
         }
         T* dst = fine + (c0 + k) * fn + i;
         if (pair_store) {
