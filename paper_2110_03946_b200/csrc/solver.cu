@@ -18,6 +18,7 @@
 #include <limits>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <vector>
 #include <functional>
 #include <memory>
@@ -822,8 +823,13 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
     lb.b.ensure(n * C * sizeof(T));
     lb.u0.ensure(n * C * sizeof(T));
     lb.u1.ensure(n * C * sizeof(T));
-    L[l] = {lw[l], lh[l], l == 0 ? d_mask : lb.mask.as<uint8_t>(), lb.b.as<T>(),
-            {lb.u0.as<T>(), lb.u1.as<T>()}, 0};
+    T* u0 = lb.u0.as<T>();
+    // fp64: the caller's output buffer is one of the finest level's ping-pong
+    // iterates, so an even number of finest sweeps needs no export copy
+    if constexpr (std::is_same<T, double>::value)
+      if (l == 0 && d_out != nullptr && d_out != d_ref) u0 = d_out;
+    L[l] = {lw[l], lh[l], l == 0 ? d_mask : lb.mask.as<uint8_t>(), lb.b.as<T>(), {u0, lb.u1.as<T>()},
+            0};
   }
   // K5 ingest: level-0 values, known count for build_rhs's check.
   const size_t n0 = static_cast<size_t>(w) * h;
@@ -909,8 +915,8 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
   else if (coarse_capped)
     std::snprintf(rep->diagnostic, sizeof rep->diagnostic, "%s",
                   "multilevel: a coarse level hit its iteration cap");
-  // Export the finest u (T -> double).
-  {
+  // Export the finest u (T -> double) unless it already lives in d_out.
+  if (static_cast<const void*>(L[0].u[L[0].cur]) != static_cast<const void*>(d_out)) {
     Timed t(x, K_INGEST, static_cast<double>(n0) * C * (8.0 + sizeof(T)));
     ++x.c.launch_count;
     convert_kernel<T, double><<<grid_for(n0 * C, 256, 148 * 16), 256, 0, x.s>>>(
