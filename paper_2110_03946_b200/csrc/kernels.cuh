@@ -213,13 +213,18 @@ __host__ __device__ constexpr int res_tma_box_w() {
   return kResTmaThreads + 2 * res_tma_lead<T>();
 }
 
-template <typename T, bool INV>
+// MTMA: the mask band arrives by a second TMA box on the same barrier (row
+// pitch a multiple of 16 bytes), else per-thread byte loads.  The CTA writes
+// its partial sum; finish_partials_kernel adds them in a fixed order (no
+// fence or ticket in this kernel).
+template <typename T, bool INV, bool MTMA>
 __global__ void __launch_bounds__(kResTmaThreads)
     residual_sumsq_tma_kernel(const __grid_constant__ CUtensorMap umap,
+                              const __grid_constant__ CUtensorMap mmap,
                               const uint8_t* __restrict__ mask, const T* __restrict__ b, int W,
-                              int H, size_t N, int row0, int row1, double* partials, double* out,
-                              unsigned int* ticket) {
+                              int H, size_t N, int row0, int row1, double* partials) {
   __shared__ __align__(128) T tile[kResTmaBand + 2][res_tma_box_w<T>()];
+  __shared__ __align__(128) uint8_t mtile[kResTmaBand][kResTmaThreads];
   __shared__ uint64_t bar;
   const int c = blockIdx.z;
   const T* __restrict__ bc = b + c * N;
@@ -236,8 +241,9 @@ __global__ void __launch_bounds__(kResTmaThreads)
              smem_addr(&tile[0][0]) % 128, smem_addr(&bar), (unsigned)sizeof(tile));
 #endif
     mbar_init(&bar, 1);
-    mbar_expect_tx(&bar, sizeof(tile));
+    mbar_expect_tx(&bar, sizeof(tile) + (MTMA ? sizeof(mtile) : 0));
     tma_load_3d(&tile[0][0], &umap, x0 - res_tma_lead<T>(), y0 - 1, c, &bar);
+    if (MTMA) tma_load_2d(&mtile[0][0], &mmap, x0, y0, &bar);
   }
   uint8_t mk[kResTmaBand];
   T bv[kResTmaBand];
@@ -246,8 +252,10 @@ __global__ void __launch_bounds__(kResTmaThreads)
   for (int k = 0; k < kResTmaBand; ++k) {
     const bool in = xin && k < ny;
     const size_t i = in ? base + static_cast<size_t>(k) * Wz : 0;
-    const uint8_t m = __ldg(mask + i);
-    mk[k] = in ? m : uint8_t(0);
+    if (!MTMA) {
+      const uint8_t m = __ldg(mask + i);
+      mk[k] = in ? m : uint8_t(0);
+    }
     if (!INV) {
       const T bb = __ldg(bc + i);
       bv[k] = in ? bb : T(0);
@@ -255,6 +263,11 @@ __global__ void __launch_bounds__(kResTmaThreads)
   }
   __syncthreads();  // barrier initialised before anyone waits on it
   mbar_wait(&bar, 0);
+  if (MTMA) {
+#pragma unroll
+    for (int k = 0; k < kResTmaBand; ++k)
+      mk[k] = (xin && k < ny) ? mtile[k][threadIdx.x] : uint8_t(0);
+  }
   const int t = threadIdx.x + res_tma_lead<T>();
   const int deg_x = (x > 0) + (x + 1 < W);
   const T deg_in = T(deg_x + 2);
@@ -277,8 +290,35 @@ __global__ void __launch_bounds__(kResTmaThreads)
     up = ctr;
     ctr = dn;
   }
-  reduce_epilogue<kResTmaThreads>(acc, partials, out, ticket, blockIdx.y * gridDim.x + blockIdx.x,
-                                  gridDim.x * gridDim.y, blockIdx.z, gridDim.z);
+  // CTA partial: warp totals, then warp 0 adds them in order
+  __shared__ double wsum[kResTmaThreads / 32];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kResTmaThreads / 32; ++w) t += wsum[w];
+    partials[static_cast<size_t>(blockIdx.z) * gridDim.x * gridDim.y + blockIdx.y * gridDim.x +
+             blockIdx.x] = t;
+  }
+}
+
+// Fixed-order sum of nblk partials per channel (grid: one CTA per channel).
+__global__ void __launch_bounds__(kRedThreads)
+    finish_partials_kernel(const double* __restrict__ partials, int nblk, double* out) {
+  __shared__ double wsum[kRedThreads / 32];
+  const int c = blockIdx.x;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += kRedThreads) s += partials[static_cast<size_t>(c) * nblk + i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kRedThreads / 32; ++w) t += wsum[w];
+    out[c] = t;
+  }
 }
 
 template <typename T>

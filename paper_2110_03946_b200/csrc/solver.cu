@@ -274,6 +274,21 @@ bool make_plane_map(CUtensorMap* m, const void* base, int W, int H, int C, int e
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 2-D u8 map over a [H][W] mask with a (box_w, box_h) box.
+bool make_mask_map(CUtensorMap* m, const void* base, int W, int H, int box_w, int box_h) {
+  auto enc = tensor_map_encoder();
+  if (!enc || tma_disabled() || W % 16 != 0 || reinterpret_cast<uintptr_t>(base) % 16 != 0 ||
+      box_w % 16 != 0 || box_w > 256 || box_h > 256)
+    return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(W)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h)};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename T>
 void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W, int H, int C,
                      int mode, double* out, bool known_invariant = true, int row0 = 0,
@@ -294,17 +309,26 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
     const int tx = (W + kResTmaThreads - 1) / kResTmaThreads;
     const int gy = (rows + kResTmaBand - 1) / kResTmaBand;
     x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(tx) * gy * C);
+    // the mask band rides on the same barrier when its rows are 16-byte aligned
+    CUtensorMap mmap{};
+    const bool mtma = make_mask_map(&mmap, mask, W, H, kResTmaThreads, kResTmaBand);
+    auto launch = [&](auto inv, auto mt) {
+      constexpr bool INV = decltype(inv)::value, MT = decltype(mt)::value;
+      ++x.c.launch_count;
+      residual_sumsq_tma_kernel<T, INV, MT><<<dim3(tx, gy, C), kResTmaThreads, 0, x.s>>>(
+          map, mmap, mask, b, W, H, N, row0, row1, x.c.red_partials.as<double>());
+    };
     if (known_invariant) {
-      ++x.c.launch_count;
-      residual_sumsq_tma_kernel<T, true><<<dim3(tx, gy, C), kResTmaThreads, 0, x.s>>>(
-          map, mask, b, W, H, N, row0, row1, x.c.red_partials.as<double>(), out,
-          x.c.ticket.as<unsigned int>());
+      if (mtma) launch(std::true_type{}, std::true_type{});
+      else launch(std::true_type{}, std::false_type{});
     } else {
-      ++x.c.launch_count;
-      residual_sumsq_tma_kernel<T, false><<<dim3(tx, gy, C), kResTmaThreads, 0, x.s>>>(
-          map, mask, b, W, H, N, row0, row1, x.c.red_partials.as<double>(), out,
-          x.c.ticket.as<unsigned int>());
+      if (mtma) launch(std::false_type{}, std::true_type{});
+      else launch(std::false_type{}, std::false_type{});
     }
+    CK(cudaGetLastError());
+    ++x.c.launch_count;
+    finish_partials_kernel<<<C, kRedThreads, 0, x.s>>>(x.c.red_partials.as<double>(), tx * gy,
+                                                       out);
   } else if (known_invariant) {
     ++x.c.launch_count;
     residual_sumsq_kernel<T, true><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
