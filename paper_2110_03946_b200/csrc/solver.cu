@@ -134,6 +134,7 @@ struct si_ctx {
   // batch's 200 MB image copies on the same engine.
   double* host_red = nullptr;                   // mapped host memory
   double* dev_red = nullptr;                    // device alias of host_red
+  size_t host_red_cap = 0;                      // doubles in host_red
   unsigned long long* host_cnt = nullptr;       // mapped host memory
   unsigned long long* dev_cnt = nullptr;        // device alias of host_cnt
   int profiling = 0;
@@ -637,12 +638,24 @@ void end_counters(Ctx& x, si_report* rep) {
   rep->local_cg_iterations += static_cast<long long>(x.c.host_cnt[1]);
 }
 
+// Mapped scalar slots for 4 values per channel (sums, r0, CG dots, PSNR).
+void ensure_red(si_ctx& c, int C) {
+  const size_t want = 4 * static_cast<size_t>(std::max(C, 1));
+  if (c.host_red && c.host_red_cap >= want) return;
+  if (c.host_red) {
+    CK(cudaDeviceSynchronize());  // no kernel may still write the old slots
+    CK(cudaFreeHost(c.host_red));
+    c.host_red = nullptr;
+  }
+  const size_t cap = std::max<size_t>(want, 256);
+  CK(cudaHostAlloc(&c.host_red, sizeof(double) * cap, cudaHostAllocMapped));
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.dev_red), c.host_red, 0));
+  c.host_red_cap = cap;
+}
+
 void prepare_red(Ctx& x, int C) {
   x.c.red_out.ensure(sizeof(double) * 4 * C);
-  if (!x.c.host_red || C > 64) {
-    // pinned staging sized for up to 64 channels
-  }
-  if (C > 64) fail(SI_ERR_UNSUPPORTED, "more than 64 channels");
+  ensure_red(x.c, C);
 }
 
 // multilevel_solve (multilevel.hpp:239-310) for the Schwarz level solvers.
@@ -1381,9 +1394,8 @@ si_status si_create(int device, si_ctx** out) {
     try {
       CK(cudaSetDevice(device));
       CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
-      CK(cudaHostAlloc(&c->host_red, sizeof(double) * 256, cudaHostAllocMapped));
+      ensure_red(*c, 64);
       CK(cudaHostAlloc(&c->host_cnt, sizeof(unsigned long long) * 8, cudaHostAllocMapped));
-      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dev_red), c->host_red, 0));
       CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dev_cnt), c->host_cnt, 0));
       if (const char* e = std::getenv("SI_SWEEP_WARPS64")) c->sweep_nw64 = std::atoi(e);
       if (const char* e = std::getenv("SI_SWEEP_WARPS32")) c->sweep_nw32 = std::atoi(e);

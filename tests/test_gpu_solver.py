@@ -481,3 +481,14 @@ def test_bitwise_deterministic_across_runs_and_contexts(solver, precision):
         assert np.array_equal(a.image.data, r.image.data)
         assert [x.rel_residual for x in a.trace.rows] == [x.rel_residual for x in r.trace.rows]
         assert a.report.local_cg_iterations == r.report.local_cg_iterations
+
+
+def test_many_channels(solver, oracle):
+    """Channels are independent CTAs of one launch; the mapped scalar slots
+    grow with the channel count (16 and 80 channels against the oracle)."""
+    for c, (w, h) in ((16, (96, 80)), (80, (40, 33))):
+        f, m = random_instance(w, h, 0.05, c, 5)
+        o = si.RunOptions(levels=2)
+        res = solver.run_method(si.Method.MultilevelOras, f, m, o)
+        ora = oracle.oracle_solve(f.data, m.known, **opts_dict(o, si.Method.MultilevelOras))
+        compare(res, ora, FP64)
