@@ -28,6 +28,7 @@
 #include "kernels.cuh"
 #include "sweep.cuh"
 #include "sweep_warp.cuh"
+#include "sweep_generic.cuh"
 #include "cg_level.cuh"
 #include "densify.cuh"
 #include "host_copy.h"
@@ -419,8 +420,6 @@ template <typename T>
 void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_new, int W, int H,
                   int C, int block, int overlap, int flavour, double alpha, const LocalCfg& lc,
                   bool known_invariant, unsigned long long* counters, int by0 = 0, int by1 = -1) {
-  if (block > kMaxBlock)
-    fail(SI_ERR_UNSUPPORTED, "block size " + std::to_string(block) + " exceeds the supported 32");
   SweepArgs<T> a{};
   a.mask = mask;
   a.b = b;
@@ -440,6 +439,24 @@ void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_
   a.counters = counters;
   if (by1 < 0) by1 = a.ay.count;
   a.by0 = by0;
+  if (block > kMaxBlock) {  // K2g: blocks beyond 32x32, CG vectors in global scratch
+    if (by1 <= by0) return;
+    const double bytes = static_cast<double>(a.N) * (2.0 * C * sizeof(T) + 1.0) * (by1 - by0) /
+                         a.ay.count;
+    Timed t(x, K_SWEEP, bytes);
+    const size_t per_row = sizeof(T) * 5 * static_cast<size_t>(block) * block * a.ax.count * C;
+    const int rows = static_cast<int>(std::max<size_t>(1, (size_t(1) << 30) / per_row));
+    x.c.scratch.ensure(per_row * std::min(rows, by1 - by0));
+    a.scratch = x.c.scratch.as<T>();
+    for (int r0 = by0; r0 < by1; r0 += rows) {
+      a.by0 = r0;
+      const int n = a.ax.count * (std::min(by1, r0 + rows) - r0);
+      ++x.c.launch_count;
+      oras_sweep_generic_kernel<T><<<dim3(n, C), kGenThreads, 0, x.s>>>(a);
+      CK(cudaGetLastError());
+    }
+    return;
+  }
   // TMA tile loads: the box starts at the 16-byte aligned column left of each
   // block (tile_lead), so any anchor works; the row pitch must be a multiple
   // of 16 bytes (checked by make_plane_map)

@@ -180,6 +180,29 @@ def test_sweep_arbitrary_u_and_b(solver, oracle):
     assert np.abs(got - want).max() <= 1e-9
 
 
+@pytest.mark.parametrize("w,h,c,d,block,overlap,flavour,seed", [
+    (100, 90, 2, 0.05, 40, 8, 1, 21),   # K2g: blocks beyond 32x32
+    (130, 70, 3, 0.03, 64, 12, 1, 22),
+    (48, 48, 1, 0.1, 48, 0, 1, 23),     # one block, overlap 0
+    (150, 97, 1, 0.2, 33, 5, 0, 24),    # RAS, shifted last blocks
+])
+def test_large_block_sweep_matches_oracle(solver, oracle, w, h, c, d, block, overlap, flavour,
+                                          seed):
+    img, mask = random_instance(w, h, d, c, seed)
+    b = np.where(mask.known[None] != 0, img.data, 0.0)
+    u = b.copy()
+    got, gfail, gits = solver.schwarz_sweep(mask.known, b, u, block, overlap, flavour)
+    want, ofail, oits = oracle.oracle_sweep(mask.known, b, u, block, overlap, flavour=flavour)
+    assert np.abs(got - want).max() <= 1e-10
+    assert gits == oits and gfail == ofail
+    rng = np.random.default_rng(seed)
+    b = rng.uniform(-1, 1, b.shape)
+    u = rng.uniform(-1, 1, b.shape)
+    got, _, _ = solver.schwarz_sweep(mask.known, b, u, block, overlap, flavour)
+    want, _, _ = oracle.oracle_sweep(mask.known, b, u, block, overlap, flavour=flavour)
+    assert np.abs(got - want).max() <= 1e-9
+
+
 def test_division_shortcut_is_ieee_exact(solver):
     """beta = rr_new/rr runs as div_by_recip(rr_new, rr, RN(1/rr)); it must equal
     the IEEE quotient bit for bit (fp64 and fp32)."""

@@ -106,6 +106,9 @@ RANDOM_CASES = [
     (1000, 600, 3, 0.04, si.Method.MultilevelOras, dict()),
     (200, 150, 3, 0.05, si.Method.Oras, dict(overlap=5)),
     (180, 90, 8, 0.05, si.Method.MultilevelOras, dict(overlap=2, levels=2)),
+    # blocks beyond 32x32 (K2g)
+    (260, 190, 3, 0.04, si.Method.MultilevelOras, dict(block_size=64, overlap=10)),
+    (120, 100, 1, 0.05, si.Method.Oras, dict(block_size=40, overlap=6)),
 ]
 
 
