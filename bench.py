@@ -368,9 +368,12 @@ def main():
                      "onchip_bound": {"pipe": "fp64", "pct_of_peak": fp64_pct,
                                       "source": "ncu --set full, first finest-level sweep"}},
         "e2e": {"value": e2e_value, "unit": "frames/s",
-                "h2d_bytes_per_step": int(C4K * n * 8 + n),
-                "d2h_bytes_per_step": int(C4K * n * 8),
-                "api": "si_run_method_batch (host f64 planar + u8 mask in, f64 out; pinned)",
+                "h2d_bytes_per_step": int(np.mean([r.report.h2d_bytes for r in e2e_res])),
+                "d2h_bytes_per_step": int(np.mean([r.report.d2h_bytes for r in e2e_res])),
+                "api": "si_run_method_batch (host f64 planar + u8 mask in, f64 out; pinned); "
+                       "a frame crosses PCIe as its mask + the f values at known pixels "
+                       "(the only ones the solver reads, multilevel.hpp:84-88), packed on "
+                       "host threads inside the timed region",
                 "frames": e2e_steps},
         "e2e_pnm": {"value": pnm_value, "unit": "frames/s",
                     "h2d_bytes_per_step": int(C4K * n + H4K * ((W4K + 7) // 8)),

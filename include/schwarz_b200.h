@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define SI_ABI_VERSION 1
+#define SI_ABI_VERSION 2
 #define SI_MAX_LEVELS 32
 
 typedef enum {
@@ -97,6 +97,8 @@ typedef struct si_report {
   long long local_failures;     /* local CG cap reached or breakdown */
   long long local_cg_iterations;/* sum of local CG iterations (device-counted) */
   double elapsed_ms;            /* host wall clock around the solve */
+  long long h2d_bytes;          /* host->device bytes this frame moved (host entries) */
+  long long d2h_bytes;          /* device->host bytes this frame moved (host entries) */
 } si_report;
 
 /* Trace sink: one call per finest-level outer iteration, row 0 included
@@ -248,6 +250,15 @@ si_status si_stripe_plan(int h, int block_size, int overlap, int world, int rank
  * x0, y0, width, height, own_x0, own_y0, own_x1, own_y1 (row-major blocks). */
 si_status si_partition_domain(int w, int h, int block_size, int overlap, int* blocks_x,
                               int* blocks_y, int* rects, int rects_capacity);
+/* Known-sample packing of the host entries' upload (si_run_method,
+ * si_run_method_batch ship a sparse frame as its mask plus these): the solver
+ * reads f only at known pixels (build_pyramid, multilevel.hpp:84-88).
+ * tile_off[t] = known pixels before tile t (ceil(w*h / SI_KNOWN_TILE) tiles),
+ * *K = known total, vals [c][K] (NULL: count only) = f at the known pixels in
+ * pixel order. */
+#define SI_KNOWN_TILE 4096
+si_status si_pack_known_samples(const double* f, const uint8_t* mask, int w, int h, int c,
+                                uint32_t* tile_off, double* vals, long long* K);
 /* synthetic_test_image (synthetic.hpp:14-59) and random_mask (masks.hpp:25-43):
  * the reference's seeded input generators (libstdc++ <random>). */
 si_status si_synthetic_test_image(int w, int h, int c, uint64_t seed, double* out);

@@ -12,7 +12,8 @@ from .api import (  # noqa: F401
     SchwarzOptions, SchwarzSolveOptions, SolveReport, SolveResult, Solver, SolverConfig,
     SolverError, Subdomain, SubdomainPartition, TraceRow, Unsupported, canonical_r0,
     clamped_partition, default_solver, is_multilevel, kDefaultOrasAlpha, method_name,
-    mse_per_channel, multilevel_solve, pack_pbm, quantise_pnm, parse_method, partition_domain,
+    mse_per_channel, multilevel_solve, pack_known_samples, pack_pbm, quantise_pnm, parse_method,
+    partition_domain,
     psnr, random_mask, run_batch, run_method, run_schwarz_level, solve_schwarz,
     synthetic_test_image, VoronoiAssignment, assign_nearest_site, voronoi_densify)
 

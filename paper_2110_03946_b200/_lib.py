@@ -56,6 +56,8 @@ class si_report(C.Structure):
         ("local_failures", C.c_longlong),
         ("local_cg_iterations", C.c_longlong),
         ("elapsed_ms", C.c_double),
+        ("h2d_bytes", C.c_longlong),
+        ("d2h_bytes", C.c_longlong),
     ]
 
 
@@ -125,6 +127,7 @@ SIGNATURES = {
                                   C.POINTER(si_options), _i, _llp, _llp, _vp]),
     "si_stripe_plan": (_i, [_i, _i, _i, _i, _i, _ip]),
     "si_partition_domain": (_i, [_i, _i, _i, _i, _ip, _ip, _ip, _i]),
+    "si_pack_known_samples": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _llp]),
     "si_synthetic_test_image": (_i, [_i, _i, _i, C.c_uint64, _vp]),
     "si_random_mask": (_i, [_i, _i, _d, C.c_uint64, _vp]),
     "si_default_densify_options": (None, [C.POINTER(si_densify_options)]),
@@ -166,7 +169,7 @@ def load(build_if_missing: bool = True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.si_abi_version() != 1:
+        if lib.si_abi_version() != 2:
             raise RuntimeError("libschwarz_b200.so ABI mismatch")
         _lib = lib
         return lib

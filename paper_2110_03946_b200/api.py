@@ -308,6 +308,8 @@ class SolveReport:  # cg.hpp:29-34 (+ per-level statistics)
     local_failures: int = 0
     local_cg_iterations: int = 0
     elapsed_ms: float = 0.0
+    h2d_bytes: int = 0   # host entries: bytes this frame moved over PCIe
+    d2h_bytes: int = 0
 
 
 @dataclass
@@ -351,7 +353,8 @@ def _report(r: L.si_report) -> SolveReport:
     return SolveReport(r.iterations, r.final_relative_residual, bool(r.converged),
                        r.diagnostic.decode(), d, list(r.level_iterations[:d]),
                        list(r.level_final_rel[:d]), [bool(v) for v in r.level_converged[:d]],
-                       r.local_solves, r.local_failures, r.local_cg_iterations, r.elapsed_ms)
+                       r.local_solves, r.local_failures, r.local_cg_iterations, r.elapsed_ms,
+                       r.h2d_bytes, r.d2h_bytes)
 
 
 # ----------------------------------------------------------------- context
@@ -742,6 +745,28 @@ def partition_domain(width: int, height: int, block_size: int, overlap: int) -> 
     r = np.frombuffer(rects, dtype=np.int32).reshape(n, 8)
     subs = [Subdomain(*map(int, row)) for row in r]
     return SubdomainPartition(width, height, block_size, overlap, bx.value, by.value, subs)
+
+
+KNOWN_TILE = 4096
+
+
+def pack_known_samples(f: ImageBuffer, mask: InpaintingMask):
+    """The host entries' known-sample upload (si_pack_known_samples, host
+    only): (tile_off uint32 [ceil(w*h/4096)], vals float64 [c, K]) with
+    vals[c] = f[c] at the known pixels in pixel order."""
+    _require_same_grid(f, mask)
+    lib = L.load()
+    n = f.width * f.height
+    tiles = np.empty((n + KNOWN_TILE - 1) // KNOWN_TILE, dtype=np.uint32)
+    K = C.c_longlong()
+    known = np.ascontiguousarray(mask.known, dtype=np.uint8)
+    data = np.ascontiguousarray(f.data, dtype=np.float64)
+    _check(lib.si_pack_known_samples(data.ctypes.data, known.ctypes.data, f.width, f.height,
+                                     f.channels, tiles.ctypes.data, None, C.byref(K)))
+    vals = np.empty((f.channels, K.value), dtype=np.float64)
+    _check(lib.si_pack_known_samples(data.ctypes.data, known.ctypes.data, f.width, f.height,
+                                     f.channels, tiles.ctypes.data, vals.ctypes.data, C.byref(K)))
+    return tiles, vals
 
 
 def synthetic_test_image(width: int, height: int, channels: int, seed: int) -> ImageBuffer:

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <condition_variable>
 #include <cstddef>
+#include <cstdint>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -23,13 +24,15 @@
 
 namespace sib {
 
-// memcpy split over a persistent pool of worker threads (the caller takes a
-// share too).
+// Work split over a persistent pool of worker threads (the caller takes a
+// share too): run(fn) calls fn(k, parts) once for every k in [0, parts).
 class CopyPool {
  public:
-  CopyPool() {
+  // threads = 0: min(hardware threads, 16)
+  explicit CopyPool(int threads = 0) {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    nworkers_ = static_cast<int>(std::min(hw, 16u)) - 1;
+    const int t = threads > 0 ? threads : static_cast<int>(std::min(hw, 16u));
+    nworkers_ = std::max(1, t) - 1;
     for (int k = 0; k < nworkers_; ++k) workers_.emplace_back([this, k] { loop(k); });
   }
   ~CopyPool() {
@@ -43,31 +46,41 @@ class CopyPool {
   CopyPool(const CopyPool&) = delete;
   CopyPool& operator=(const CopyPool&) = delete;
 
-  void memcpy(void* dst, const void* src, size_t n) {
+  int parts() const { return nworkers_ + 1; }
+
+  void run(const std::function<void(int, int)>& fn) {
     const int parts = nworkers_ + 1;
-    if (n < (size_t(1) << 20) || parts == 1) {
-      std::memcpy(dst, src, n);
+    if (parts == 1) {
+      fn(0, 1);
       return;
     }
     {
       std::lock_guard<std::mutex> g(m_);
-      dst_ = static_cast<char*>(dst);
-      src_ = static_cast<const char*>(src);
-      n_ = n;
+      job_ = &fn;
       pending_ = nworkers_;
       ++gen_;
     }
     cv_.notify_all();
-    slice(parts - 1, parts);  // the caller's share
+    fn(parts - 1, parts);  // the caller's share
     std::unique_lock<std::mutex> lk(m_);
     done_cv_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+  void memcpy(void* dst, const void* src, size_t n) {
+    if (n < (size_t(1) << 20) || nworkers_ == 0) {
+      std::memcpy(dst, src, n);
+      return;
+    }
+    char* d = static_cast<char*>(dst);
+    const char* s = static_cast<const char*>(src);
+    run([&](int k, int parts) {
+      const size_t a = n * k / parts, b = n * (k + 1) / parts;
+      std::memcpy(d + a, s + a, b - a);
+    });
   }
 
  private:
-  void slice(int k, int parts) {
-    const size_t a = n_ * k / parts, b = n_ * (k + 1) / parts;
-    std::memcpy(dst_ + a, src_ + a, b - a);
-  }
   void loop(int k) {
     long seen = 0;
     for (;;) {
@@ -75,8 +88,9 @@ class CopyPool {
       cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
       if (stop_) return;
       seen = gen_;
+      const std::function<void(int, int)>* job = job_;
       lk.unlock();
-      slice(k, nworkers_ + 1);
+      (*job)(k, nworkers_ + 1);
       lk.lock();
       if (--pending_ == 0) done_cv_.notify_one();
     }
@@ -86,13 +100,103 @@ class CopyPool {
   std::vector<std::thread> workers_;
   std::mutex m_;
   std::condition_variable cv_, done_cv_;
-  char* dst_ = nullptr;
-  const char* src_ = nullptr;
-  size_t n_ = 0;
+  const std::function<void(int, int)>* job_ = nullptr;
   int pending_ = 0;
   long gen_ = 0;
   bool stop_ = false;
 };
+
+// Known-sample upload (batch entry): the solver reads f only where the mask
+// is set (build_pyramid zeroes the rest, multilevel.hpp:84-88), so a frame
+// crosses PCIe as its mask, the known values in pixel order per channel and
+// the exclusive known-count of every kKnownTile-pixel tile (the device
+// scatter's offsets).  Pass 1 counts per tile, pass 2 gathers.
+constexpr int kKnownTile = 4096;
+
+// high bit of every nonzero byte of w
+inline uint64_t nonzero_bytes(uint64_t w) {
+  constexpr uint64_t lo7 = 0x7F7F7F7F7F7F7F7Full;
+  return (((w & lo7) + lo7) | w) & ~lo7;
+}
+
+inline uint64_t load_word(const uint8_t* p) {
+  uint64_t w;
+  std::memcpy(&w, p, 8);
+  return w;
+}
+
+// Bit j of the result = (mask[a + j] != 0), j < min(64, b - a).  Branch-free
+// over eight 8-byte words (the high bits of nonzero_bytes gathered by one
+// multiply).
+inline uint64_t known_bits64(const uint8_t* mask, size_t a, size_t b) {
+  uint64_t bits = 0;
+  if (b - a >= 64) {
+    for (int k = 0; k < 8; ++k) {
+      const uint64_t hi = nonzero_bytes(load_word(mask + a + 8 * k)) >> 7;  // bit 8j
+      bits |= ((hi * 0x0102040810204080ull) >> 56) << (8 * k);
+    }
+  } else {
+    for (size_t i = a; i < b; ++i) bits |= static_cast<uint64_t>(mask[i] != 0) << (i - a);
+  }
+  return bits;
+}
+
+// tile_off[t] <- known pixels in tiles [0, t); returns the total.
+inline size_t count_known_tiles(CopyPool& pool, const uint8_t* mask, size_t n, uint32_t* tile_off) {
+  const size_t ntiles = (n + kKnownTile - 1) / kKnownTile;
+  pool.run([&](int k, int parts) {
+    const size_t t0 = ntiles * k / parts, t1 = ntiles * (k + 1) / parts;
+    for (size_t t = t0; t < t1; ++t) {
+      const size_t a = t * kKnownTile, b = std::min(n, a + kKnownTile);
+      uint32_t cnt = 0;
+      for (size_t i = a; i < b; i += 64)
+        cnt += __builtin_popcountll(known_bits64(mask, i, std::min(b, i + 64)));
+      tile_off[t] = cnt;
+    }
+  });
+  size_t run = 0;
+  for (size_t t = 0; t < ntiles; ++t) {
+    const uint32_t c = tile_off[t];
+    tile_off[t] = static_cast<uint32_t>(run);
+    run += c;
+  }
+  return run;
+}
+
+// vals[c*K + rank] = f[c*n + p] for the rank-th known pixel p.  Each part
+// lists its known positions first (64 pixels per mask word, one tzcnt per
+// known pixel), then gathers channel by channel with software prefetch: the
+// loads are independent, so the part runs at memory-level parallelism
+// instead of stalling on mispredicted mask branches.
+inline void gather_known(CopyPool& pool, const uint8_t* mask, const double* f, size_t n, int C,
+                         const uint32_t* tile_off, size_t K, double* vals) {
+  const size_t ntiles = (n + kKnownTile - 1) / kKnownTile;
+  pool.run([&](int k, int parts) {
+    const size_t t0 = ntiles * k / parts, t1 = ntiles * (k + 1) / parts;
+    if (t0 >= t1) return;
+    const size_t o0 = tile_off[t0], o1 = t1 < ntiles ? tile_off[t1] : K;
+    std::vector<size_t> pos(o1 - o0 + 1);
+    size_t o = 0;
+    const size_t a = t0 * kKnownTile, b = std::min(n, t1 * kKnownTile);
+    for (size_t i = a; i < b; i += 64) {
+      uint64_t bits = known_bits64(mask, i, std::min(b, i + 64));
+      while (bits) {
+        pos[o++] = i + __builtin_ctzll(bits);
+        bits &= bits - 1;
+      }
+    }
+    const size_t m = o;
+    constexpr size_t kAhead = 24;
+    for (int c = 0; c < C; ++c) {
+      const double* fc = f + static_cast<size_t>(c) * n;
+      double* vc = vals + static_cast<size_t>(c) * K + o0;
+      for (size_t j = 0; j < m; ++j) {
+        if (j + kAhead < m) __builtin_prefetch(fc + pos[j + kAhead]);
+        vc[j] = fc[pos[j]];
+      }
+    }
+  });
+}
 
 inline bool host_is_pinned(const void* p) {
   cudaPointerAttributes a{};

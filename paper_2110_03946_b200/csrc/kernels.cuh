@@ -391,6 +391,51 @@ __global__ void ingest_kernel(const double* __restrict__ f, const uint8_t* __res
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(known, static_cast<unsigned long long>(cnt));
 }
 
+// K5s: the same level-0 values from the known samples alone (the batch
+// upload, host_copy.h): vals[c*K + rank] is the rank-th known pixel's value,
+// tile_off[t] the known count before tile t (kKnownTile = 4096 pixels).
+// One CTA per tile, warp w walks pixels w*512 .. w*512+511 of it in 16
+// coalesced steps: the ballots of pass 1 give the warp totals, pass 2 the
+// ranks (popc of the lower lanes' bits).
+constexpr int kScatterTile = 4096, kScatterWarps = 8, kScatterSteps = kScatterTile / (32 * kScatterWarps);
+template <typename T>
+__global__ void __launch_bounds__(kScatterWarps * 32) known_scatter_kernel(
+    const uint8_t* __restrict__ mask, size_t N, int C, const double* __restrict__ vals, size_t K,
+    const uint32_t* __restrict__ tile_off, T* __restrict__ b, unsigned long long* known) {
+  __shared__ uint32_t warp_cnt[kScatterWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t base = static_cast<size_t>(blockIdx.x) * kScatterTile + warp * (32 * kScatterSteps);
+  uint32_t ballot[kScatterSteps];
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int s = 0; s < kScatterSteps; ++s) {
+    const size_t p = base + s * 32 + lane;
+    const bool k = p < N && mask[p] != 0;
+    ballot[s] = __ballot_sync(0xffffffffu, k);
+    cnt += __popc(ballot[s]);
+  }
+  if (lane == 0) warp_cnt[warp] = cnt;
+  __syncthreads();
+  size_t o = tile_off[blockIdx.x];
+  for (int w = 0; w < warp; ++w) o += warp_cnt[w];
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < kScatterWarps; ++w) tot += warp_cnt[w];
+    if (tot) atomicAdd(known, static_cast<unsigned long long>(tot));
+  }
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int s = 0; s < kScatterSteps; ++s) {
+    const size_t p = base + s * 32 + lane;
+    const bool k = (ballot[s] >> lane) & 1u;
+    const size_t r = o + __popc(ballot[s] & lt);
+    if (p < N)
+      for (int c = 0; c < C; ++c)
+        b[c * N + p] = k ? static_cast<T>(vals[c * K + r]) : T(0);
+    o += __popc(ballot[s]);
+  }
+}
+
 // K3: restrict_level (multilevel.hpp:33-70): coarse pixel = clipped 2x2 fine
 // cell; known = OR; value = mean of known fine values (KnownOnly) or of all
 // of them (AllPixels), accumulated in row-major order like the reference.

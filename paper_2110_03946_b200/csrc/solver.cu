@@ -21,6 +21,7 @@
 #include <type_traits>
 #include <vector>
 #include <functional>
+#include <future>
 #include <memory>
 
 #include "../../include/schwarz_b200.h"
@@ -153,6 +154,11 @@ struct si_ctx {
   std::unique_ptr<sib::Stager> stager;          // pageable host <-> device copies
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_solved[2] = {nullptr, nullptr},
               ev_d2h[2] = {nullptr, nullptr};
+  // known-sample upload of the batch entry (host_copy.h): pinned packs
+  // [tile offsets | values] per slot, packed by pack_pool
+  std::unique_ptr<sib::CopyPool> pack_pool;
+  void* pack_buf[2] = {nullptr, nullptr};
+  size_t pack_cap[2] = {0, 0};
 };
 
 namespace {
@@ -849,13 +855,23 @@ LevelOutcome run_cg_level(Ctx& x, LevelView<T>& V, int C, double tol, const si_o
   return out;
 }
 
+// Level-0 input as known samples (batch upload, host_copy.h) instead of f.
+struct KnownSamples {
+  const double* vals;        // [C][K]
+  const uint32_t* tile_off;  // known count before each kScatterTile-pixel tile
+  size_t K;
+  size_t bytes;              // uploaded: offsets + values
+};
+static_assert(kScatterTile == sib::kKnownTile, "host and device tile sizes differ");
+
 // fixed_block >= 0 selects solve_schwarz's explicit, unclamped partition
 // (schwarz.hpp:349-389) instead of clamped_partition per level.
 template <typename T>
 void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
                        const uint8_t* d_mask, int w, int h, int C, const si_options& o,
                        const double* d_ref, double* d_out, si_report* rep, const Trace& tr,
-                       int fixed_block = -1, int fixed_overlap = 0) {
+                       int fixed_block = -1, int fixed_overlap = 0,
+                       const KnownSamples* ks = nullptr) {
   prepare_red(x, C);
   check_arg(levels_req >= 1, "build_pyramid: levels must be >= 1");
   // Level geometry: halve (ceil) until the requested depth or a level that
@@ -887,7 +903,15 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
   }
   // K5 ingest: level-0 values, known count for build_rhs's check.
   const size_t n0 = static_cast<size_t>(w) * h;
-  {
+  if (ks) {  // K5s: only the known samples came over
+    Timed t(x, K_INGEST, static_cast<double>(n0) * (C * sizeof(T) + 1.0) + ks->K * C * 8.0);
+    ++x.c.launch_count;
+    known_scatter_kernel<T><<<static_cast<unsigned>((n0 + kScatterTile - 1) / kScatterTile),
+                              kScatterWarps * 32, 0, x.s>>>(
+        d_mask, n0, C, ks->vals, ks->K, ks->tile_off, x.c.levels[0].b.as<T>(),
+        x.c.counters.as<unsigned long long>() + 2);
+    CK(cudaGetLastError());
+  } else {
     Timed t(x, K_INGEST, static_cast<double>(n0) * (C * (8.0 + sizeof(T)) + 1.0));
     ++x.c.launch_count;
     ingest_kernel<T><<<grid_for(n0, 256, 148 * 16), 256, 0, x.s>>>(
@@ -1032,7 +1056,8 @@ void check_dims(int w, int h, int c) {
 
 void run_device(si_ctx* ctx, int method, const double* d_f, const uint8_t* d_mask, int w, int h,
                 int c, const si_options& o, const double* d_ref, double* d_out, si_report* rep,
-                si_trace_fn trace, void* user, cudaStream_t s, Clock::time_point t0) {
+                si_trace_fn trace, void* user, cudaStream_t s, Clock::time_point t0,
+                const KnownSamples* ks = nullptr) {
   check_method(method);
   check_dims(w, h, c);
   validate_options_common(o);
@@ -1042,11 +1067,75 @@ void run_device(si_ctx* ctx, int method, const double* d_f, const uint8_t* d_mas
   Trace tr{trace, user, t0};
   if (o.precision == SI_PRECISION_FP32)
     multilevel_device<float>(x, levels_for(method, o), flavour_for(method), d_f, d_mask, w, h, c,
-                             o, d_ref, d_out, rep, tr);
+                             o, d_ref, d_out, rep, tr, -1, 0, ks);
   else
     multilevel_device<double>(x, levels_for(method, o), flavour_for(method), d_f, d_mask, w, h, c,
-                              o, d_ref, d_out, rep, tr);
+                              o, d_ref, d_out, rep, tr, -1, 0, ks);
   end_counters(x, rep);
+}
+
+// SI_NO_KNOWN_PACK=1: always upload the full f (A/B measurements).
+// Host threads packing known samples (SI_PACK_THREADS; default half the
+// hardware threads, at most 8: a 4K RGB frame packs in ~9 ms on one thread,
+// memory-latency bound, and the thread driving the solves must keep a core;
+// scripts/e2e_probe.py measures the settings).
+int pack_threads() {
+  static const int n = [] {
+    const char* e = std::getenv("SI_PACK_THREADS");
+    const int v = e ? std::atoi(e) : 0;
+    const int hw = static_cast<int>(std::max(2u, std::thread::hardware_concurrency()));
+    return v > 0 ? v : std::min(8, hw / 2);
+  }();
+  return n;
+}
+
+bool known_pack_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("SI_NO_KNOWN_PACK");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
+// Single-frame known-sample upload into ctx->in_f (host_copy.h): packs on the
+// host pool into pack_buf[0] and queues the copy on x.s.  False (nothing
+// queued) when more than 1/8 of the pixels are known.
+bool upload_known(Ctx& x, const double* f, const uint8_t* mask, size_t n, int C,
+                  KnownSamples* ks) {
+  si_ctx& c = x.c;
+  const size_t ntiles = (n + sib::kKnownTile - 1) / sib::kKnownTile;
+  const size_t off_bytes = (ntiles * sizeof(uint32_t) + 15) / 16 * 16;
+  if (n < (size_t(1) << 16) || known_pack_disabled()) return false;  // small: one plain copy
+  if (!c.pack_pool) c.pack_pool = std::make_unique<sib::CopyPool>(pack_threads());
+  if (c.ev_h2d[0]) CK(cudaEventSynchronize(c.ev_h2d[0]));  // a batch upload may still read it
+  CK(cudaStreamSynchronize(x.s));                          // and so may this stream's last one
+  auto grow = [&](size_t need, size_t keep) {
+    if (c.pack_cap[0] >= need) return;
+    void* nb = nullptr;
+    const size_t cap = need + need / 4;
+    CK(cudaMallocHost(&nb, cap));
+    if (c.pack_buf[0]) {
+      std::memcpy(nb, c.pack_buf[0], keep);
+      CK(cudaFreeHost(c.pack_buf[0]));
+    }
+    c.pack_buf[0] = nb;
+    c.pack_cap[0] = cap;
+  };
+  grow(off_bytes, 0);
+  const size_t K = sib::count_known_tiles(*c.pack_pool, mask, n,
+                                          static_cast<uint32_t*>(c.pack_buf[0]));
+  if (K * 8 > n) return false;
+  const size_t bytes = off_bytes + K * C * sizeof(double);
+  grow(bytes, off_bytes);
+  char* buf = static_cast<char*>(c.pack_buf[0]);
+  sib::gather_known(*c.pack_pool, mask, f, n, C, reinterpret_cast<const uint32_t*>(buf), K,
+                    reinterpret_cast<double*>(buf + off_bytes));
+  CK(cudaMemcpyAsync(c.in_f.ptr, buf, bytes, cudaMemcpyHostToDevice, x.s));
+  ks->tile_off = c.in_f.as<uint32_t>();
+  ks->vals = reinterpret_cast<const double*>(c.in_f.as<uint8_t>() + off_bytes);
+  ks->K = K;
+  ks->bytes = bytes;
+  return true;
 }
 
 // Batch pipeline shared by si_run_method_batch (f64 planar in/out) and
@@ -1081,25 +1170,91 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
   auto raw_in = [&](int s) { return ctx->slot_f[s].as<uint8_t>() + (pnm ? img : 0); };
   auto raw_mask = [&](int s) { return ctx->slot_mask[s].as<uint8_t>() + (pnm ? n_px : 0); };
   auto raw_out = [&](int s) { return ctx->slot_out[s].as<uint8_t>() + (pnm ? img : 0); };
+  // Known-sample upload (f64 frames whose mask is at most 1/8 known): a
+  // helper thread packs frame k+2 on the host pool while frame k is solved
+  // and frame k+1 is in flight; pack_buf[s] = [tile offsets | C x K values].
+  const size_t ntiles = (n_px + sib::kKnownTile - 1) / sib::kKnownTile;
+  const size_t off_bytes = (ntiles * sizeof(uint32_t) + 15) / 16 * 16;
+  struct Pack {
+    size_t K = 0;
+    bool sparse = false;
+    long long h2d = 0;
+  };
+  std::vector<Pack> packs(n);
+  const bool may_pack = !pnm && !known_pack_disabled();
+  if (may_pack && !ctx->pack_pool) ctx->pack_pool = std::make_unique<sib::CopyPool>(pack_threads());
+  auto grow = [&](int s, size_t need, size_t keep) {
+    if (ctx->pack_cap[s] >= need) return;
+    void* nb = nullptr;
+    const size_t cap = need + need / 4;
+    CK(cudaMallocHost(&nb, cap));
+    if (ctx->pack_buf[s]) {
+      std::memcpy(nb, ctx->pack_buf[s], keep);
+      CK(cudaFreeHost(ctx->pack_buf[s]));
+    }
+    ctx->pack_buf[s] = nb;
+    ctx->pack_cap[s] = cap;
+  };
+  auto pack = [&](int k) {
+    const int s = k & 1;
+    CK(cudaEventSynchronize(ctx->ev_h2d[s]));  // frame k-2's upload left pack_buf[s]
+    grow(s, off_bytes, 0);
+    uint32_t* off = static_cast<uint32_t*>(ctx->pack_buf[s]);
+    Pack& P = packs[k];
+    P.K = sib::count_known_tiles(*ctx->pack_pool, mask[k], n_px, off);
+    P.sparse = P.K * 8 <= n_px;
+    if (!P.sparse) return;
+    grow(s, off_bytes + P.K * c * sizeof(double), off_bytes);
+    sib::gather_known(*ctx->pack_pool, mask[k], static_cast<const double*>(in[k]), n_px, c,
+                      static_cast<const uint32_t*>(ctx->pack_buf[s]), P.K,
+                      reinterpret_cast<double*>(static_cast<char*>(ctx->pack_buf[s]) + off_bytes));
+  };
   auto h2d = [&](int k) {
     const int s = k & 1;
-    CK(cudaMemcpyAsync(raw_in(s), in[k], in_bytes, cudaMemcpyHostToDevice, ctx->h2d_stream));
+    Pack& P = packs[k];
+    if (P.sparse) {
+      const size_t bytes = off_bytes + P.K * c * sizeof(double);
+      CK(cudaMemcpyAsync(raw_in(s), ctx->pack_buf[s], bytes, cudaMemcpyHostToDevice,
+                         ctx->h2d_stream));
+      P.h2d = static_cast<long long>(bytes + mask_bytes);
+    } else {
+      CK(cudaMemcpyAsync(raw_in(s), in[k], in_bytes, cudaMemcpyHostToDevice, ctx->h2d_stream));
+      P.h2d = static_cast<long long>(in_bytes + mask_bytes);
+    }
     CK(cudaMemcpyAsync(raw_mask(s), mask[k], mask_bytes, cudaMemcpyHostToDevice,
                        ctx->h2d_stream));
     CK(cudaEventRecord(ctx->ev_h2d[s], ctx->h2d_stream));
   };
+  std::future<void> packing;
+  auto pack_async = [&](int k) {
+    if (may_pack && k < n) packing = std::async(std::launch::async, [&pack, k] { pack(k); });
+  };
   cudaStream_t cs = ctx->own_stream;
-  if (n > 0) h2d(0);
+  if (n > 0) {
+    if (may_pack) pack(0);
+    h2d(0);
+    pack_async(1);
+  }
   for (int k = 0; k < n; ++k) {
     const int s = k & 1;
     // the other slot's input was consumed by frame k-1 (solved synchronously)
-    if (k + 1 < n) h2d(k + 1);
+    if (k + 1 < n) {
+      if (may_pack) packing.get();
+      h2d(k + 1);
+      pack_async(k + 2);
+    }
     CK(cudaStreamWaitEvent(cs, ctx->ev_h2d[s], 0));
     if (k >= 2) CK(cudaStreamWaitEvent(cs, ctx->ev_d2h[s], 0));  // out slot free again
     si_report local;
     si_report* rep = reports ? &reports[k] : &local;
     clear_report(rep);
     const auto t0 = Clock::now();
+    KnownSamples ks{};
+    if (packs[k].sparse) {
+      ks.tile_off = ctx->slot_f[s].as<uint32_t>();
+      ks.vals = reinterpret_cast<const double*>(ctx->slot_f[s].as<uint8_t>() + off_bytes);
+      ks.K = packs[k].K;
+    }
     if (pnm) {
       // read_pnm / read_mask_pbm (pnm.hpp:98-188) on device
       ++ctx->launch_count;
@@ -1109,7 +1264,8 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
       CK(cudaGetLastError());
     }
     run_device(ctx, method, ctx->slot_f[s].as<double>(), ctx->slot_mask[s].as<uint8_t>(), w, h, c,
-               o, nullptr, ctx->slot_out[s].as<double>(), rep, nullptr, nullptr, cs, t0);
+               o, nullptr, ctx->slot_out[s].as<double>(), rep, nullptr, nullptr, cs, t0,
+               packs[k].sparse ? &ks : nullptr);
     if (pnm) {
       // write_pnm's quantise (pnm.hpp:82-85, 130-147)
       ++ctx->launch_count;
@@ -1118,6 +1274,8 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
       CK(cudaGetLastError());
     }
     rep->elapsed_ms = ms_since(t0);
+    rep->h2d_bytes = packs[k].h2d;
+    rep->d2h_bytes = static_cast<long long>(out_bytes);
     CK(cudaEventRecord(ctx->ev_solved[s], cs));
     CK(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_solved[s], 0));
     CK(cudaMemcpyAsync(out[k], raw_out(s), out_bytes, cudaMemcpyDeviceToHost, ctx->d2h_stream));
@@ -1441,6 +1599,9 @@ void si_destroy(si_ctx* c) {
     b->release();
   c->vz.release();
   c->stager.reset();
+  c->pack_pool.reset();
+  for (void* b : c->pack_buf)
+    if (b) cudaFreeHost(b);
   for (auto& p : c->pending) {
     cudaEventDestroy(p.start);
     cudaEventDestroy(p.stop);
@@ -1515,17 +1676,23 @@ si_status si_run_method(si_ctx* ctx, int method, const double* f, const uint8_t*
     ctx->in_f.ensure(n * c * sizeof(double));
     ctx->in_mask.ensure(n);
     ctx->out_img.ensure(n * c * sizeof(double));
-    h2d(x, ctx->in_f.ptr, f, n * c * sizeof(double));
+    KnownSamples ks{};
+    const bool sparse = upload_known(x, f, mask, n, c, &ks);
+    if (!sparse) h2d(x, ctx->in_f.ptr, f, n * c * sizeof(double));
     h2d(x, ctx->in_mask.ptr, mask, n);
+    long long up = static_cast<long long>(sparse ? ks.bytes : n * c * sizeof(double)) + n;
     const double* d_ref = nullptr;
     if (reference) {
       ctx->in_ref.ensure(n * c * sizeof(double));
       h2d(x, ctx->in_ref.ptr, reference, n * c * sizeof(double));
       d_ref = ctx->in_ref.as<double>();
+      up += static_cast<long long>(n * c * sizeof(double));
     }
     run_device(ctx, method, ctx->in_f.as<double>(), ctx->in_mask.as<uint8_t>(), w, h, c, o, d_ref,
-               ctx->out_img.as<double>(), rep, trace, user, x.s, t0);
+               ctx->out_img.as<double>(), rep, trace, user, x.s, t0, sparse ? &ks : nullptr);
     d2h(x, out, ctx->out_img.ptr, n * c * sizeof(double));
+    rep->h2d_bytes = up;
+    rep->d2h_bytes = static_cast<long long>(n * c * sizeof(double));
   });
   rep->elapsed_ms = ms_since(t0);
   return st;
@@ -2031,6 +2198,22 @@ si_status si_device_sweep_rows(si_ctx* ctx, const uint8_t* d_mask, const void* d
 #endif
     if (failures) *failures = static_cast<long long>(ctx->host_cnt[0]);
     if (cg_iterations) *cg_iterations = static_cast<long long>(ctx->host_cnt[1]);
+  });
+}
+
+si_status si_pack_known_samples(const double* f, const uint8_t* mask, int w, int h, int c,
+                                uint32_t* tile_off, double* vals, long long* K) {
+  return guard([&] {
+    check_arg(mask && tile_off && K && (f || !vals), "null argument");
+    check_dims(w, h, c);
+    static_assert(SI_KNOWN_TILE == sib::kKnownTile, "header and host tile sizes differ");
+    static sib::CopyPool pool;
+    static std::mutex m;
+    std::lock_guard<std::mutex> g(m);
+    const size_t n = static_cast<size_t>(w) * h;
+    const size_t k = sib::count_known_tiles(pool, mask, n, tile_off);
+    if (vals) sib::gather_known(pool, mask, f, n, c, tile_off, k, vals);
+    *K = static_cast<long long>(k);
   });
 }
 

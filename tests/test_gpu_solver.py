@@ -340,6 +340,73 @@ def test_batch_equals_individual_solves(solver):
         assert b.report.converged
 
 
+def _device_solve(solver, method, f, m, o):
+    """run_method through the device entry (dense on-device ingest)."""
+    import torch
+    df = torch.from_numpy(np.ascontiguousarray(f.data)).cuda()
+    dm = torch.from_numpy(np.ascontiguousarray(m.known)).cuda()
+    out = torch.empty_like(df)
+    rep = solver.run_method_device(method, df.data_ptr(), dm.data_ptr(), f.width, f.height,
+                                   f.channels, out.data_ptr(), o)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), rep
+
+
+def test_known_sample_upload_matches_dense_ingest(solver):
+    """si_run_method ships a sparse frame as mask + known samples (scatter
+    kernel on the device); the result equals the dense device ingest bitwise,
+    NaN at unknown pixels and mask bytes other than 1 included."""
+    w, h, c = 701, 389, 3
+    f = si.synthetic_test_image(w, h, c, 5)
+    m = si.random_mask(w, h, 0.04, 6)
+    m.known[m.known != 0] = 200
+    f.data[:, m.known == 0] = np.nan
+    o = si.RunOptions()
+    res = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    want, rep = _device_solve(solver, si.Method.MultilevelOras, f, m, o)
+    assert np.array_equal(res.image.data, want)
+    assert res.report.level_iterations == rep.level_iterations
+    K = int((m.known != 0).sum())
+    tiles = (w * h + 4095) // 4096
+    assert res.report.h2d_bytes == (tiles * 4 + 15) // 16 * 16 + K * c * 8 + w * h
+    assert res.report.d2h_bytes == w * h * c * 8
+
+
+def test_batch_known_sample_and_dense_frames(solver):
+    """A batch mixing sparse frames (known-sample upload) and dense ones
+    (mask density above 1/8: plain upload) equals the device path frame by
+    frame, bitwise; the reports carry each frame's PCIe bytes."""
+    w, h, c = 300, 200, 3
+    dens = [0.04, 0.5, 0.02, 0.2, 0.04, 0.01]
+    frames = []
+    for k, d in enumerate(dens):
+        f = si.synthetic_test_image(w, h, c, 40 + k)
+        m = si.random_mask(w, h, d, 50 + k)
+        f.data[:, m.known == 0] = np.inf
+        frames.append((f, m))
+    o = si.RunOptions()
+    batch = solver.run_batch(si.Method.MultilevelOras, frames, o)
+    for (f, m), b in zip(frames, batch):
+        want, rep = _device_solve(solver, si.Method.MultilevelOras, f, m, o)
+        assert np.array_equal(b.image.data, want)
+        assert b.report.level_iterations == rep.level_iterations
+        K = int((m.known != 0).sum())
+        if K * 8 <= w * h:
+            tiles = (w * h + 4095) // 4096
+            assert b.report.h2d_bytes == (tiles * 4 + 15) // 16 * 16 + K * c * 8 + w * h
+        else:
+            assert b.report.h2d_bytes == w * h * c * 8 + w * h
+
+
+def test_known_sample_upload_empty_mask_raises(solver):
+    f = si.synthetic_test_image(400, 300, 1, 1)
+    m = si.InpaintingMask(400, 300)
+    with pytest.raises(si.InvalidArgument, match="no known pixels"):
+        solver.run_method(si.Method.MultilevelOras, f, m)
+    with pytest.raises(si.InvalidArgument, match="no known pixels"):
+        solver.run_batch(si.Method.MultilevelOras, [(f, m)])
+
+
 # ---------------------------------------------------------------- multilevel CG
 CG_CASES = [
     (si.Method.MultilevelCg, C1, dict(levels=2)),
