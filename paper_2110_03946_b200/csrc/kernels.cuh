@@ -373,8 +373,12 @@ __global__ void ingest_kernel(const double* __restrict__ f, const uint8_t* __res
     for (size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < pairs; j += stride) {
       const uchar2 m = reinterpret_cast<const uchar2*>(mask)[j];
       cnt += (m.x != 0) + (m.y != 0);
+      // f is read only where a pixel of the pair is known: at sparse masks
+      // most 32-byte sectors of f are never fetched
+      const bool any = m.x || m.y;
       for (int c = 0; c < C; ++c) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(f + c * N) + j);
+        double2 v = make_double2(0.0, 0.0);
+        if (any) v = __ldg(reinterpret_cast<const double2*>(f + c * N) + j);
         T* dst = b + c * N + 2 * j;
         dst[0] = m.x ? static_cast<T>(v.x) : T(0);
         dst[1] = m.y ? static_cast<T>(v.y) : T(0);
