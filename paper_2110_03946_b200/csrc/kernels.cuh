@@ -629,3 +629,74 @@ __global__ void convert_kernel(const Tin* __restrict__ in, Tout* __restrict__ ou
 }
 
 }  // namespace sib
+
+namespace sib {
+
+// ---- device-driven outer iteration (CUDA graph with conditional nodes) ----
+// run_schwarz_level's host loop (schwarz.hpp:266-323) moved to the device:
+// level_decide_kernel evaluates the stopping test of one outer iteration
+// with the host's arithmetic (joint norm sqrt-then-fma, IEEE division) and
+// drives the WHILE / IF nodes that contain the next sweeps.
+struct LevelState {
+  double r0;         // canonical r0 (schwarz.hpp:333-345)
+  double final_rel;  // last relative residual
+  int outer;         // sweeps done
+  int iterations;    // report.iterations
+  int converged;
+  int pad;
+};
+
+__device__ __forceinline__ double joint_norm_dev(const double* s, int C) {
+  double joint = 0.0;
+  for (int k = 0; k < C; ++k) {
+    const double nrm = sqrt(s[k]);
+    joint = fma(nrm, nrm, joint);
+  }
+  return sqrt(joint);
+}
+
+// first: also takes r0 from r0sums and resets the level.  Sets hw (loop
+// continue) and, when set_i, hi (the second sweep of the body) to "sweep
+// again".
+__global__ void level_decide_kernel(const double* __restrict__ sums,
+                                    const double* __restrict__ r0sums, int C, double tol,
+                                    int max_outer, LevelState* st, cudaGraphConditionalHandle hw,
+                                    cudaGraphConditionalHandle hi, int first, int set_i) {
+  if (threadIdx.x != 0) return;
+  if (first) {
+    st->r0 = joint_norm_dev(r0sums, C);
+    st->outer = 0;
+    st->converged = 0;
+  }
+  const double r0 = st->r0;
+  const double rel = r0 > 0.0 ? joint_norm_dev(sums, C) / r0 : 0.0;
+  st->iterations = st->outer;
+  st->final_rel = rel;
+  unsigned cont = 0;
+  if (rel <= tol)
+    st->converged = 1;
+  else if (st->outer < max_outer) {
+    cont = 1;
+    st->outer += 1;
+  }
+  cudaGraphSetConditional(hw, cont);
+  if (set_i) cudaGraphSetConditional(hi, cont);
+}
+
+// After the loop the level's iterate is in u1 when the sweep count is odd:
+// move it to u0 so the next stage reads a fixed buffer.
+template <typename T>
+__global__ void parity_fixup_kernel(const LevelState* st, const T* __restrict__ u1,
+                                    T* __restrict__ u0, size_t n) {
+  if ((st->outer & 1) == 0) return;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    u0[i] = u1[i];
+}
+
+__global__ void copy_bytes_kernel(const unsigned long long* __restrict__ src,
+                                  unsigned long long* __restrict__ dst, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+}  // namespace sib

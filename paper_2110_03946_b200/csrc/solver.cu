@@ -123,6 +123,21 @@ struct PendingEvent {
 
 }  // namespace
 
+// A batch frame whose device-driven levels are queued but not yet read back.
+struct GraphCounts {
+  long long fixed, per_sweep;  // kernels per level-graph launch / per sweep
+};
+struct PendingFrame {
+  bool active = false;
+  int slot = 0, depth = 0, fixed_block = -1;
+  bool known_checked = false;
+  int graph_level[SI_MAX_LEVELS] = {};
+  GraphCounts counts[SI_MAX_LEVELS] = {};
+  long long blocks[SI_MAX_LEVELS] = {};
+  si_report* rep = nullptr;
+};
+constexpr int kFrameWords = SI_MAX_LEVELS * 4 + 4;  // LevelStates + counters
+
 struct si_ctx {
   int device = 0;
   cudaStream_t own_stream = nullptr;
@@ -159,6 +174,29 @@ struct si_ctx {
   std::unique_ptr<sib::CopyPool> pack_pool;
   void* pack_buf[2] = {nullptr, nullptr};
   size_t pack_cap[2] = {0, 0};
+  // device-driven outer iterations (batch entry): one cached CUDA graph per
+  // level geometry and buffer set, conditional WHILE/IF nodes around the sweeps
+  struct LevelGraph {
+    std::vector<uint64_t> key;
+    cudaGraphExec_t exec = nullptr;
+    long long fixed = 0, per_sweep = 0;  // kernels per launch / per sweep
+    unsigned long long stamp = 0;
+  };
+  std::vector<LevelGraph> graphs;
+  unsigned long long graph_clock = 0;
+  int graph_mode = 0;
+  si_report batch_scratch_report[2];            // batch frames without a caller report
+  int counters_fresh = 0;                       // host_cnt current (graph-mode frame)
+  cudaStream_t cap_stream[2] = {nullptr, nullptr};
+  DevBuf lvl_state, lvl_sums;
+  unsigned long long* host_state = nullptr;     // mapped: LevelState[SI_MAX_LEVELS]
+  unsigned long long* dev_state = nullptr;      // device alias of host_state
+  // batch pipelining: a graph-mode frame's outcome lands in frame_host[slot]
+  // and is read while the next frame is already queued
+  struct PendingFrame* defer_to = nullptr;
+  unsigned long long* frame_host[2] = {nullptr, nullptr};  // mapped
+  unsigned long long* frame_dev[2] = {nullptr, nullptr};
+  cudaEvent_t frame_done[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -641,6 +679,7 @@ __global__ void copy_u64_kernel(const unsigned long long* src, unsigned long lon
 }
 
 void begin_counters(Ctx& x) {
+  x.c.counters_fresh = 0;
   x.c.counters.ensure(sizeof(unsigned long long) * 8);
   ++x.c.launch_count;
   copy_u64_kernel<<<1, 32, 0, x.s>>>(x.c.counters.as<unsigned long long>(), nullptr, 8, true);
@@ -656,7 +695,9 @@ void publish_counters(Ctx& x, int n) {
 }
 
 void end_counters(Ctx& x, si_report* rep) {
-  publish_counters(x, 2);
+  // a graph-mode frame published them with its level states, nothing ran since
+  if (!x.c.counters_fresh) publish_counters(x, 2);
+  x.c.counters_fresh = 0;
   rep->local_failures += static_cast<long long>(x.c.host_cnt[0]);
   rep->local_cg_iterations += static_cast<long long>(x.c.host_cnt[1]);
 }
@@ -679,6 +720,207 @@ void ensure_red(si_ctx& c, int C) {
 void prepare_red(Ctx& x, int C) {
   x.c.red_out.ensure(sizeof(double) * 4 * C);
   ensure_red(x.c, C);
+}
+
+// Diagnostics as multilevel_solve writes them (multilevel.hpp:284-293).
+void write_diagnostic(si_report* rep, int depth, int fixed_block) {
+  bool coarse_capped = false;
+  for (int l = 1; l < depth; ++l) coarse_capped |= !rep->level_converged[l];
+  if (!rep->converged)
+    std::snprintf(rep->diagnostic, sizeof rep->diagnostic, "%s",
+                  fixed_block >= 0 ? "schwarz: outer iteration cap reached"
+                                   : "multilevel: finest level did not converge");
+  else if (coarse_capped)
+    std::snprintf(rep->diagnostic, sizeof rep->diagnostic, "%s",
+                  "multilevel: a coarse level hit its iteration cap");
+}
+
+// Completes a deferred batch frame: waits for its publish, fills the report
+// exactly as the synchronous path does.
+void finish_frame(si_ctx& c, PendingFrame& P) {
+  if (!P.active) return;
+  P.active = false;
+  CK(cudaEventSynchronize(c.frame_done[P.slot]));
+  const unsigned long long* w = c.frame_host[P.slot];
+  const unsigned long long* cnt = w + SI_MAX_LEVELS * 4;
+  if (!P.known_checked) check_arg(cnt[2] > 0, "build_rhs: mask has no known pixels");
+  si_report* rep = P.rep;
+  const LevelState* hs = reinterpret_cast<const LevelState*>(w);
+  for (int l = 0; l < P.depth; ++l) {
+    const LevelState& S = hs[l];
+    rep->level_iterations[l] = S.iterations;
+    rep->level_final_rel[l] = S.final_rel;
+    rep->level_converged[l] = S.converged != 0;
+    rep->local_solves += static_cast<long long>(S.outer) * P.blocks[l];
+    c.launch_count += P.counts[l].fixed + P.counts[l].per_sweep * S.outer;
+    if (l == 0) {
+      rep->iterations = S.iterations;
+      rep->final_relative_residual = S.final_rel;
+      rep->converged = S.converged != 0;
+    }
+  }
+  rep->local_failures += static_cast<long long>(cnt[0]);
+  rep->local_cg_iterations += static_cast<long long>(cnt[1]);
+  write_diagnostic(rep, P.depth, P.fixed_block);
+}
+
+// ---- device-driven level (graph mode) ---------------------------------------
+// Adds a conditional node at the capture point of stream s; returns its body.
+cudaGraph_t add_conditional(cudaStream_t s, cudaGraphConditionalHandle h,
+                            cudaGraphConditionalNodeType type) {
+  cudaStreamCaptureStatus st;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(s, &st, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams p{};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = type;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, g, deps, nd, &p));
+  CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+  return p.conditional.phGraph_out[0];
+}
+
+cudaGraph_t capturing_graph(cudaStream_t s) {
+  cudaStreamCaptureStatus st;
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamGetCaptureInfo(s, &st, nullptr, &g, nullptr, nullptr));
+  return g;
+}
+
+// Graph mode applies when nothing needs the host between outer iterations:
+// Schwarz levels without trace sink, reference image or kernel profiling,
+// K2 blocks, valid local options (validated up front; the host loop checks
+// them only before a sweep, so invalid ones take the host path).
+bool graph_eligible(const Ctx& x, const si_options& o, const Trace& tr, const double* d_ref,
+                    int flavour, int block) {
+  if (!x.c.graph_mode || tr.fn || d_ref || x.c.profiling || x.c.sweep_warp) return false;
+  if (flavour == kFlavourCg || block > kMaxBlock) return false;
+  return o.local_tolerance > 0.0 && o.local_max_iterations >= 0 && o.local_check_interval >= 1;
+}
+
+// One level's outer iteration as a cached graph:
+//   r0 residual, residual(u0), decide -> WHILE { sweep u0->u1, residual(u1),
+//   decide -> IF { sweep u1->u0, residual(u0), decide } }, parity fixup.
+// Launched on x.s without any host synchronisation; the LevelState slot
+// `level` holds the outcome.  Returns the cache entry (launch counts).
+template <typename T>
+GraphCounts launch_level_graph(Ctx& x, LevelView<T>& L, int C, int level, int block,
+                                             int overlap, double tol, int flavour,
+                                             const si_options& o) {
+  si_ctx& c = x.c;
+  LevelState* st = c.lvl_state.as<LevelState>() + level;
+  double* sums = c.lvl_sums.as<double>() + static_cast<size_t>(level) * 2 * C;
+  double* r0s = sums + C;
+  // every buffer the captured kernels touch must stay put: size the shared
+  // partials for this level first (launch_residual never grows it then)
+  const size_t parts = static_cast<size_t>((L.w + kResTmaThreads - 1) / kResTmaThreads + 1) *
+                       ((L.h + kResBand - 1) / kResBand + 1) * C;
+  c.red_partials.ensure(sizeof(double) * parts);
+  c.ticket.ensure(sizeof(unsigned int) * 4);
+  const double alpha = o.alpha;
+  uint64_t a_bits, t_bits, lt_bits;
+  std::memcpy(&a_bits, &alpha, 8);
+  std::memcpy(&t_bits, &tol, 8);
+  std::memcpy(&lt_bits, &o.local_tolerance, 8);
+  std::vector<uint64_t> key = {
+      sizeof(T), static_cast<uint64_t>(c.local_fp32), static_cast<uint64_t>(L.w),
+      static_cast<uint64_t>(L.h), static_cast<uint64_t>(C), static_cast<uint64_t>(level),
+      static_cast<uint64_t>(block), static_cast<uint64_t>(overlap),
+      static_cast<uint64_t>(flavour), a_bits, t_bits, lt_bits,
+      static_cast<uint64_t>(o.local_max_iterations), static_cast<uint64_t>(o.local_check_interval),
+      static_cast<uint64_t>(o.max_outer_iterations), static_cast<uint64_t>(o.normalizer),
+      reinterpret_cast<uint64_t>(L.mask), reinterpret_cast<uint64_t>(L.b),
+      reinterpret_cast<uint64_t>(L.u[0]), reinterpret_cast<uint64_t>(L.u[1]),
+      reinterpret_cast<uint64_t>(st), reinterpret_cast<uint64_t>(sums),
+      reinterpret_cast<uint64_t>(c.red_partials.ptr), reinterpret_cast<uint64_t>(c.ticket.ptr),
+      reinterpret_cast<uint64_t>(c.counters.ptr), static_cast<uint64_t>(tma_disabled()),
+      static_cast<uint64_t>(sizeof(T) == 8 ? c.sweep_nw64 : c.sweep_nw32)};
+  for (auto& g : c.graphs)
+    if (g.key == key) {
+      g.stamp = ++c.graph_clock;
+      CK(cudaGraphLaunch(g.exec, x.s));
+      return {g.fixed, g.per_sweep};
+    }
+  for (cudaStream_t& cs : c.cap_stream)
+    if (!cs) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  const LocalCfg lc{o.local_tolerance, o.local_max_iterations, o.local_check_interval};
+  const size_t n = static_cast<size_t>(L.w) * L.h * C;
+  const long long lc_before = c.launch_count;
+  unsigned long long* cnt = c.counters.as<unsigned long long>();
+  CK(cudaStreamBeginCapture(x.s, cudaStreamCaptureModeThreadLocal));
+  launch_residual<T>(x, L.mask, L.b, L.b, L.w, L.h, C, o.normalizer == 1 ? 1 : 0, r0s);
+  launch_residual<T>(x, L.mask, L.u[0], L.b, L.w, L.h, C, 0, sums, true);
+  cudaGraphConditionalHandle hw;
+  CK(cudaGraphConditionalHandleCreate(&hw, capturing_graph(x.s), 0, cudaGraphCondAssignDefault));
+  ++c.launch_count;
+  level_decide_kernel<<<1, 32, 0, x.s>>>(sums, r0s, C, tol, o.max_outer_iterations, st, hw, 0, 1,
+                                         0);
+  CK(cudaGetLastError());
+  const long long lc_loop = c.launch_count;
+  {
+    cudaGraph_t body = add_conditional(x.s, hw, cudaGraphCondTypeWhile);
+    Ctx xb{c, c.cap_stream[0]};
+    CK(cudaStreamBeginCaptureToGraph(xb.s, body, nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    cudaGraphConditionalHandle hi;
+    CK(cudaGraphConditionalHandleCreate(&hi, body, 0, 0));
+    launch_sweep<T>(xb, L.mask, L.b, L.u[0], L.u[1], L.w, L.h, C, block, overlap, flavour, alpha,
+                    lc, true, cnt);
+    launch_residual<T>(xb, L.mask, L.u[1], L.b, L.w, L.h, C, 0, sums, true);
+    ++c.launch_count;
+    level_decide_kernel<<<1, 32, 0, xb.s>>>(sums, r0s, C, tol, o.max_outer_iterations, st, hw,
+                                            hi, 0, 1);
+    CK(cudaGetLastError());
+    {
+      cudaGraph_t body2 = add_conditional(xb.s, hi, cudaGraphCondTypeIf);
+      Ctx xc{c, c.cap_stream[1]};
+      CK(cudaStreamBeginCaptureToGraph(xc.s, body2, nullptr, nullptr, 0,
+                                       cudaStreamCaptureModeThreadLocal));
+      launch_sweep<T>(xc, L.mask, L.b, L.u[1], L.u[0], L.w, L.h, C, block, overlap, flavour,
+                      alpha, lc, true, cnt);
+      launch_residual<T>(xc, L.mask, L.u[0], L.b, L.w, L.h, C, 0, sums, true);
+      ++c.launch_count;
+      level_decide_kernel<<<1, 32, 0, xc.s>>>(sums, r0s, C, tol, o.max_outer_iterations, st, hw,
+                                              0, 0, 0);
+      CK(cudaGetLastError());
+      cudaGraph_t tmp;
+      CK(cudaStreamEndCapture(xc.s, &tmp));
+    }
+    cudaGraph_t tmp;
+    CK(cudaStreamEndCapture(xb.s, &tmp));
+  }
+  const long long per_sweep = (c.launch_count - lc_loop) / 2;
+  ++c.launch_count;
+  parity_fixup_kernel<T><<<grid_for(n, 256, 148 * 8), 256, 0, x.s>>>(st, L.u[1], L.u[0], n);
+  CK(cudaGetLastError());
+  cudaGraph_t graph;
+  CK(cudaStreamEndCapture(x.s, &graph));
+  cudaGraphExec_t exec;
+  CK(cudaGraphInstantiate(&exec, graph, 0));
+  CK(cudaGraphDestroy(graph));
+  const long long captured = c.launch_count - lc_before;
+  c.launch_count = lc_before;  // counted when they run (finish_level_graphs)
+  if (c.graphs.size() >= 16) {
+    auto old = std::min_element(c.graphs.begin(), c.graphs.end(),
+                                [](const si_ctx::LevelGraph& a, const si_ctx::LevelGraph& b) {
+                                  return a.stamp < b.stamp;
+                                });
+    CK(cudaGraphExecDestroy(old->exec));
+    c.graphs.erase(old);
+  }
+  si_ctx::LevelGraph g;
+  g.key = std::move(key);
+  g.exec = exec;
+  g.per_sweep = per_sweep;
+  g.fixed = captured - 2 * per_sweep;
+  g.stamp = ++c.graph_clock;
+  c.graphs.push_back(std::move(g));
+  CK(cudaGraphLaunch(exec, x.s));
+  return {captured - 2 * per_sweep, per_sweep};
 }
 
 // multilevel_solve (multilevel.hpp:239-310) for the Schwarz level solvers.
@@ -927,6 +1169,14 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
     CK(cudaGetLastError());
   }
   bool known_checked = false;
+  // graph-mode levels: outcome read after the frame's single synchronisation
+  std::vector<int> graph_level(depth, 0);
+  std::vector<GraphCounts> graph_counts(depth, GraphCounts{0, 0});
+  std::vector<long long> graph_blocks(depth, 0);
+  if (x.c.graph_mode) {
+    x.c.lvl_state.ensure(sizeof(LevelState) * SI_MAX_LEVELS);
+    x.c.lvl_sums.ensure(sizeof(double) * 2 * C * SI_MAX_LEVELS);
+  }
   for (int level = depth - 1; level >= 0; --level) {
     LevelView<T>& V = L[level];
     const size_t n = static_cast<size_t>(V.w) * V.h;
@@ -944,7 +1194,8 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
     if (!cg_level && fixed_block < 0) cp = clamp_partition(V.w, V.h, o.block_size, o.overlap);
     if (flavour == SI_FLAVOUR_ORAS)
       check_arg(std::isfinite(o.alpha), "run_schwarz_level: alpha must be finite");
-    if (!known_checked) {
+    const bool by_graph = graph_eligible(x, o, tr, d_ref, flavour, cp.block);
+    if (!known_checked && !by_graph) {
       // build_rhs rejects an empty mask (operators.hpp:83): read the count
       // taken by the ingest kernel.
       publish_counters(x, 3);
@@ -958,7 +1209,14 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
       known_checked = true;
     }
     LevelOutcome oc;
-    if (cg_level) {
+    if (by_graph) {
+      graph_level[level] = 1;
+      graph_counts[level] = launch_level_graph<T>(x, V, C, level, cp.block, cp.overlap, tol,
+                                                  flavour, o);
+      graph_blocks[level] = static_cast<long long>(Axis::make(V.w, cp.block, cp.overlap).count) *
+                            Axis::make(V.h, cp.block, cp.overlap).count * C;
+      V.cur = 0;  // the parity fixup leaves the level's iterate in u[0]
+    } else if (cg_level) {
       oc = run_cg_level<T>(x, V, C, tol, o, finest, tr, finest ? d_ref : nullptr);
     } else {
       double r0 = 0.0;
@@ -983,16 +1241,69 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
       F.cur = 0;
     }
   }
-  // Diagnostics as multilevel_solve writes them (multilevel.hpp:284-293).
-  bool coarse_capped = false;
-  for (int l = 1; l < depth; ++l) coarse_capped |= !rep->level_converged[l];
-  if (!rep->converged)
-    std::snprintf(rep->diagnostic, sizeof rep->diagnostic, "%s",
-                  fixed_block >= 0 ? "schwarz: outer iteration cap reached"
-                                   : "multilevel: finest level did not converge");
-  else if (coarse_capped)
-    std::snprintf(rep->diagnostic, sizeof rep->diagnostic, "%s",
-                  "multilevel: a coarse level hit its iteration cap");
+  const int n_graph = static_cast<int>(std::count(graph_level.begin(), graph_level.end(), 1));
+  if (x.c.defer_to && n_graph == depth) {
+    // batch pipelining: level states + counters to this slot's mapped words,
+    // read by finish_frame once the next frame is queued
+    PendingFrame& P = *x.c.defer_to;
+    const int sl = P.slot;
+    if (!x.c.frame_host[sl]) {
+      CK(cudaHostAlloc(&x.c.frame_host[sl], sizeof(unsigned long long) * kFrameWords,
+                       cudaHostAllocMapped));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&x.c.frame_dev[sl]),
+                                  x.c.frame_host[sl], 0));
+      CK(cudaEventCreateWithFlags(&x.c.frame_done[sl], cudaEventDisableTiming));
+    }
+    const int words = static_cast<int>(sizeof(LevelState) / 8) * depth;
+    ++x.c.launch_count;
+    copy_bytes_kernel<<<1, 64, 0, x.s>>>(x.c.lvl_state.as<unsigned long long>(),
+                                         x.c.frame_dev[sl], words);
+    ++x.c.launch_count;
+    copy_bytes_kernel<<<1, 64, 0, x.s>>>(x.c.counters.as<unsigned long long>(),
+                                         x.c.frame_dev[sl] + SI_MAX_LEVELS * 4, 3);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(x.c.frame_done[sl], x.s));
+    P.active = true;
+    P.depth = depth;
+    P.fixed_block = fixed_block;
+    P.known_checked = known_checked;
+    P.rep = rep;
+    for (int l = 0; l < depth; ++l) {
+      P.graph_level[l] = 1;
+      P.counts[l] = graph_counts[l];
+      P.blocks[l] = graph_blocks[l];
+    }
+  } else if (n_graph > 0) {
+    // the frame's one synchronisation: level states and counters to the host
+    if (!x.c.host_state) {
+      CK(cudaHostAlloc(&x.c.host_state, sizeof(LevelState) * SI_MAX_LEVELS, cudaHostAllocMapped));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&x.c.dev_state), x.c.host_state, 0));
+    }
+    const int words = static_cast<int>(sizeof(LevelState) / 8) * depth;
+    ++x.c.launch_count;
+    copy_bytes_kernel<<<1, 64, 0, x.s>>>(x.c.lvl_state.as<unsigned long long>(), x.c.dev_state,
+                                         words);
+    CK(cudaGetLastError());
+    publish_counters(x, 3);
+    if (!known_checked) check_arg(x.c.host_cnt[2] > 0, "build_rhs: mask has no known pixels");
+    x.c.counters_fresh = 1;
+    const LevelState* hs = reinterpret_cast<const LevelState*>(x.c.host_state);
+    for (int l = 0; l < depth; ++l) {
+      if (!graph_level[l]) continue;
+      const LevelState& S = hs[l];
+      rep->level_iterations[l] = S.iterations;
+      rep->level_final_rel[l] = S.final_rel;
+      rep->level_converged[l] = S.converged != 0;
+      rep->local_solves += static_cast<long long>(S.outer) * graph_blocks[l];
+      x.c.launch_count += graph_counts[l].fixed + graph_counts[l].per_sweep * S.outer;
+      if (l == 0) {
+        rep->iterations = S.iterations;
+        rep->final_relative_residual = S.final_rel;
+        rep->converged = S.converged != 0;
+      }
+    }
+  }
+  if (!(x.c.defer_to && x.c.defer_to->active)) write_diagnostic(rep, depth, fixed_block);
   // Export the finest u (T -> double) unless it already lives in d_out.
   if (static_cast<const void*>(L[0].u[L[0].cur]) != static_cast<const void*>(d_out)) {
     Timed t(x, K_INGEST, static_cast<double>(n0) * C * (8.0 + sizeof(T)));
@@ -1071,7 +1382,16 @@ void run_device(si_ctx* ctx, int method, const double* d_f, const uint8_t* d_mas
   else
     multilevel_device<double>(x, levels_for(method, o), flavour_for(method), d_f, d_mask, w, h, c,
                               o, d_ref, d_out, rep, tr, -1, 0, ks);
-  end_counters(x, rep);
+  if (!(ctx->defer_to && ctx->defer_to->active)) end_counters(x, rep);
+}
+
+// SI_NO_GRAPHS=1: batch frames keep the host-driven outer iteration.
+bool graphs_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("SI_NO_GRAPHS");
+    return e && e[0] == '1';
+  }();
+  return off;
 }
 
 // SI_NO_KNOWN_PACK=1: always upload the full f (A/B measurements).
@@ -1182,6 +1502,13 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
   };
   std::vector<Pack> packs(n);
   const bool may_pack = !pnm && !known_pack_disabled();
+  // outer iterations decided on the device (cached level graphs): no host
+  // round trip per iteration while the result copies load the link
+  struct GraphMode {
+    si_ctx* c;
+    explicit GraphMode(si_ctx* ctx) : c(ctx) { c->graph_mode = !graphs_disabled(); }
+    ~GraphMode() { c->graph_mode = 0; }
+  } graph_mode_guard(ctx);
   if (may_pack && !ctx->pack_pool) ctx->pack_pool = std::make_unique<sib::CopyPool>(pack_threads());
   auto grow = [&](int s, size_t need, size_t keep) {
     if (ctx->pack_cap[s] >= need) return;
@@ -1235,20 +1562,44 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
     h2d(0);
     pack_async(1);
   }
+  // SI_BATCH_TRACE=1: per-frame host timeline and D2H durations on stderr
+  static const bool trace_on = [] {
+    const char* e = std::getenv("SI_BATCH_TRACE");
+    return e && e[0] == '1';
+  }();
+  std::vector<cudaEvent_t> tev;
+  std::vector<double> th;
+  const auto tb = Clock::now();
+  // graph-mode frames are read back one frame late: frame k is queued before
+  // frame k-1's outcome is waited for, so the device never idles on the host
+  PendingFrame pend[2];
+  std::vector<Clock::time_point> t_start(n);
+  struct DeferGuard {
+    si_ctx* c;
+    ~DeferGuard() { c->defer_to = nullptr; }
+  } defer_guard{ctx};
+  auto finish = [&](int j) {
+    PendingFrame& P = pend[j & 1];
+    if (!P.active) return;
+    finish_frame(*ctx, P);
+    P.rep->elapsed_ms = ms_since(t_start[j]);
+  };
   for (int k = 0; k < n; ++k) {
     const int s = k & 1;
+    if (trace_on) th.resize(3 * k + 3, 0.0), th[3 * k] = ms_since(tb);
     // the other slot's input was consumed by frame k-1 (solved synchronously)
     if (k + 1 < n) {
       if (may_pack) packing.get();
+      if (trace_on) th[3 * k + 1] = ms_since(tb);
       h2d(k + 1);
       pack_async(k + 2);
     }
     CK(cudaStreamWaitEvent(cs, ctx->ev_h2d[s], 0));
     if (k >= 2) CK(cudaStreamWaitEvent(cs, ctx->ev_d2h[s], 0));  // out slot free again
-    si_report local;
-    si_report* rep = reports ? &reports[k] : &local;
+    si_report* rep = reports ? &reports[k] : &ctx->batch_scratch_report[s];
     clear_report(rep);
     const auto t0 = Clock::now();
+    t_start[k] = t0;
     KnownSamples ks{};
     if (packs[k].sparse) {
       ks.tile_off = ctx->slot_f[s].as<uint32_t>();
@@ -1263,9 +1614,12 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
           ctx->slot_mask[s].as<uint8_t>());
       CK(cudaGetLastError());
     }
+    pend[s].slot = s;
+    ctx->defer_to = ctx->graph_mode ? &pend[s] : nullptr;
     run_device(ctx, method, ctx->slot_f[s].as<double>(), ctx->slot_mask[s].as<uint8_t>(), w, h, c,
                o, nullptr, ctx->slot_out[s].as<double>(), rep, nullptr, nullptr, cs, t0,
                packs[k].sparse ? &ks : nullptr);
+    ctx->defer_to = nullptr;
     if (pnm) {
       // write_pnm's quantise (pnm.hpp:82-85, 130-147)
       ++ctx->launch_count;
@@ -1278,8 +1632,38 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
     rep->d2h_bytes = static_cast<long long>(out_bytes);
     CK(cudaEventRecord(ctx->ev_solved[s], cs));
     CK(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_solved[s], 0));
-    CK(cudaMemcpyAsync(out[k], raw_out(s), out_bytes, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    if (trace_on) {
+      for (int j = 0; j < 3; ++j) {
+        tev.emplace_back();
+        CK(cudaEventCreate(&tev.back()));
+      }
+      CK(cudaEventRecord(tev[tev.size() - 3], cs));
+      CK(cudaEventRecord(tev[tev.size() - 2], ctx->d2h_stream));
+      th[3 * k + 2] = ms_since(tb);
+    }
+    if (!(trace_on && std::getenv("SI_BATCH_NO_D2H")))  // diagnostics only
+      CK(cudaMemcpyAsync(out[k], raw_out(s), out_bytes, cudaMemcpyDeviceToHost,
+                         ctx->d2h_stream));
     CK(cudaEventRecord(ctx->ev_d2h[s], ctx->d2h_stream));
+    if (trace_on) CK(cudaEventRecord(tev.back(), ctx->d2h_stream));
+    if (k >= 1) finish(k - 1);
+  }
+  if (n >= 1) finish(n - 1);
+  if (trace_on) {
+    CK(cudaDeviceSynchronize());
+    const size_t per = 3;
+    for (int k = 0; k < n; ++k) {
+      float solved = 0.f, d2h0 = 0.f, d2h1 = 0.f;
+      cudaEventElapsedTime(&solved, tev[0], tev[3 * k]);
+      cudaEventElapsedTime(&d2h0, tev[0], tev[3 * k + 1]);
+      cudaEventElapsedTime(&d2h1, tev[0], tev[3 * k + 2]);
+      std::fprintf(stderr, "frame %d host", k);
+      for (size_t j = 0; j < per && k * per + j < th.size(); ++j)
+        std::fprintf(stderr, " %.2f", th[k * per + j]);
+      std::fprintf(stderr, " | dev solved %.2f d2h %.2f..%.2f (%.2f ms)\n", solved, d2h0, d2h1,
+                   d2h1 - d2h0);
+    }
+    for (auto e : tev) cudaEventDestroy(e);
   }
   CK(cudaStreamSynchronize(ctx->d2h_stream));
   CK(cudaStreamSynchronize(ctx->h2d_stream));
@@ -1600,6 +1984,18 @@ void si_destroy(si_ctx* c) {
   c->vz.release();
   c->stager.reset();
   c->pack_pool.reset();
+  for (auto& g : c->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  c->graphs.clear();
+  for (cudaStream_t cs : c->cap_stream)
+    if (cs) cudaStreamDestroy(cs);
+  if (c->host_state) cudaFreeHost(c->host_state);
+  for (int k = 0; k < 2; ++k) {
+    if (c->frame_host[k]) cudaFreeHost(c->frame_host[k]);
+    if (c->frame_done[k]) cudaEventDestroy(c->frame_done[k]);
+  }
+  c->lvl_state.release();
+  c->lvl_sums.release();
   for (void* b : c->pack_buf)
     if (b) cudaFreeHost(b);
   for (auto& p : c->pending) {

@@ -398,6 +398,43 @@ def test_batch_known_sample_and_dense_frames(solver):
             assert b.report.h2d_bytes == w * h * c * 8 + w * h
 
 
+@pytest.mark.parametrize("method,kw", [
+    (si.Method.MultilevelOras, dict()),
+    (si.Method.MultilevelOras, dict(levels=4, tolerance=1e-6)),
+    (si.Method.MultilevelOras, dict(tolerance=1e-12, max_outer_iterations=3)),  # cap, odd
+    (si.Method.Oras, dict(tolerance=1e-4)),
+    (si.Method.Ras, dict(max_outer_iterations=0)),
+    (si.Method.MultilevelOras, dict(precision=si.Precision.FP32)),
+    (si.Method.MultilevelOras, dict(precision=si.Precision.MIXED, alpha=0.5, overlap=3)),
+    (si.Method.MultilevelOras, dict(normalizer=si.ResidualNormalizer.RhsNorm, levels=2)),
+    (si.Method.MultilevelCg, dict(levels=2)),   # host-driven CG levels in the batch
+])
+def test_batch_device_driven_levels_match_host_loop(solver, method, kw):
+    """The batch entry runs the outer iteration as cached CUDA graphs with
+    conditional nodes (decisions on the device); results and every report
+    field equal the host-driven loop of the device entry, bitwise."""
+    w, h, c = 230, 170, 3
+    frames = []
+    for k in range(4):
+        f = si.synthetic_test_image(w, h, c, 60 + k)
+        m = si.random_mask(w, h, 0.05, 70 + k)
+        frames.append((f, m))
+    o = si.RunOptions(**kw)
+    batch = solver.run_batch(method, frames + frames[:2], o)  # repeats hit the graph cache
+    for (f, m), b in zip(frames + frames[:2], batch):
+        want, rep = _device_solve(solver, method, f, m, o)
+        assert np.array_equal(b.image.data, want)
+        r = b.report
+        assert r.level_iterations == rep.level_iterations
+        assert r.level_final_rel == rep.level_final_rel
+        assert r.level_converged == rep.level_converged
+        assert (r.iterations, r.final_relative_residual, r.converged) == \
+            (rep.iterations, rep.final_relative_residual, rep.converged)
+        assert (r.local_solves, r.local_failures, r.local_cg_iterations) == \
+            (rep.local_solves, rep.local_failures, rep.local_cg_iterations)
+        assert r.diagnostic == rep.diagnostic
+
+
 def test_known_sample_upload_empty_mask_raises(solver):
     f = si.synthetic_test_image(400, 300, 1, 1)
     m = si.InpaintingMask(400, 300)
