@@ -373,7 +373,8 @@ def main():
                 "api": "si_run_method_batch (host f64 planar + u8 mask in, f64 out; pinned); "
                        "a frame crosses PCIe as its mask + the f values at known pixels "
                        "(the only ones the solver reads, multilevel.hpp:84-88), packed on "
-                       "host threads inside the timed region",
+                       "host threads inside the timed region; outer iterations decided on "
+                       "the device (cached CUDA graphs with conditional nodes)",
                 "frames": e2e_steps},
         "e2e_pnm": {"value": pnm_value, "unit": "frames/s",
                     "h2d_bytes_per_step": int(C4K * n + H4K * ((W4K + 7) // 8)),
