@@ -2023,6 +2023,9 @@ si_status si_trim(si_ctx* c) {
     check_arg(c != nullptr, "null context");
     set_device(c);
     CK(cudaStreamSynchronize(c->own_stream));
+    for (auto& g : c->graphs)
+      if (g.exec) CK(cudaGraphExecDestroy(g.exec));
+    c->graphs.clear();
     for (auto& l : c->levels) {
       l.mask.release();
       l.b.release();
