@@ -96,12 +96,22 @@ __device__ __forceinline__ T robin_diag(int gx, int gy, int lx, int ly, int B, i
   return T(deg) + am1 * T(cut);
 }
 
+// W/E stencil neighbours by warp shuffle for a double local CG (the staged
+// shared-memory row kept the L1 data pipe 73% busy: 3.135 -> 3.079 ms per
+// frame's sweeps); a float CG keeps the staged row (one 4-byte shuffle per
+// neighbour does not pay there: 437 -> 414 frames/s with shuffles).
+template <typename L>
+constexpr bool kShflWE = sizeof(L) == 8;
+
 // T: storage / outer-iteration type of the image, L: type of the local CG
 // (L = T, or float under double storage for the mixed-precision mode).
 template <typename T, int NW, typename L = T>
 struct SweepSmem {
   __align__(128) T ut[kTileH][tile_w<T>()];  // u_old tile with halo (TMA destination)
   uint64_t bar;                    // TMA completion
+  // float local CG: stencil operand rows with zero ghost columns 0 and B+1
+  // (double takes W/E by shuffle instead, see kShflWE)
+  L pt[sizeof(L) == 8 ? 1 : kMaxBlock][sizeof(L) == 8 ? 1 : kMaxBlock + 2];
   L bt[kMaxBlock][kMaxBlock];      // local right-hand side (true-residual checks)
   L pub[NW][2][3][32];             // [warp][top/bottom][r,p,x][col]
   L pubt[NW][2][32];               // true-residual boundary rows
@@ -427,6 +437,17 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
   for (int i = 0; i < R; ++i) {
     x[i] = L(0);
     S.bt[c.row0 + i][lane] = r[i];
+    if constexpr (!kShflWE<L>) S.pt[c.row0 + i][lane + 1] = r[i];  // p = r initially
+  }
+  if constexpr (!kShflWE<L>) {
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) S.pt[c.row0 + i][0] = L(0);
+    }
+    if (lane == B - 1 || (!FULL && lane == 31)) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) S.pt[c.row0 + i][B + 1] = L(0);
+    }
   }
   const int any_unknown = __syncthreads_or(unk != 0);
 #ifdef SI_PROBE_SETUP
@@ -491,18 +512,35 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
         }
       }
     };
+    // float: stage my rows of v as stencil operand (the warp owns whole rows,
+    // so a warp barrier suffices; the ghost columns stay zero)
+    auto stage = [&](const L(&v)[R]) {
+      if constexpr (!kShflWE<L>) {
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < R; ++i) S.pt[c.row0 + i][lane + 1] = v[i];
+        __syncwarp();
+      }
+    };
     // o = A v on my cells (LocalStencilOperator::apply, schwarz.hpp:146-159):
     // o = unk * (d*v - vW - vE - vN - vS); block-external neighbours are
-    // ghost zeros.  W/E come from the neighbouring lanes by shuffle (lane 0's
-    // W and lane 31's E are the ghost zeros; columns >= B of a partial block
-    // hold zeros), N/S from my registers or the neighbour warps' rows vN0/vS1.
+    // ghost zeros.  double: W/E come from the neighbouring lanes by shuffle
+    // (lane 0's W and lane 31's E are the ghost zeros; columns >= B of a
+    // partial block hold zeros); float: from the staged row.  N/S from my
+    // registers or the neighbour warps' rows vN0/vS1.
     auto apply = [&](const L(&v)[R], L vN0, L vS1, L(&o)[R]) {
 #pragma unroll
       for (int i = 0; i < R; ++i) {
-        const L sW = __shfl_up_sync(0xffffffffu, v[i], 1);
-        const L sE = __shfl_down_sync(0xffffffffu, v[i], 1);
-        const L vW = lane > 0 ? sW : L(0);
-        const L vE = lane < 31 ? sE : L(0);
+        L vW, vE;
+        if constexpr (kShflWE<L>) {
+          const L sW = __shfl_up_sync(0xffffffffu, v[i], 1);
+          const L sE = __shfl_down_sync(0xffffffffu, v[i], 1);
+          vW = lane > 0 ? sW : L(0);
+          vE = lane < 31 ? sE : L(0);
+        } else {
+          vW = S.pt[c.row0 + i][lane];
+          vE = S.pt[c.row0 + i][lane + 2];
+        }
         const L vN = i > 0 ? v[i - 1] : vN0;
         const L vS = i + 1 < R ? v[i + 1] : vS1;
         L d;
@@ -563,6 +601,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
         SI_PROBE_MARK(1);
         if (cadence || maybe_done) {
           // True residual b - A x, then confirm or replace (cg.hpp:131-146).
+          stage(x);
           // the neighbours' boundary rows of x were published before the rr
           // barrier of this iteration
           const L nx0 = (NW > 1 && warp > 0) ? S.pub[warp - 1][1][2][lane] : L(0);
@@ -593,6 +632,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
         const L beta = div_by_recip(rr_new, rr, rr_rcp);  // == rr_new / rr
 #pragma unroll
         for (int i = 0; i < R; ++i) p[i] = fmaT(beta, p[i], r[i]);
+        stage(p);
         nb_p[0] = fmaT(beta, nb_p[0], nb_r[0]);
         nb_p[1] = fmaT(beta, nb_p[1], nb_r[1]);
         rr = rr_new;
