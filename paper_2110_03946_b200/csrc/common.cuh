@@ -12,6 +12,16 @@ constexpr int kMaxBlock = 32;   // subdomain edge handled by the sweep kernel
 // needed on device.  partition_axis / owned_end (partition.hpp:46-63):
 // anchors k*(B-o), last block flush to the edge; block k owns pixels up to
 // the midpoint between its centre and the next block's centre (ties low).
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor in the
+// stream drains; pdl_wait() blocks until the predecessor grid has completed
+// and its memory is visible (a no-op for an ordinary launch), pdl_trigger()
+// lets this grid's dependents start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 struct Axis {
   int extent, block, stride, count;
 

@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(kResTmaThreads)
   const int ny = min(kResTmaBand, row1 - y0);
   const bool xin = x < W;
   const size_t Wz = static_cast<size_t>(W);
+  pdl_wait();  // u is the predecessor's output
   if (threadIdx.x == 0) {
 #ifdef SI_TMA_DEBUG
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
@@ -302,6 +303,7 @@ __global__ void __launch_bounds__(kResTmaThreads)
     partials[static_cast<size_t>(blockIdx.z) * gridDim.x * gridDim.y + blockIdx.y * gridDim.x +
              blockIdx.x] = t;
   }
+  pdl_trigger();
 }
 
 // Fixed-order sum of nblk partials per channel (grid: one CTA per channel).
@@ -309,6 +311,7 @@ __global__ void __launch_bounds__(kRedThreads)
     finish_partials_kernel(const double* __restrict__ partials, int nblk, double* out) {
   __shared__ double wsum[kRedThreads / 32];
   const int c = blockIdx.x;
+  pdl_wait();
   double s = 0.0;
   for (int i = threadIdx.x; i < nblk; i += kRedThreads) s += partials[static_cast<size_t>(c) * nblk + i];
   s = warp_sum(s);

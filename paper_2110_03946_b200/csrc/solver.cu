@@ -335,6 +335,32 @@ bool make_mask_map(CUtensorMap* m, const void* base, int W, int H, int box_w, in
              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Kernel launch with programmatic stream serialization (PDL, see pdl_wait in
+// common.cuh): the kernel must pdl_wait() before touching its predecessor's
+// data.  SI_NO_PDL=1 launches normally (the waits are then no-ops).
+bool pdl_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("SI_NO_PDL");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_disabled() ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 template <typename T>
 void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W, int H, int C,
                      int mode, double* out, bool known_invariant = true, int row0 = 0,
@@ -361,8 +387,8 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
     auto launch = [&](auto inv, auto mt) {
       constexpr bool INV = decltype(inv)::value, MT = decltype(mt)::value;
       ++x.c.launch_count;
-      residual_sumsq_tma_kernel<T, INV, MT><<<dim3(tx, gy, C), kResTmaThreads, 0, x.s>>>(
-          map, mmap, mask, b, W, H, N, row0, row1, x.c.red_partials.as<double>());
+      launch_pdl(residual_sumsq_tma_kernel<T, INV, MT>, dim3(tx, gy, C), kResTmaThreads, x.s,
+                 map, mmap, mask, b, W, H, N, row0, row1, x.c.red_partials.as<double>());
     };
     if (known_invariant) {
       if (mtma) launch(std::true_type{}, std::true_type{});
@@ -373,8 +399,8 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
     }
     CK(cudaGetLastError());
     ++x.c.launch_count;
-    finish_partials_kernel<<<C, kRedThreads, 0, x.s>>>(x.c.red_partials.as<double>(), tx * gy,
-                                                       out);
+    launch_pdl(finish_partials_kernel, dim3(C), kRedThreads, x.s,
+               static_cast<const double*>(x.c.red_partials.as<double>()), tx * gy, out);
   } else if (known_invariant) {
     ++x.c.launch_count;
     residual_sumsq_kernel<T, true><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(

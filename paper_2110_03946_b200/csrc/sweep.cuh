@@ -669,6 +669,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
     }
     if (own) un[pix] = uo + v;
   }
+  pdl_trigger();  // the residual of u_new may start launching
   if (tid == 0 && a.counters && any_unknown) {
     if (!converged) atomicAdd(&a.counters[0], 1ull);
     atomicAdd(&a.counters[1], static_cast<unsigned long long>(iters));
