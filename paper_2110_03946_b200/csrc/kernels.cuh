@@ -451,6 +451,7 @@ template <typename T, bool VEC>
 __global__ void restrict_kernel(const uint8_t* __restrict__ fmask, const T* __restrict__ fval,
                                 int fw, int fh, int C, int averaging, uint8_t* __restrict__ cmask,
                                 T* __restrict__ cval) {
+  pdl_wait();
   const int cw = (fw + 1) / 2, ch = (fh + 1) / 2;
   const size_t fn = static_cast<size_t>(fw) * fh, cn = static_cast<size_t>(cw) * ch;
   const int cx = blockIdx.x * blockDim.x + threadIdx.x, cy = blockIdx.y;
@@ -507,6 +508,7 @@ __global__ void __launch_bounds__(256, SI_PRO_OCC)
                         T* __restrict__ fine) {
   constexpr int kCh = 3;  // channels staged per pass
   __shared__ T tile[kCh][kProCY][kProCX];
+  pdl_wait();
   const size_t fn = static_cast<size_t>(fw) * fh, cn = static_cast<size_t>(cw) * ch;
   const int fx0 = blockIdx.x * kProX, fy0 = blockIdx.y * kProY;
   const int cx0 = fx0 / 2 - 1, cy0 = fy0 / 2 - 1;  // staged window origin
@@ -626,6 +628,7 @@ __global__ void quantise_kernel(const double* __restrict__ u, size_t N, int C,
 
 template <typename Tin, typename Tout>
 __global__ void convert_kernel(const Tin* __restrict__ in, Tout* __restrict__ out, size_t n) {
+  pdl_wait();
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
     out[i] = static_cast<Tout>(in[i]);

@@ -434,10 +434,12 @@ void launch_restrict(Ctx& x, const uint8_t* fmask, const T* fval, int fw, int fh
   const dim3 grid((cw + 127) / 128, ch);
   if (fw % 2 == 0 && reinterpret_cast<uintptr_t>(fval) % 16 == 0) {
     ++x.c.launch_count;
-    restrict_kernel<T, true><<<grid, 128, 0, x.s>>>(fmask, fval, fw, fh, C, averaging, cmask, cval);
+    launch_pdl(restrict_kernel<T, true>, grid, 128, x.s, fmask, fval, fw, fh, C, averaging, cmask,
+               cval);
   } else {
     ++x.c.launch_count;
-    restrict_kernel<T, false><<<grid, 128, 0, x.s>>>(fmask, fval, fw, fh, C, averaging, cmask, cval);
+    launch_pdl(restrict_kernel<T, false>, grid, 128, x.s, fmask, fval, fw, fh, C, averaging, cmask,
+               cval);
   }
   CK(cudaGetLastError());
 }
@@ -447,7 +449,7 @@ void launch_prolong(Ctx& x, const T* coarse, int cw, int ch, int fw, int fh, int
                     const uint8_t* fmask, const T* fval, T* fine) {
   const dim3 grid((fw + kProX - 1) / kProX, (fh + kProY - 1) / kProY);
   ++x.c.launch_count;
-  prolong_snap_kernel<T><<<grid, 256, 0, x.s>>>(coarse, cw, ch, fw, fh, C, fmask, fval, fine);
+  launch_pdl(prolong_snap_kernel<T>, grid, 256, x.s, coarse, cw, ch, fw, fh, C, fmask, fval, fine);
   CK(cudaGetLastError());
 }
 
@@ -1209,7 +1211,8 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
     if (level == depth - 1) {
       // canonical start u0 = b on the coarsest level (multilevel.hpp:267-273)
       ++x.c.launch_count;
-      convert_kernel<T, T><<<grid_for(n * C, 256, 148 * 16), 256, 0, x.s>>>(V.b, V.u[0], n * C);
+      launch_pdl(convert_kernel<T, T>, dim3(grid_for(n * C, 256, 148 * 16)), 256, x.s,
+                 static_cast<const T*>(V.b), V.u[0], n * C);
       CK(cudaGetLastError());
       V.cur = 0;
     }
