@@ -435,6 +435,33 @@ def test_batch_device_driven_levels_match_host_loop(solver, method, kw):
         assert r.diagnostic == rep.diagnostic
 
 
+@pytest.mark.parametrize("w,h,c", [(231, 171, 1), (97, 401, 5), (64, 33, 2)])
+def test_batch_device_driven_odd_shapes(solver, w, h, c):
+    """Odd widths (cooperative tile staging instead of TMA), many channels
+    and clamped coarse partitions through the graph-mode batch."""
+    frames = [(si.synthetic_test_image(w, h, c, 90 + k), si.random_mask(w, h, 0.06, 95 + k))
+              for k in range(3)]
+    o = si.RunOptions(levels=3)
+    batch = solver.run_batch(si.Method.MultilevelOras, frames, o)
+    for (f, m), b in zip(frames, batch):
+        want, rep = _device_solve(solver, si.Method.MultilevelOras, f, m, o)
+        assert np.array_equal(b.image.data, want)
+        assert b.report.level_iterations == rep.level_iterations
+        assert b.report.local_cg_iterations == rep.local_cg_iterations
+
+
+def test_batch_empty_mask_in_a_later_frame_raises(solver):
+    w, h = 300, 200
+    good = (si.synthetic_test_image(w, h, 3, 1), si.random_mask(w, h, 0.05, 2))
+    bad = (si.synthetic_test_image(w, h, 3, 3), si.InpaintingMask(w, h))
+    with pytest.raises(si.InvalidArgument, match="no known pixels"):
+        solver.run_batch(si.Method.MultilevelOras, [good, good, bad, good])
+    # the context stays usable
+    res = solver.run_batch(si.Method.MultilevelOras, [good])
+    want, _ = _device_solve(solver, si.Method.MultilevelOras, *good, si.RunOptions())
+    assert np.array_equal(res[0].image.data, want)
+
+
 def test_known_sample_upload_empty_mask_raises(solver):
     f = si.synthetic_test_image(400, 300, 1, 1)
     m = si.InpaintingMask(400, 300)
