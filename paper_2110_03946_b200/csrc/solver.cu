@@ -1539,6 +1539,17 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
     ~GraphMode() { c->graph_mode = 0; }
   } graph_mode_guard(ctx);
   if (may_pack && !ctx->pack_pool) ctx->pack_pool = std::make_unique<sib::CopyPool>(pack_threads());
+  // outgrown pack buffers are freed after the batch: cudaFreeHost may
+  // synchronise the device, which must not happen on the packing thread while
+  // the solving thread captures a level graph
+  std::vector<void*> retired;
+  std::mutex retired_m;
+  struct RetiredFree {
+    std::vector<void*>& v;
+    ~RetiredFree() {
+      for (void* p : v) cudaFreeHost(p);
+    }
+  } retired_free{retired};
   auto grow = [&](int s, size_t need, size_t keep) {
     if (ctx->pack_cap[s] >= need) return;
     void* nb = nullptr;
@@ -1546,7 +1557,8 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
     CK(cudaMallocHost(&nb, cap));
     if (ctx->pack_buf[s]) {
       std::memcpy(nb, ctx->pack_buf[s], keep);
-      CK(cudaFreeHost(ctx->pack_buf[s]));
+      std::lock_guard<std::mutex> g(retired_m);
+      retired.push_back(ctx->pack_buf[s]);
     }
     ctx->pack_buf[s] = nb;
     ctx->pack_cap[s] = cap;
