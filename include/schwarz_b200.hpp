@@ -20,6 +20,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "schwarz_b200.h"
@@ -206,6 +207,42 @@ inline SolveResult run_method(Method method, const ImageBuffer& f, const Inpaint
                                      res.image.data.data(), &rep, &detail::trace_sink,
                                      &res.trace));
   res.report = detail::to_report(rep);
+  return res;
+}
+
+// Many independent frames of one shape (the CLI's inpaint over a list of
+// files, main.cpp:101) through si_run_method_batch: each frame's upload and
+// the previous frame's result copy overlap the current solve, and the outer
+// iterations are decided on the device.  Same results as run_method per
+// frame; no trace rows (the batch entry has no trace sink).
+inline std::vector<SolveResult> run_batch(
+    Method method, const std::vector<std::pair<const ImageBuffer*, const InpaintingMask*>>& frames,
+    const RunOptions& options, Context& ctx = Context::thread_default()) {
+  std::vector<SolveResult> res(frames.size());
+  if (frames.empty()) return res;
+  const ImageBuffer& f0 = *frames[0].first;
+  std::vector<const double*> fp;
+  std::vector<const uint8_t*> mp;
+  std::vector<double*> op;
+  for (size_t k = 0; k < frames.size(); ++k) {
+    const ImageBuffer& f = *frames[k].first;
+    const InpaintingMask& m = *frames[k].second;
+    detail::check_arg(f.width == m.width && f.height == m.height,
+                      "image and mask dimensions differ");
+    detail::check_arg(f.width == f0.width && f.height == f0.height && f.channels == f0.channels,
+                      "run_batch: frames must share one shape");
+    res[k].image = ImageBuffer(f.width, f.height, f.channels);
+    fp.push_back(f.data.data());
+    mp.push_back(m.known.data());
+    op.push_back(res[k].image.data.data());
+  }
+  std::vector<si_report> reps(frames.size());
+  const si_options o = options.to_c();
+  detail::throw_status(si_run_method_batch(ctx.get(), static_cast<int>(method),
+                                           static_cast<int>(frames.size()), fp.data(), mp.data(),
+                                           f0.width, f0.height, f0.channels, &o, op.data(),
+                                           reps.data()));
+  for (size_t k = 0; k < frames.size(); ++k) res[k].report = detail::to_report(reps[k]);
   return res;
 }
 

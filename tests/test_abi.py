@@ -181,6 +181,9 @@ def test_cpp_wrapper_header_compiles(tmp_path):
                    '  auto (*dens)(const sb::ImageBuffer&, double, uint64_t, const sb::DensifyOptions&,\n'
                    '              sb::Context&) = &sb::voronoi_densify; (void)dens;\n'
                    '  auto (*asg)(const sb::InpaintingMask&, sb::Context&) = &sb::assign_nearest_site;\n'
+                   '  auto (*bat)(sb::Method, const std::vector<std::pair<const sb::ImageBuffer*,\n'
+                   '              const sb::InpaintingMask*>>&, const sb::RunOptions&,\n'
+                   '              sb::Context&) = &sb::run_batch; (void)bat;\n'
                    '  (void)asg; return 0; }\n')
     out = subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src),
                           L.lib_path(), "-o", str(tmp_path / "t"),

@@ -575,6 +575,10 @@ def test_cpp_dropin_header_on_device(tmp_path, solver):
         '  auto res = sb::voronoi_densify(g, 0.08, 17, d);\n'
         '  size_t k = 0; for (auto b : res.mask.known) k += b != 0;\n'
         '  std::printf("%d %d %zu\\n", res.sweeps, (int)res.reached_target, k);\n'
+        '  auto m2 = sb::random_mask(256, 256, 0.05, 12);\n'
+        '  auto b = sb::run_batch(sb::Method::MultilevelOras, {{&f, &m}, {&f, &m2}, {&f, &m}}, o);\n'
+        '  int same = b[0].image.data == r.image.data && b[2].image.data == r.image.data;\n'
+        '  std::printf("%d %d\\n", same, b[1].report.level_iterations[0]);\n'
         '  return 0; }\n')
     lib_dir = os.path.join(root, "paper_2110_03946_b200")
     exe = str(tmp_path / "t")
@@ -584,7 +588,12 @@ def test_cpp_dropin_header_on_device(tmp_path, solver):
     assert cc.returncode == 0, cc.stderr
     run = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert run.returncode == 0, run.stderr
-    l1, l2 = run.stdout.strip().splitlines()
+    l1, l2, l3 = run.stdout.strip().splitlines()
+    same, it_b1 = (int(v) for v in l3.split())
+    assert same == 1  # run_batch == run_method, bitwise
+    ref2 = solver.run_method(si.Method.MultilevelOras, si.synthetic_test_image(256, 256, 1, 7),
+                             si.random_mask(256, 256, 0.05, 12), si.RunOptions(levels=2))
+    assert it_b1 == ref2.report.level_iterations[0]
     it0, it1, checksum = l1.split()
     f = si.synthetic_test_image(256, 256, 1, 7)
     m = si.random_mask(256, 256, 0.05, 11)
