@@ -167,6 +167,7 @@ struct si_ctx {
   DevBuf slot_f[2], slot_mask[2], slot_out[2];
   VoronoiBufs vz;                               // densification
   std::unique_ptr<sib::Stager> stager;          // pageable host <-> device copies
+  std::unique_ptr<sib::Stager> drain_stager;    // batch: pageable result copies (helper thread)
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_solved[2] = {nullptr, nullptr},
               ev_d2h[2] = {nullptr, nullptr};
   // known-sample upload of the batch entry (host_copy.h): pinned packs
@@ -1580,6 +1581,9 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
   auto h2d = [&](int k) {
     const int s = k & 1;
     Pack& P = packs[k];
+    // slot s still feeds frame k-2 until its solve ends (frames are queued
+    // ahead of their completion in graph mode)
+    if (k >= 2) CK(cudaStreamWaitEvent(ctx->h2d_stream, ctx->ev_solved[s], 0));
     if (P.sparse) {
       const size_t bytes = off_bytes + P.K * c * sizeof(double);
       CK(cudaMemcpyAsync(raw_in(s), ctx->pack_buf[s], bytes, cudaMemcpyHostToDevice,
@@ -1615,6 +1619,8 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
   // frame k-1's outcome is waited for, so the device never idles on the host
   PendingFrame pend[2];
   std::vector<Clock::time_point> t_start(n);
+  // pageable result copies in flight (chained helper-thread jobs)
+  std::vector<std::shared_future<void>> drains(n);
   struct DeferGuard {
     si_ctx* c;
     ~DeferGuard() { c->defer_to = nullptr; }
@@ -1636,7 +1642,12 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
       pack_async(k + 2);
     }
     CK(cudaStreamWaitEvent(cs, ctx->ev_h2d[s], 0));
-    if (k >= 2) CK(cudaStreamWaitEvent(cs, ctx->ev_d2h[s], 0));  // out slot free again
+    if (k >= 2) {  // out slot free again
+      if (drains[k - 2].valid())
+        drains[k - 2].get();
+      else
+        CK(cudaStreamWaitEvent(cs, ctx->ev_d2h[s], 0));
+    }
     si_report* rep = reports ? &reports[k] : &ctx->batch_scratch_report[s];
     clear_report(rep);
     const auto t0 = Clock::now();
@@ -1682,14 +1693,34 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
       CK(cudaEventRecord(tev[tev.size() - 2], ctx->d2h_stream));
       th[3 * k + 2] = ms_since(tb);
     }
-    if (!(trace_on && std::getenv("SI_BATCH_NO_D2H")))  // diagnostics only
-      CK(cudaMemcpyAsync(out[k], raw_out(s), out_bytes, cudaMemcpyDeviceToHost,
-                         ctx->d2h_stream));
-    CK(cudaEventRecord(ctx->ev_d2h[s], ctx->d2h_stream));
+    if (out_bytes >= (size_t(1) << 20) && !sib::host_is_pinned(out[k])) {
+      // pageable result: a plain async copy would block this thread for the
+      // whole transfer; a helper thread drains it through pinned chunks
+      // (host_copy.h Stager) while the next frame is queued
+      if (!ctx->drain_stager)
+        ctx->drain_stager = std::make_unique<sib::Stager>([](cudaError_t e, const char* what) {
+          cuda_check(e, what);
+        });
+      std::shared_future<void> prev = k >= 1 ? drains[k - 1] : std::shared_future<void>();
+      void* dst = out[k];
+      const void* src = raw_out(s);
+      drains[k] = std::async(std::launch::async, [ctx, prev, dst, src, out_bytes, s] {
+                    if (prev.valid()) prev.wait();
+                    CK(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_solved[s], 0));
+                    ctx->drain_stager->d2h(dst, src, out_bytes, ctx->d2h_stream);
+                  }).share();
+    } else {
+      if (!(trace_on && std::getenv("SI_BATCH_NO_D2H")))  // diagnostics only
+        CK(cudaMemcpyAsync(out[k], raw_out(s), out_bytes, cudaMemcpyDeviceToHost,
+                           ctx->d2h_stream));
+      CK(cudaEventRecord(ctx->ev_d2h[s], ctx->d2h_stream));
+    }
     if (trace_on) CK(cudaEventRecord(tev.back(), ctx->d2h_stream));
     if (k >= 1) finish(k - 1);
   }
   if (n >= 1) finish(n - 1);
+  for (auto& d : drains)
+    if (d.valid()) d.get();
   if (trace_on) {
     CK(cudaDeviceSynchronize());
     const size_t per = 3;
@@ -2024,6 +2055,7 @@ void si_destroy(si_ctx* c) {
     b->release();
   c->vz.release();
   c->stager.reset();
+  c->drain_stager.reset();
   c->pack_pool.reset();
   for (auto& g : c->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
