@@ -450,6 +450,27 @@ def test_batch_device_driven_odd_shapes(solver, w, h, c):
         assert b.report.local_cg_iterations == rep.local_cg_iterations
 
 
+@pytest.mark.parametrize("pinned_out", [False, True])
+def test_batch_many_distinct_frames_no_slot_race(solver, pinned_out):
+    """16 distinct small frames (the queueing thread runs far ahead of the
+    device): every frame's inputs, outputs and report stay its own."""
+    import torch
+    w, h, c = 320, 200, 3
+    frames = [(si.synthetic_test_image(w, h, c, 200 + k), si.random_mask(w, h, 0.03 + 0.01 * (k % 5),
+                                                                         300 + k))
+              for k in range(16)]
+    outs = None
+    if pinned_out:
+        outs = [si.ImageBuffer(data=torch.empty((c, h, w), dtype=torch.float64).pin_memory().numpy())
+                for _ in frames]
+    o = si.RunOptions()
+    batch = solver.run_batch(si.Method.MultilevelOras, frames, o, outs)
+    for (f, m), b in zip(frames, batch):
+        want, rep = _device_solve(solver, si.Method.MultilevelOras, f, m, o)
+        assert np.array_equal(b.image.data, want)
+        assert b.report.level_iterations == rep.level_iterations
+
+
 def test_batch_empty_mask_in_a_later_frame_raises(solver):
     w, h = 300, 200
     good = (si.synthetic_test_image(w, h, 3, 1), si.random_mask(w, h, 0.05, 2))
