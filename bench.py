@@ -23,6 +23,7 @@ import json
 import os
 import statistics
 import sys
+import threading
 import time
 
 import numpy as np
@@ -42,6 +43,8 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--precision", default="fp64", choices=["fp64", "fp32", "mixed"])
     p.add_argument("--frames", type=int, default=2, help="distinct frames per rank")
+    p.add_argument("--inflight", type=int, default=2,
+                   help="frames in flight per rank (one context, stream and host thread each)")
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -219,16 +222,24 @@ def main():
         df = torch.from_numpy(f.data).to(f"cuda:{local}")
         dm = torch.from_numpy(m.known).to(f"cuda:{local}")
         dev.append((df, dm))
-    out = torch.empty((C4K, H4K, W4K), dtype=torch.float64, device=f"cuda:{local}")
+    # independent frames in flight: lane i has its own context, stream and
+    # output; lane 0 is the profiled/e2e solver on torch's current stream
+    inflight = max(1, args.inflight)
+    solvers = [solver] + [si.Solver(local) for _ in range(inflight - 1)]
+    streams = [stream] + [torch.cuda.Stream(device=local) for _ in range(inflight - 1)]
+    outs = [torch.empty((C4K, H4K, W4K), dtype=torch.float64, device=f"cuda:{local}")
+            for _ in range(inflight)]
 
-    def step(j):
+    def step(j, lane=0):
         df, dm = dev[j % len(dev)]
-        return solver.run_method_device(si.Method.MultilevelOras, df.data_ptr(), dm.data_ptr(),
-                                        W4K, H4K, C4K, out.data_ptr(), opts,
-                                        stream=stream.cuda_stream)
+        return solvers[lane].run_method_device(si.Method.MultilevelOras, df.data_ptr(),
+                                               dm.data_ptr(), W4K, H4K, C4K,
+                                               outs[lane].data_ptr(), opts,
+                                               stream=streams[lane].cuda_stream)
 
-    for j in range(max(args.warmup, 3)):
-        rep = step(j)
+    for lane in range(inflight):
+        for j in range(max(args.warmup, 3)):
+            rep = step(j, lane)
     torch.cuda.synchronize()
 
     def barrier():
@@ -246,24 +257,43 @@ def main():
     clocks = ClockSampler(local)
     # (no per-kernel events inside the timed region; they are collected in a
     # separate profiled pass below)
-    solver.set_profiling(False)
-    solver.kernel_stats(reset=True)
-    iters = []
+    for sv in solvers:
+        sv.set_profiling(False)
+        sv.kernel_stats(reset=True)
+    iters = [None] * args.steps
     barrier()
     torch.cuda.synchronize()
     clocks.start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for j in range(args.steps):
-        rep = step(j)
-        iters.append(tuple(rep.level_iterations))
+    for s in streams[1:]:
+        s.wait_event(ev0)
+
+    def run_lane(lane):
+        for j in range(lane, args.steps, inflight):
+            iters[j] = tuple(step(j, lane).level_iterations)
+
+    if inflight == 1:
+        run_lane(0)
+    else:  # ctypes releases the GIL: the lanes' host loops overlap
+        lanes = [threading.Thread(target=run_lane, args=(i,)) for i in range(inflight)]
+        for t in lanes:
+            t.start()
+        for t in lanes:
+            t.join()
+    for s in streams[1:]:
+        e = torch.cuda.Event()
+        e.record(s)
+        stream.wait_event(e)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
+    if any(x is None for x in iters):
+        raise RuntimeError("a frame lane failed inside the timed region")
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
-    launches = int(solver.kernel_stats(reset=True)["total_launches"])
+    launches = sum(int(sv.kernel_stats(reset=True)["total_launches"]) for sv in solvers)
 
     # ---- per-kernel device times (CUDA events on the launching stream) over
     # a separate pass of the same frames: the roofline numbers below
@@ -356,7 +386,7 @@ def main():
         "config": {"workload": "3840x2160 RGB, 4% random mask, 3-level ORAS, tol 1e-3 "
                                "(BASELINE configs[2]); per rank independent frames (configs[3])",
                    "block": 32, "overlap": 6, "alpha": 0.25, "levels": LEVELS,
-                   "frames_per_rank": len(dev), "seeds": "image 7+k, mask 11+k",
+                   "frames_per_rank": len(dev), "frames_in_flight": inflight, "seeds": "image 7+k, mask 11+k",
                    "l2": "inputs larger than L2 (199 MB f64 input, ~0.8 GB working set)"},
         "roofline": {"bound": "hbm", "kernel": "oras_sweep_kernel", "achieved": achieved,
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s",
