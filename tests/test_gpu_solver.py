@@ -647,6 +647,57 @@ def test_bitwise_deterministic_across_runs_and_contexts(solver, precision):
         assert a.report.local_cg_iterations == r.report.local_cg_iterations
 
 
+def test_concurrent_contexts_in_flight_match_sequential(solver):
+    """bench.py's frames-in-flight mode: independent contexts, each on its own
+    stream and host thread, solving device-resident frames at the same time
+    give the bit-identical images and reports of one-at-a-time solves."""
+    import threading
+
+    import torch
+    w, h, c = 640, 360, 3
+    frames = []
+    for k in range(4):
+        f = si.synthetic_test_image(w, h, c, 40 + k)
+        m = si.random_mask(w, h, 0.04, 50 + k)
+        frames.append((torch.from_numpy(f.data).cuda(), torch.from_numpy(m.known).cuda()))
+    o = si.RunOptions(levels=3)
+
+    def solve(sv, j, out, stream):
+        df, dm = frames[j]
+        rep = sv.run_method_device(si.Method.MultilevelOras, df.data_ptr(), dm.data_ptr(), w, h,
+                                   c, out.data_ptr(), o, stream=stream)
+        return rep
+
+    seq_out = [torch.empty((c, h, w), dtype=torch.float64, device="cuda") for _ in frames]
+    seq_rep = [solve(solver, j, seq_out[j], torch.cuda.current_stream().cuda_stream)
+               for j in range(len(frames))]
+    torch.cuda.synchronize()
+
+    lanes = [si.Solver(0), si.Solver(0)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    par_out = [torch.empty_like(x) for x in seq_out]
+    par_rep = [None] * len(frames)
+
+    def run(lane):
+        for _ in range(3):  # repeated so the lanes' kernels really overlap
+            for j in range(lane, len(frames), 2):
+                par_rep[j] = solve(lanes[lane], j, par_out[j], streams[lane].cuda_stream)
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    torch.cuda.synchronize()
+    for lane in lanes:
+        lane.close()
+    for j in range(len(frames)):
+        assert par_rep[j] is not None
+        assert torch.equal(seq_out[j], par_out[j])
+        assert par_rep[j].level_iterations == seq_rep[j].level_iterations
+        assert par_rep[j].final_relative_residual == seq_rep[j].final_relative_residual
+
+
 def test_many_channels(solver, oracle):
     """Channels are independent CTAs of one launch; the mapped scalar slots
     grow with the channel count (16 and 80 channels against the oracle)."""
