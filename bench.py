@@ -8,9 +8,12 @@ outer ORAS iterations to the reference's residual tolerance (1e-3 finest,
 reference's run_method(Method::MultilevelOras) with default RunOptions.
 
   value : frames/s with inputs resident in HBM (si_run_method_device),
-          CUDA events on the launching stream, max over ranks.
-  e2e   : frames/s through the public host API (si_run_method) from pinned
-          host buffers, H2D of f+mask and D2H of the result inside the timing.
+          --inflight independent frames at a time (default 2: one context,
+          stream and host thread each), CUDA events on the launching stream
+          bracketing every lane's stream, max over ranks.
+  e2e   : frames/s through the public host batch API (si_run_method_batch)
+          from pinned host buffers, H2D of each frame's inputs and D2H of its
+          result inside the timing.
 Multi-GPU (torchrun): independent frames per rank (configs[3]); no
 collective on the data path ("scaling": "weak").
 
