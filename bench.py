@@ -38,6 +38,37 @@ METRIC = "4K RGB inpaint frames/s at fixed residual tol; fraction of HBM rooflin
 W4K, H4K, C4K, DENSITY, LEVELS = 3840, 2160, 3, 0.04, 3
 
 
+# One config dict for both arms (the driver compares them verbatim).
+CONFIG = {"workload": "3840x2160 RGB, 4% random mask, 3-level ORAS, tol 1e-3 (BASELINE configs[2]); "
+                      "per rank independent frames (configs[3])",
+          "block": 32, "overlap": 6, "alpha": 0.25, "levels": LEVELS,
+          "seeds": "image 7+k, mask 11+k (frame k = rank*64 + j)",
+          "l2": "inputs larger than L2 (199 MB f64 input, ~0.8 GB working set)"}
+
+
+def level_sizes(w, h, levels):
+    """build_pyramid's level pixel counts (multilevel.hpp:90-93), finest first."""
+    out = [(w, h)]
+    while len(out) < levels and out[-1][0] >= 2 and out[-1][1] >= 2:
+        out.append(((out[-1][0] + 1) // 2, (out[-1][1] + 1) // 2))
+    return [a * b for a, b in out]
+
+
+def survey_frame_bytes(level_iters, w=W4K, h=H4K, c=C4K, s=8):
+    """Algorithmic HBM bytes of one frame by SURVEY.md §8d: per level k_L sweeps
+    ((2Cs+1) N_L each), k_L+1 residual checks and one r0 pass ((Cs+1) N_L
+    each), the restrictions (Cs+1)(N_L + N_{L+1}) and the prolongations plus
+    snap Cs N_{L+1} + (2Cs+1) N_L."""
+    n = level_sizes(w, h, len(level_iters))
+    tot = 0.0
+    for lvl, k in enumerate(level_iters):
+        tot += (k * (2 * c * s + 1) + (k + 2) * (c * s + 1)) * n[lvl]
+    for lvl in range(len(n) - 1):
+        tot += (c * s + 1) * (n[lvl] + n[lvl + 1])
+        tot += c * s * n[lvl + 1] + (2 * c * s + 1) * n[lvl]
+    return tot
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -73,7 +104,7 @@ class ClockSampler:
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, device: int, period_s: float = 0.02):
+    def __init__(self, device: int, period_s: float = 0.005):
         self.device = device
         self.period = period_s
         self.samples = []
@@ -132,7 +163,9 @@ def cpu_reference_run(frames, steps, warmup, budget_s):
     """Time the reference's own CPU run_method (oracle/_ref, all host threads);
     falls back to the single-threaded C restatement when _ref is absent."""
     from oracle import pyoracle as P
+    build = None
     if P.ref_available():
+        build = P.use_tuned_reference()
         lib = P.ref()
         lib.ref_set_threads(0)
         cores = int(lib.ref_thread_count())
@@ -158,7 +191,8 @@ def cpu_reference_run(frames, steps, warmup, budget_s):
             times.append(dt)
         if time.perf_counter() - t_start > budget_s and times:
             break
-    return {"times": times, "cores": cores, "kind": kind, "finest_iterations": iters}
+    return {"times": times, "cores": cores, "kind": kind, "finest_iterations": iters,
+            "build": build}
 
 
 def host_frames(n, rank=0):
@@ -172,10 +206,27 @@ def host_frames(n, rank=0):
     return out
 
 
+def ref_frames(n, rank=0):
+    """Reference-arm inputs from the reference's OWN generators
+    (synthetic.hpp:14-59, masks.hpp:25-43 in oracle/_ref/libref.so): the arm
+    never loads this repository's library."""
+    from oracle import pyoracle as P
+    out = []
+    for j in range(n):
+        sf, sm = frame_seeds(rank, j)
+        out.append((P.ref_synthetic_test_image(W4K, H4K, C4K, sf),
+                    P.ref_random_mask(W4K, H4K, DENSITY, sm)))
+    return out
+
+
 def run_reference_arm(args, world, rank):
+    """The reference's own CPU run_method (oracle/_ref/libref.so = the
+    unmodified headers, -O3 tuned for the box's CPU) on all host threads.
+    Rank 0 only; other ranks exit without work."""
     if rank != 0:
         return 0
-    frames = [(f.data, m.known) for f, m in host_frames(min(args.frames, 2))]
+    from oracle import pyoracle as P
+    frames = ref_frames(min(args.frames, 2))
     r = cpu_reference_run(frames, args.steps, args.warmup, budget_s=240.0)
     ms = 1e3 * sum(r["times"]) / len(r["times"])
     fps = 1e3 / ms
@@ -184,17 +235,50 @@ def run_reference_arm(args, world, rank):
         "n_gpus": args.gpus, "steps": len(r["times"]), "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "3840x2160 RGB, 4% random mask, 3-level ORAS, tol 1e-3",
-                   "seeds": "image 7+k, mask 11+k", "l2": "inputs larger than L2"},
+        "config": dict(CONFIG),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": r["cores"],
-                         "kind": r["kind"],
+                         "kind": r["kind"], "build": r.get("build"),
                          "sample": f"{len(r['times'])} full 4K RGB frames (run_method mloras)"},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "outer_iterations_finest": r["finest_iterations"],
     }
+    if r["kind"] == "reference" and not args.no_cpu_baseline:
+        # SURVEY.md §8d protocol: the same frame at 1 thread, and C5 (8K, 2%)
+        # on all threads, in the same run
+        lib = P.ref()
+        lib.ref_set_threads(1)
+        f, m = frames[0]
+        t0 = time.perf_counter()
+        P.ref_run_method("mloras", f, m, levels=LEVELS)
+        line["cpu_baseline_1thread"] = {"value": 1.0 / (time.perf_counter() - t0),
+                                        "unit": "frames/s", "cores": 1,
+                                        "sample": "1 full 4K RGB frame"}
+        lib.ref_set_threads(0)
+        f5 = P.ref_synthetic_test_image(7680, 4320, 3, 7)
+        m5 = P.ref_random_mask(7680, 4320, 0.02, 11)
+        t0 = time.perf_counter()
+        res5 = P.ref_run_method("mloras", f5, m5, levels=LEVELS)
+        line["c5_reference"] = {"ms_per_frame": 1e3 * (time.perf_counter() - t0),
+                                "cores": r["cores"], "finest_iterations": res5.iterations,
+                                "workload": "7680x4320 RGB, 2% mask, 3 levels (configs[4])"}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: re-launch this command as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1;
+    rank 0 prints the line, the exit code is the launcher's."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -203,6 +287,10 @@ def main():
     world, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference_arm(args, world, rank)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     import torch
     import paper_2110_03946_b200 as si
@@ -298,6 +386,18 @@ def main():
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     launches = sum(int(sv.kernel_stats(reset=True)["total_launches"]) for sv in solvers)
 
+    # ---- single-frame latency (one lane, nothing else in flight)
+    lat = []
+    for j in range(5):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(j)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        lat.append(e0.elapsed_time(e1))
+    latency_ms = statistics.median(lat)
+
     # ---- per-kernel device times (CUDA events on the launching stream) over
     # a separate pass of the same frames: the roofline numbers below
     prof_steps = min(args.steps, 4)
@@ -378,7 +478,8 @@ def main():
         except ValueError:
             pass
     total_dev = sum(v["device_ms"] for k, v in stats.items() if isinstance(v, dict))
-    frame_bytes = sum(v["algorithmic_bytes"] for k, v in stats.items() if isinstance(v, dict))
+    frame_bytes_survey = survey_frame_bytes(list(iters[-1]),
+                                            s=4 if prec == si.Precision.FP32 else 8)
 
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
@@ -386,17 +487,17 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": {si.Precision.FP64: "f64", si.Precision.FP32: "f32",
                   si.Precision.MIXED: "f64 (local CG f32)"}[prec], "data": "synthetic",
-        "config": {"workload": "3840x2160 RGB, 4% random mask, 3-level ORAS, tol 1e-3 "
-                               "(BASELINE configs[2]); per rank independent frames (configs[3])",
-                   "block": 32, "overlap": 6, "alpha": 0.25, "levels": LEVELS,
-                   "frames_per_rank": len(dev), "frames_in_flight": inflight, "seeds": "image 7+k, mask 11+k",
-                   "l2": "inputs larger than L2 (199 MB f64 input, ~0.8 GB working set)"},
+        "config": dict(CONFIG),
+        "lanes": {"frames_per_rank": len(dev), "frames_in_flight": inflight,
+                  "latency_ms_one_frame": latency_ms},
         "roofline": {"bound": "hbm", "kernel": "oras_sweep_kernel", "achieved": achieved,
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "traffic_launch": "finest-level sweep, ncu dram__bytes_read+write",
                      "traffic_algorithmic": traffic_alg,
-                     "frame_hbm_frac": (frame_bytes / prof_steps) / (ms_per_step / 1e3) / 1e9 / peak,
+                     "frame_hbm_frac": frame_bytes_survey / (ms_per_step / 1e3) / 1e9 / peak,
+                     "frame_bytes": frame_bytes_survey,
+                     "frame_bytes_formula": "SURVEY.md 8d per-frame formula with the measured k_L",
                      "sweep_share_of_step": sw["device_ms"] / max(total_dev, 1e-9),
                      "onchip_bound": {"pipe": "fp64", "pct_of_peak": fp64_pct,
                                       "source": "ncu --set full, first finest-level sweep"}},
@@ -427,7 +528,7 @@ def main():
                                   budget_s=20.0)
             ms = 1e3 * statistics.median(r["times"])
             line["cpu_baseline"] = {"value": 1e3 / ms, "unit": "frames/s", "cores": r["cores"],
-                                    "kind": r["kind"],
+                                    "kind": r["kind"], "build": r.get("build"),
                                     "sample": f"{len(r['times'])} full 4K RGB frame(s), median"}
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}

@@ -24,6 +24,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libref.so")
+REF_SPR_SO = os.path.join(HERE, "_ref", "libref_spr.so")   # -march=sapphirerapids
+_ref_path = REF_SO
 
 MAX_LEVELS = 32
 
@@ -129,13 +131,40 @@ def ref_available() -> bool:
     return os.path.exists(REF_SO)
 
 
+def _cpu_flags() -> set:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("flags"):
+                return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
+
+
+def use_tuned_reference() -> str:
+    """Select the reference build tuned for this host (the `-march=native`
+    of the benchmark protocol) when the CPU supports it; call
+    before the first ref().  Returns a description of the build in use."""
+    global _ref_path
+    if _ref is None and os.path.exists(REF_SPR_SO) and \
+            {"avx512f", "avx512_fp16", "amx_tile"} <= _cpu_flags():
+        _ref_path = REF_SPR_SO
+    return ref_build()
+
+
+def ref_build() -> str:
+    return ("g++ -std=c++20 -O3 " +
+            ("-march=sapphirerapids" if _ref_path == REF_SPR_SO else "-march=x86-64-v3") +
+            " -pthread (" + os.path.relpath(_ref_path, os.path.dirname(HERE)) + ")")
+
+
 def ref():
     """The compiled reference (raises if it was never built here)."""
     global _ref
     if _ref is None:
         if not ref_available():
             raise FileNotFoundError(REF_SO)
-        lib = C.CDLL(REF_SO)
+        lib = C.CDLL(_ref_path)
         lib.ref_last_error.restype = C.c_char_p
         lib.ref_synthetic_test_image.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, _f64]
         lib.ref_random_mask.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint64, _u8]
@@ -185,6 +214,7 @@ class Solve:
     local_failures: int = 0
     local_cg_iterations: int = 0
     elapsed_ms: float = 0.0
+    psnr: object = None               # per trace row (ref_run_method with a reference)
 
 
 def _flat(f: np.ndarray):
@@ -249,14 +279,17 @@ def ref_run_method(method: str, f: np.ndarray, mask: np.ndarray, reference=None,
     fr, ms = C.c_double(), C.c_double()
     cap = max(o.max_outer_iterations, 100000) + 2
     trace = np.zeros(cap)
+    psnr = np.full(cap, np.nan)
     refbuf = None if reference is None else _flat(reference)
     rc = ref().ref_run_method(METHODS[method], f.ravel(), m.ravel(), w, h, c, C.byref(o),
                               None if refbuf is None else refbuf.ctypes.data, out.ravel(),
                               C.byref(it), C.byref(fr), C.byref(conv), trace.ctypes.data,
-                              None, None, cap, C.byref(rows), C.byref(ms))
+                              None, psnr.ctypes.data, cap, C.byref(rows), C.byref(ms))
     if rc != 0:
         raise ValueError(ref().ref_last_error().decode())
-    s = Solve(out, it.value, fr.value, bool(conv.value), trace[: min(rows.value, cap)].copy())
+    n = min(rows.value, cap)
+    s = Solve(out, it.value, fr.value, bool(conv.value), trace[:n].copy())
+    s.psnr = psnr[:n].copy()  # metrics.hpp:30-56 per trace row (NaN without a reference)
     s.elapsed_ms = ms.value
     return s
 

@@ -447,6 +447,10 @@ class Solver:
             if (f.width, f.height, f.channels) != (f0.width, f0.height, f0.channels):
                 raise InvalidArgument("run_batch: frames must share one shape")
         outs = outputs or [_result_buffer(f0.width, f0.height, f0.channels) for _ in range(n)]
+        # the C ABI receives raw pointers: every output must be a full,
+        # C-contiguous float64 (c, h, w) buffer (no NULL, no short list)
+        _require_outputs([o.data for o in outs], n, (f0.channels, f0.height, f0.width),
+                         np.float64, "run_batch")
         fp = (C.c_void_p * n)(*[f.data.ctypes.data for f, _ in frames])
         mp = (C.c_void_p * n)(*[m.known.ctypes.data for _, m in frames])
         op = (C.c_void_p * n)(*[o.data.ctypes.data for o in outs])
@@ -475,6 +479,7 @@ class Solver:
             if p_.shape != px0.shape or m_.shape != (h, (w + 7) // 8):
                 raise InvalidArgument("run_pnm_batch: frames must share one shape")
         outs = outputs or [np.empty_like(ins[0]) for _ in range(n)]
+        _require_outputs(outs, n, px0.shape, np.uint8, "run_pnm_batch")
         ip = (C.c_void_p * n)(*[a.ctypes.data for a in ins])
         mp = (C.c_void_p * n)(*[a.ctypes.data for a in masks])
         op = (C.c_void_p * n)(*[a.ctypes.data for a in outs])
@@ -681,6 +686,18 @@ def voronoi_densify(f: ImageBuffer, target_density: float, seed: int,
 
 def assign_nearest_site(mask: InpaintingMask) -> VoronoiAssignment:
     return default_solver().assign_nearest_site(mask)
+
+
+def _require_outputs(outs, n: int, shape, dtype, who: str):
+    """Caller-supplied batch outputs: exactly n C-contiguous arrays of the
+    frame's shape and dtype (the library writes through raw pointers)."""
+    if len(outs) != n:
+        raise InvalidArgument(f"{who}: expected {n} outputs, got {len(outs)}")
+    for k, a in enumerate(outs):
+        if not isinstance(a, np.ndarray) or a.dtype != dtype or tuple(a.shape) != tuple(shape) \
+                or not a.flags.c_contiguous or not a.flags.writeable:
+            raise InvalidArgument(f"{who}: output {k} must be a writeable C-contiguous "
+                                  f"{np.dtype(dtype).name} array of shape {tuple(shape)}")
 
 
 def _require_same_grid(f: ImageBuffer, mask: InpaintingMask):

@@ -28,7 +28,6 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "sweep.cuh"
-#include "sweep_warp.cuh"
 #include "sweep_generic.cuh"
 #include "cg_level.cuh"
 #include "densify.cuh"
@@ -160,7 +159,6 @@ struct si_ctx {
   si_kernel_stats stats{};
   int sweep_nw64 = 2, sweep_nw32 = 2;           // warps per sweep CTA (measured best)
   long long launch_count = 0;                   // kernels launched (always counted)
-  int sweep_warp = 0;                           // 1: full blocks on the one-warp variant
   int local_fp32 = 0;                           // MIXED precision: float local CG (set per call)
   // batch pipeline: two staging slots, one stream per copy direction
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
@@ -473,13 +471,7 @@ void launch_sweep_nw(Ctx& x, const SweepArgs<T>& a, int nblocks, int C) {
       return;
     }
   }
-  if (a.ax.block == kMaxBlock && x.c.sweep_warp) {
-    x.c.scratch.ensure(sizeof(T) * kMaxBlock * kMaxBlock * static_cast<size_t>(nblocks) * C);
-    SweepArgs<T> aw = a;
-    aw.scratch = x.c.scratch.as<T>();
-    ++x.c.launch_count;
-    oras_sweep_warp_kernel<T><<<dim3(nblocks, C), 32, 0, x.s>>>(aw);
-  } else if (a.ax.block == kMaxBlock) {
+  if (a.ax.block == kMaxBlock) {
     ++x.c.launch_count;
     oras_sweep_kernel<T, NW, true><<<dim3(nblocks, C), NW * 32, 0, x.s>>>(a);
   } else {
@@ -826,7 +818,7 @@ cudaGraph_t capturing_graph(cudaStream_t s) {
 // them only before a sweep, so invalid ones take the host path).
 bool graph_eligible(const Ctx& x, const si_options& o, const Trace& tr, const double* d_ref,
                     int flavour, int block) {
-  if (!x.c.graph_mode || tr.fn || d_ref || x.c.profiling || x.c.sweep_warp) return false;
+  if (!x.c.graph_mode || tr.fn || d_ref || x.c.profiling) return false;
   if (flavour == kFlavourCg || block > kMaxBlock) return false;
   return o.local_tolerance > 0.0 && o.local_max_iterations >= 0 && o.local_check_interval >= 1;
 }
@@ -1607,14 +1599,6 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
     h2d(0);
     pack_async(1);
   }
-  // SI_BATCH_TRACE=1: per-frame host timeline and D2H durations on stderr
-  static const bool trace_on = [] {
-    const char* e = std::getenv("SI_BATCH_TRACE");
-    return e && e[0] == '1';
-  }();
-  std::vector<cudaEvent_t> tev;
-  std::vector<double> th;
-  const auto tb = Clock::now();
   // graph-mode frames are read back one frame late: frame k is queued before
   // frame k-1's outcome is waited for, so the device never idles on the host
   PendingFrame pend[2];
@@ -1625,6 +1609,27 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
     si_ctx* c;
     ~DeferGuard() { c->defer_to = nullptr; }
   } defer_guard{ctx};
+  // An error part way through (e.g. an empty mask found by finish_frame)
+  // unwinds through here: wait for the packing and drain helpers and the
+  // three streams, so no copy into a caller buffer is still in flight when
+  // the status is returned.
+  struct Unwind {
+    si_ctx* c;
+    cudaStream_t cs;
+    std::future<void>& packing;
+    std::vector<std::shared_future<void>>& drains;
+    bool armed = true;
+    ~Unwind() {
+      if (!armed) return;
+      if (packing.valid()) packing.wait();
+      for (auto& d : drains)
+        if (d.valid()) d.wait();
+      cudaStreamSynchronize(c->d2h_stream);
+      cudaStreamSynchronize(c->h2d_stream);
+      cudaStreamSynchronize(cs);
+      cudaGetLastError();
+    }
+  } unwind{ctx, cs, packing, drains};
   auto finish = [&](int j) {
     PendingFrame& P = pend[j & 1];
     if (!P.active) return;
@@ -1633,11 +1638,9 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
   };
   for (int k = 0; k < n; ++k) {
     const int s = k & 1;
-    if (trace_on) th.resize(3 * k + 3, 0.0), th[3 * k] = ms_since(tb);
     // the other slot's input was consumed by frame k-1 (solved synchronously)
     if (k + 1 < n) {
       if (may_pack) packing.get();
-      if (trace_on) th[3 * k + 1] = ms_since(tb);
       h2d(k + 1);
       pack_async(k + 2);
     }
@@ -1684,15 +1687,6 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
     rep->d2h_bytes = static_cast<long long>(out_bytes);
     CK(cudaEventRecord(ctx->ev_solved[s], cs));
     CK(cudaStreamWaitEvent(ctx->d2h_stream, ctx->ev_solved[s], 0));
-    if (trace_on) {
-      for (int j = 0; j < 3; ++j) {
-        tev.emplace_back();
-        CK(cudaEventCreate(&tev.back()));
-      }
-      CK(cudaEventRecord(tev[tev.size() - 3], cs));
-      CK(cudaEventRecord(tev[tev.size() - 2], ctx->d2h_stream));
-      th[3 * k + 2] = ms_since(tb);
-    }
     if (out_bytes >= (size_t(1) << 20) && !sib::host_is_pinned(out[k])) {
       // pageable result: a plain async copy would block this thread for the
       // whole transfer; a helper thread drains it through pinned chunks
@@ -1710,33 +1704,16 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
                     ctx->drain_stager->d2h(dst, src, out_bytes, ctx->d2h_stream);
                   }).share();
     } else {
-      if (!(trace_on && std::getenv("SI_BATCH_NO_D2H")))  // diagnostics only
-        CK(cudaMemcpyAsync(out[k], raw_out(s), out_bytes, cudaMemcpyDeviceToHost,
-                           ctx->d2h_stream));
+      CK(cudaMemcpyAsync(out[k], raw_out(s), out_bytes, cudaMemcpyDeviceToHost,
+                         ctx->d2h_stream));
       CK(cudaEventRecord(ctx->ev_d2h[s], ctx->d2h_stream));
     }
-    if (trace_on) CK(cudaEventRecord(tev.back(), ctx->d2h_stream));
     if (k >= 1) finish(k - 1);
   }
   if (n >= 1) finish(n - 1);
   for (auto& d : drains)
     if (d.valid()) d.get();
-  if (trace_on) {
-    CK(cudaDeviceSynchronize());
-    const size_t per = 3;
-    for (int k = 0; k < n; ++k) {
-      float solved = 0.f, d2h0 = 0.f, d2h1 = 0.f;
-      cudaEventElapsedTime(&solved, tev[0], tev[3 * k]);
-      cudaEventElapsedTime(&d2h0, tev[0], tev[3 * k + 1]);
-      cudaEventElapsedTime(&d2h1, tev[0], tev[3 * k + 2]);
-      std::fprintf(stderr, "frame %d host", k);
-      for (size_t j = 0; j < per && k * per + j < th.size(); ++j)
-        std::fprintf(stderr, " %.2f", th[k * per + j]);
-      std::fprintf(stderr, " | dev solved %.2f d2h %.2f..%.2f (%.2f ms)\n", solved, d2h0, d2h1,
-                   d2h1 - d2h0);
-    }
-    for (auto e : tev) cudaEventDestroy(e);
-  }
+  unwind.armed = false;
   CK(cudaStreamSynchronize(ctx->d2h_stream));
   CK(cudaStreamSynchronize(ctx->h2d_stream));
   CK(cudaStreamSynchronize(cs));
@@ -2030,7 +2007,6 @@ si_status si_create(int device, si_ctx** out) {
       CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dev_cnt), c->host_cnt, 0));
       if (const char* e = std::getenv("SI_SWEEP_WARPS64")) c->sweep_nw64 = std::atoi(e);
       if (const char* e = std::getenv("SI_SWEEP_WARPS32")) c->sweep_nw32 = std::atoi(e);
-      if (const char* e = std::getenv("SI_SWEEP_WARP")) c->sweep_warp = std::atoi(e);
     } catch (...) {
       si_destroy(c);
       throw;

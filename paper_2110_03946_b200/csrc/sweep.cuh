@@ -76,7 +76,7 @@ struct SweepArgs {
                        // known pixels (so r = 0 there); b is never read
   unsigned long long* counters;  // [0] failures, [1] CG iterations (may be null)
   int by0;             // first block row of this launch (stripe mode; 0 otherwise)
-  T* scratch;          // one-warp variant: 32x32 rhs tile per (block, channel)
+  T* scratch;          // K2g (blocks > 32): per-CTA CG vectors in global memory
 };
 
 template <typename T>

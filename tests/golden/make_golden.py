@@ -8,11 +8,16 @@ the reference's own outputs on seeded inputs from its own generators:
   c1.npz        256x256 grey, 5%, 2 levels: full output, trace, level counts
   c2.npz/c3.npz 1080p / 4K RGB: trace, level counts, local-solve statistics,
                 per-channel sums and 4096 sampled output pixels
+  c4k{1,2,3}.npz  4K RGB frames k = 1..3 of BASELINE configs[3] (seeds 7+k, 11+k)
+  c5.npz        8K RGB, 2%, 3 levels (BASELINE configs[4]); same fields
+  c5f.npz       C5 forced-sweep variant (tolerance 1e-12, max_outer_iterations 2)
+  psnr.npz      run_method with a reference image: per-row rel and PSNR
+                (metrics.hpp:30-56, multilevel.hpp:252-261)
   small.npz     12 small instances over the option space, full outputs
   kernels.npz   restriction / prolongation / local-operator probes
   densify.npz   assign_nearest_site / voronoi_densify (masks.hpp) outputs
 
-Usage: python tests/golden/make_golden.py [--only densify]
+Usage: python tests/golden/make_golden.py [--only densify|psnr|big|c5|c5f|c4k1 ...]
 """
 import hashlib
 import json
@@ -32,6 +37,24 @@ CONFIGS = {
     "c2": dict(w=1920, h=1080, c=3, d=0.04, levels=2),
     "c3": dict(w=3840, h=2160, c=3, d=0.04, levels=3),
 }
+
+# Headline-scale fixtures added in round 2: seeds (7+k, 11+k)
+BIG = {
+    "c4k1": dict(w=3840, h=2160, c=3, d=0.04, k=1, opts=dict(levels=3)),
+    "c4k2": dict(w=3840, h=2160, c=3, d=0.04, k=2, opts=dict(levels=3)),
+    "c4k3": dict(w=3840, h=2160, c=3, d=0.04, k=3, opts=dict(levels=3)),
+    "c5": dict(w=7680, h=4320, c=3, d=0.02, k=0, opts=dict(levels=3)),
+    "c5f": dict(w=7680, h=4320, c=3, d=0.02, k=0,
+                opts=dict(levels=3, tolerance=1e-12, max_outer_iterations=2)),
+}
+
+# run_method(..., reference) trace rows with PSNR: (w, h, c, d, seed_img, seed_mask, method, opts)
+PSNR_CASES = [
+    (256, 256, 1, 0.05, 7, 11, "mloras", dict(levels=2)),
+    (320, 240, 3, 0.04, 21, 22, "mloras", dict(levels=3, tolerance=1e-5)),
+    (200, 120, 3, 0.06, 23, 24, "oras", dict(tolerance=1e-4)),
+    (160, 96, 2, 0.08, 25, 26, "mlcg", dict(levels=2, flavour=2)),
+]
 
 SMALL = [
     # w, h, c, density, seed, options
@@ -107,13 +130,70 @@ def instance(w, h, c, d, seed_img, seed_mask):
     return P.ref_synthetic_test_image(w, h, c, seed_img), P.ref_random_mask(w, h, d, seed_mask)
 
 
+def big_fixtures(names=None):
+    """Headline-size fixtures: counts, trace, local statistics, sums, samples."""
+    hashes = {}
+    for name, cfg in BIG.items():
+        if names and name not in names:
+            continue
+        k = cfg["k"]
+        f, m = instance(cfg["w"], cfg["h"], cfg["c"], cfg["d"], 7 + k, 11 + k)
+        run = P.ref_run_method("mloras", f, m, **cfg["opts"])
+        lv = P.ref_solve_levels(f, m, **cfg["opts"])
+        assert np.array_equal(run.image, lv.image) and np.array_equal(run.trace, lv.trace)
+        rng = np.random.default_rng(1234)
+        idx = rng.choice(f.size, size=4096, replace=False)
+        np.savez_compressed(
+            os.path.join(HERE, f"{name}.npz"), trace=run.trace,
+            level_iterations=np.array(lv.level_iterations), iterations=run.iterations,
+            final_rel=run.final_rel, converged=run.converged, local_solves=lv.local_solves,
+            local_failures=lv.local_failures, channel_sum=run.image.sum(axis=(1, 2)),
+            channel_sumsq=(run.image ** 2).sum(axis=(1, 2)), sample_index=idx,
+            sample_value=run.image.reshape(-1)[idx])
+        hashes[name] = {"image": sha(f), "mask": sha(m), "w": cfg["w"], "h": cfg["h"],
+                        "c": cfg["c"], "d": cfg["d"], "seed_image": 7 + k, "seed_mask": 11 + k,
+                        "options": cfg["opts"]}
+        print(name, lv.level_iterations, run.trace, flush=True)
+    return hashes
+
+
+def psnr_fixtures():
+    out = {}
+    for i, (w, h, c, d, si_, sm_, meth, opts) in enumerate(PSNR_CASES):
+        f, m = instance(w, h, c, d, si_, sm_)
+        run = P.ref_run_method(meth, f, m, reference=f, **opts)
+        assert np.isfinite(run.psnr).all()
+        out[f"case{i}_trace"] = run.trace
+        out[f"case{i}_psnr"] = run.psnr
+        out[f"case{i}_image"] = run.image
+    np.savez_compressed(os.path.join(HERE, "psnr.npz"), **out)
+    print("psnr fixtures:", [len(out[f"case{i}_psnr"]) for i in range(len(PSNR_CASES))])
+
+
+def merge_hashes(extra):
+    path = os.path.join(HERE, "inputs.json")
+    cur = json.load(open(path)) if os.path.exists(path) else {}
+    cur.update(extra)
+    with open(path, "w") as fh:
+        json.dump(cur, fh, indent=1, sort_keys=True)
+
+
 def main():
     if not P.ref_available():
         sys.exit("oracle/_ref/libref.so missing: run `make -C oracle` where /root/reference exists")
     P.ref().ref_set_threads(0)
-    if "--only" in sys.argv and "densify" in sys.argv:
-        densify_fixtures()
+    if "--only" in sys.argv:
+        what = sys.argv[sys.argv.index("--only") + 1:]
+        if "densify" in what:
+            densify_fixtures()
+        if "psnr" in what:
+            psnr_fixtures()
+        big = [w for w in what if w in BIG] or (list(BIG) if "big" in what else [])
+        if big:
+            merge_hashes(big_fixtures(big))
         return
+    densify_fixtures()
+    psnr_fixtures()
     densify_fixtures()
     hashes = {}
     for name, cfg in CONFIGS.items():
@@ -182,8 +262,8 @@ def main():
     k["localop_mask"], k["localop_in"], k["localop_out"] = m, v, out
     np.savez_compressed(os.path.join(HERE, "kernels.npz"), **k)
 
-    with open(os.path.join(HERE, "inputs.json"), "w") as fh:
-        json.dump(hashes, fh, indent=1, sort_keys=True)
+    hashes.update(big_fixtures())
+    merge_hashes(hashes)
     print("wrote fixtures to", HERE)
 
 

@@ -192,3 +192,23 @@ def test_cpp_wrapper_header_compiles(tmp_path):
     assert out.returncode == 0, out.stderr
     run = subprocess.run([str(tmp_path / "t")], capture_output=True, text=True)
     assert run.returncode == 0, run.stderr
+
+
+def test_batch_outputs_are_validated_before_the_abi():
+    """run_batch / run_pnm_batch hand raw pointers to the library: a short
+    list, a wrong shape/dtype or a non-contiguous view must raise first."""
+    from paper_2110_03946_b200.api import _require_outputs
+    good = [np.empty((3, 4, 5)) for _ in range(2)]
+    _require_outputs(good, 2, (3, 4, 5), np.float64, "run_batch")
+    with pytest.raises(si.InvalidArgument):
+        _require_outputs(good[:1], 2, (3, 4, 5), np.float64, "run_batch")
+    with pytest.raises(si.InvalidArgument):
+        _require_outputs([good[0], np.empty((3, 4, 4))], 2, (3, 4, 5), np.float64, "run_batch")
+    with pytest.raises(si.InvalidArgument):
+        _require_outputs([good[0], np.empty((3, 4, 5), np.float32)], 2, (3, 4, 5), np.float64,
+                         "run_batch")
+    with pytest.raises(si.InvalidArgument):
+        _require_outputs([good[0], np.empty((3, 4, 10))[:, :, ::2]], 2, (3, 4, 5), np.float64,
+                         "run_batch")
+    with pytest.raises(si.InvalidArgument):
+        _require_outputs([np.empty((4, 5, 3), np.uint8)], 1, (4, 5, 3), np.float64, "run_pnm_batch")
