@@ -46,6 +46,16 @@ CONFIG = {"workload": "3840x2160 RGB, 4% random mask, 3-level ORAS, tol 1e-3 (BA
           "l2": "inputs larger than L2 (199 MB f64 input, ~0.8 GB working set)"}
 
 
+def hbm_peak():
+    """(GB/s, source): MEASURED_PEAKS.json (driver-measured copy bandwidth),
+    else the B200_PROFILING.md fallback."""
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(peaks["hbm_gbs"]), "measured"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback"
+
+
 def level_sizes(w, h, levels):
     """build_pyramid's level pixel counts (multilevel.hpp:90-93), finest first."""
     out = [(w, h)]
@@ -81,6 +91,7 @@ def parse():
                    help="frames in flight per rank (one context, stream and host thread each)")
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-c5", action="store_true", help="skip the configs[4] stripe leg")
     return p.parse_args()
 
 
@@ -264,6 +275,81 @@ def run_reference_arm(args, world, rank):
                                 "workload": "7680x4320 RGB, 2% mask, 3 levels (configs[4])"}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def c5_leg(args, world, rank, local, dist, solver):
+    """BASELINE configs[4]: ONE 7680x4320 RGB frame (2% mask, 3 levels)
+    striped over the `world` ranks (si_run_method_striped_device: each rank
+    holds, ingests, restricts, sweeps and prolongs only its rows; NCCL
+    all-gathers of the partial norms and halo rows between neighbours).
+    Device-resident, CUDA events on the solve stream, max over ranks; plus
+    the forced-sweep variant (tolerance 1e-12, max_outer 2) and a bit-identity
+    check of the assembled image against the single-GPU run_method."""
+    import hashlib
+    import torch
+    import paper_2110_03946_b200 as si
+    from paper_2110_03946_b200 import stripes as S
+    w, h, c = 7680, 4320, 3
+    f = si.synthetic_test_image(w, h, c, 7)
+    m = si.random_mask(w, h, 0.02, 11)
+    comm = S.nccl_comm(solver, dist) if dist is not None else S.local_comms([solver])[0]
+    dev = f"cuda:{local}"
+    stream = torch.cuda.current_stream()
+    out = {"workload": "7680x4320 RGB, 2% random mask, 3-level ORAS (BASELINE configs[4]), "
+                       "one frame striped over n_gpus ranks", "comm": comm.kind}
+    for name, o in (("tol", si.RunOptions(levels=LEVELS)),
+                    ("forced", si.RunOptions(levels=LEVELS, tolerance=1e-12,
+                                             max_outer_iterations=2))):
+        pl = S.level_plan(si.Method.MultilevelOras, w, h, c, o, world, rank)[0]
+        df = torch.from_numpy(np.ascontiguousarray(f.data[:, pl.store_lo:pl.store_hi])).to(dev)
+        dm = torch.from_numpy(np.ascontiguousarray(m.known[pl.store_lo:pl.store_hi])).to(dev)
+        do = torch.empty((c, pl.own_hi - pl.own_lo, w), dtype=torch.float64, device=dev)
+
+        def run():
+            return S.run_method_striped_device(solver, comm, si.Method.MultilevelOras,
+                                               df.data_ptr(), dm.data_ptr(), w, h, c,
+                                               do.data_ptr(), o, stream=stream.cuda_stream)
+        for _ in range(max(args.warmup, 3)):
+            rep = run()
+        steps = max(3, min(args.steps, 20))
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            rep = run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        if dist is not None:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        # bit identity against the single-GPU solve (hash of each rank's rows)
+        mine = hashlib.sha256(do.cpu().numpy().tobytes()).hexdigest()
+        spans = [(pl.own_lo, pl.own_hi)]
+        if dist is not None:
+            got = [None] * world
+            dist.all_gather_object(got, (mine, pl.own_lo, pl.own_hi))
+        else:
+            got = [(mine, pl.own_lo, pl.own_hi)]
+        same = None
+        if rank == 0:
+            ref = solver.run_method(si.Method.MultilevelOras, f, m, o)
+            same = all(hashlib.sha256(np.ascontiguousarray(ref.image.data[:, a:b]).tobytes())
+                       .hexdigest() == hx for hx, a, b in got)
+            same = same and list(rep.level_iterations) == list(ref.report.level_iterations)
+        n_px = w * h
+        out[name] = {"ms_per_frame": ms, "frames_per_s": 1e3 / ms, "steps": steps,
+                     "level_iterations": list(rep.level_iterations),
+                     "bit_identical_to_1gpu": same,
+                     "store_rows_rank0": [pl.store_lo, pl.store_hi],
+                     "hbm_frac_rank_avg": survey_frame_bytes(list(rep.level_iterations), w, h, c)
+                     / world / (ms / 1e3) / 1e9 / hbm_peak()[0]}
+        del df, dm, do
+    comm.close()
+    return out
 
 
 def spawn_ranks(n):
@@ -460,13 +546,7 @@ def main():
 
     # ---- roofline of the dominant kernel (K2 sweep)
     sw = stats["sweep"]
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except (OSError, ValueError):
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    peak, peak_src = hbm_peak()
     achieved = (sw["algorithmic_bytes"] / (sw["device_ms"] / 1e3) / 1e9) if sw["device_ms"] else 0.0
     traffic, traffic_alg, fp64_pct = None, None, None
     tfile = os.path.join(ROOT, "profiles", "sweep_dram_traffic.json")
@@ -521,6 +601,9 @@ def main():
         "kernel_ms_per_step": {k: v["device_ms"] / prof_steps for k, v in stats.items()
                                if isinstance(v, dict) and v["launches"]},
     }
+
+    if not args.no_c5:
+        line["c5"] = c5_leg(args, world, rank, local, dist, solver)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

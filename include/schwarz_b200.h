@@ -202,47 +202,56 @@ si_status si_local_operator_apply(si_ctx* ctx, const uint8_t* mask, int w, int h
                                   int overlap, int index, int flavour, double alpha,
                                   const double* v, double* out);
 
-/* ---- device building blocks for distributed (stripe) solves ---------------
- * One very large image split into horizontal stripes across ranks
- * (SURVEY.md §8e): every rank keeps full-size buffers but only computes its
- * stripe; the caller moves halo rows and all-reduces the partial norms.
- * All image pointers are DEVICE memory of ctx's device in the planar layout;
- * `precision` selects the element type of b/u/values buffers (si_precision:
- * double or float); d_f is always double.  Work runs on `stream` (NULL = the
- * context's own) and is complete when the call returns. */
+/* ---- one image over G ranks: horizontal stripes (BASELINE configs[4]) ----
+ * multilevel_solve (multilevel.hpp:239-310) with every pyramid level split
+ * into G stripes of whole block rows of that level's own partition
+ * (partition_domain, partition.hpp:46-106).  Each rank allocates, ingests,
+ * restricts, sweeps and prolongs only its rows (plus halos); per outer
+ * iteration the G x C partial residual sums are all-gathered (every rank
+ * takes run_schwarz_level's stop decision, schwarz.hpp:288-300, in the same
+ * fixed rank order) and halo rows move between neighbours.  The image equals
+ * the single-GPU solve's bit for bit whenever the stop decisions agree.
+ * Schwarz methods only (ras, oras, mloras); CG methods -> SI_ERR_UNSUPPORTED.
+ *
+ * A communicator joins the ranks: NCCL (one process per GPU; rank 0 makes
+ * the id with si_nccl_unique_id and the caller broadcasts its 128 bytes) or
+ * local (G ranks as host threads of one process, possibly on one device). */
+typedef struct si_stripe_comm si_stripe_comm;
+#define SI_NCCL_ID_BYTES 128
+si_status si_nccl_unique_id(unsigned char* id /* SI_NCCL_ID_BYTES */);
+si_status si_stripe_comm_init_nccl(si_ctx* ctx, int world, int rank, const unsigned char* id,
+                                   si_stripe_comm** out);
+/* comms_out[r] for r < world, rank r driven on ctxs[r] (one host thread each). */
+si_status si_stripe_comm_init_local(si_ctx* const* ctxs, int world, si_stripe_comm** comms_out);
+void si_stripe_comm_destroy(si_stripe_comm* comm);
 
-/* level 0: b = f at known pixels, 0 elsewhere (multilevel.hpp:84-88); *known
- * receives the known-pixel count. */
-si_status si_device_ingest(si_ctx* ctx, const double* d_f, const uint8_t* d_mask, int w, int h,
-                           int c, int precision, void* d_b, long long* known, void* stream);
-/* restrict_level (multilevel.hpp:33-70) on device buffers. */
-si_status si_device_restrict(si_ctx* ctx, const uint8_t* d_mask, const void* d_values, int w, int h,
-                             int c, int averaging, int precision, uint8_t* d_cmask,
-                             void* d_cvalues, void* stream);
-/* prolongate + snap (multilevel.hpp:101-128, 294-303): full fine image. */
-si_status si_device_prolong_snap(si_ctx* ctx, const void* d_coarse, int cw, int ch, int fw, int fh,
-                                 int c, const uint8_t* d_fmask, const void* d_fvalues,
-                                 int precision, void* d_fine, void* stream);
-/* per-channel sum of (b - A u)^2 over rows [row0, row1) (mode 0), or of b^2
- * (mode 1, RhsNorm); sums: host array of c doubles.  known_invariant: 1 when
- * u == b at known pixels and b == 0 at unknown ones (the multilevel flow). */
-si_status si_device_residual_rows(si_ctx* ctx, const uint8_t* d_mask, const void* d_u,
-                                  const void* d_b, int w, int h, int c, int row0, int row1,
-                                  int mode, int known_invariant, int precision, double* sums,
-                                  void* stream);
-/* One ORAS/RAS sweep restricted to block rows [by0, by1) of
- * partition_domain(w, h, block, overlap): u_new is written on the owned
- * rectangles of those blocks only.  Counters may be NULL. */
-si_status si_device_sweep_rows(si_ctx* ctx, const uint8_t* d_mask, const void* d_b,
-                               const void* d_u_old, void* d_u_new, int w, int h, int c,
-                               int block_size, int overlap, int by0, int by1, int flavour,
-                               const si_options* opt, int known_invariant, long long* failures,
-                               long long* cg_iterations, void* stream);
-/* Stripe geometry of one level for `rank` of `world` (host only).  out[8]:
- * blocks_y, k0, k1 (block rows), own_lo, own_hi (pixel rows this rank owns),
- * win_lo, win_hi (rows it must hold: sweep windows + residual stencil),
- * valid (1 when every halo row is owned by rank-1 or rank+1). */
-si_status si_stripe_plan(int h, int block_size, int overlap, int world, int rank, int* out);
+/* Rows of every level for `rank` (host only, no device): out receives
+ * SI_STRIPE_PLAN_INTS ints per level (index 0 = finest): k0, k1 (block rows),
+ * own_lo, own_hi (rows it owns), win_lo, win_hi (rows its sweeps read),
+ * need_lo, need_hi (coarse rows its prolongation reads), store_lo, store_hi
+ * (rows it holds), block, overlap (clamped partition).  *depth = levels. */
+#define SI_STRIPE_PLAN_INTS 12
+si_status si_stripe_level_plan(int method, int w, int h, int c, const si_options* opt, int world,
+                               int rank, int* depth, int* out /* SI_MAX_LEVELS*12 */);
+
+/* run_method over the ranks of `comm` (collective: every rank calls it).
+ * f / mask: the full HOST image (only this rank's level-0 store rows are
+ * uploaded); out: full-size host buffer, this rank writes its own finest
+ * rows.  Every rank's report carries the global counts. */
+si_status si_run_method_striped(si_ctx* ctx, si_stripe_comm* comm, int method, const double* f,
+                                const uint8_t* mask, int w, int h, int c, const si_options* opt,
+                                double* out, si_report* report, si_trace_fn trace, void* user);
+/* Device-resident: d_f_rows / d_mask_rows hold level-0 rows [store_lo,
+ * store_hi) (compact planar), d_out_rows receives rows [own_lo, own_hi). */
+si_status si_run_method_striped_device(si_ctx* ctx, si_stripe_comm* comm, int method,
+                                       const double* d_f_rows, const uint8_t* d_mask_rows, int w,
+                                       int h, int c, const si_options* opt, double* d_out_rows,
+                                       si_report* report, void* stream);
+/* Convenience: `world` ranks as threads of this process on ctxs[] over a
+ * local communicator; out receives the whole image; reports: NULL or world. */
+si_status si_run_method_striped_group(si_ctx* const* ctxs, int world, int method, const double* f,
+                                      const uint8_t* mask, int w, int h, int c,
+                                      const si_options* opt, double* out, si_report* reports);
 
 /* ---- host-only helpers (no device needed) -------------------------------- */
 

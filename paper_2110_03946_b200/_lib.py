@@ -12,6 +12,8 @@ import threading
 from . import build as _build
 
 MAX_LEVELS = 32
+SI_MAX_LEVELS = MAX_LEVELS
+SI_NCCL_ID_BYTES = 128
 
 SI_OK = 0
 SI_ERR_INVALID_ARGUMENT = 1
@@ -118,14 +120,17 @@ SIGNATURES = {
     "si_restrict_level": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
     "si_prolongate": (_i, [_vp, _vp, _i, _i, _i, _i, _vp]),
     "si_local_operator_apply": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _i, _d, _vp, _vp]),
-    "si_device_ingest": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _llp, _vp]),
-    "si_device_restrict": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp]),
-    "si_device_prolong_snap": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _i, _vp, _vp]),
-    "si_device_residual_rows": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _dp,
-                                     _vp]),
-    "si_device_sweep_rows": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i,
-                                  C.POINTER(si_options), _i, _llp, _llp, _vp]),
-    "si_stripe_plan": (_i, [_i, _i, _i, _i, _i, _ip]),
+    "si_nccl_unique_id": (_i, [_vp]),
+    "si_stripe_comm_init_nccl": (_i, [_vp, _i, _i, _vp, C.POINTER(_vp)]),
+    "si_stripe_comm_init_local": (_i, [C.POINTER(_vp), _i, C.POINTER(_vp)]),
+    "si_stripe_comm_destroy": (None, [_vp]),
+    "si_stripe_level_plan": (_i, [_i, _i, _i, _i, C.POINTER(si_options), _i, _i, _ip, _ip]),
+    "si_run_method_striped": (_i, [_vp, _vp, _i, _vp, _vp, _i, _i, _i, C.POINTER(si_options),
+                                   _vp, C.POINTER(si_report), TRACE_FN, _vp]),
+    "si_run_method_striped_device": (_i, [_vp, _vp, _i, _vp, _vp, _i, _i, _i,
+                                          C.POINTER(si_options), _vp, C.POINTER(si_report), _vp]),
+    "si_run_method_striped_group": (_i, [C.POINTER(_vp), _i, _i, _vp, _vp, _i, _i, _i,
+                                         C.POINTER(si_options), _vp, C.POINTER(si_report)]),
     "si_partition_domain": (_i, [_i, _i, _i, _i, _ip, _ip, _ip, _i]),
     "si_pack_known_samples": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _llp]),
     "si_synthetic_test_image": (_i, [_i, _i, _i, C.c_uint64, _vp]),

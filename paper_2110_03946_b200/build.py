@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libschwarz_b200.so")
 
 SOURCES = ["solver.cu", "generators.cpp"]
-HEADERS = ["common.cuh", "kernels.cuh", "sweep.cuh", "sweep_generic.cuh", "cg_level.cuh", "densify.cuh", "tma.cuh", "host_copy.h"]
+HEADERS = ["common.cuh", "kernels.cuh", "sweep.cuh", "stripes.cuh", "sweep_generic.cuh", "cg_level.cuh", "densify.cuh", "tma.cuh", "host_copy.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -93,9 +93,11 @@ template <typename T, bool INV>
 __global__ void __launch_bounds__(kRedThreads)
     residual_sumsq_kernel(const uint8_t* __restrict__ mask, const T* __restrict__ u,
                           const T* __restrict__ b, int W, int H, size_t N, int mode, int row0,
-                          int row1, double* partials, double* out, unsigned int* ticket) {
+                          int row1, int srow_lo, int srow_hi, double* partials, double* out,
+                          unsigned int* ticket) {
   // rows [row0, row1) only (stripe mode); the stencil still sees rows
-  // row0-1 and row1 as neighbours.
+  // row0-1 and row1 as neighbours.  The buffers hold rows [srow_lo, srow_hi)
+  // (pointers pre-offset, N = storage plane); whole image: 0 and H.
   __shared__ T tile[kResBand + 2][kResTileW];
   const int c = blockIdx.z;
   const T* __restrict__ uc = u + c * N;
@@ -106,6 +108,8 @@ __global__ void __launch_bounds__(kRedThreads)
   const int ny = min(kResBand, row1 - y0);
   const bool xin = x < W;
   const size_t Wz = static_cast<size_t>(W);
+  // inactive lanes address row0 (stored under stripe storage too)
+  const T* ustored = uc + static_cast<size_t>(row0) * Wz;
   double acc = 0.0;
   if (mode == 1) {
     T v[kResBand];
@@ -126,8 +130,8 @@ __global__ void __launch_bounds__(kRedThreads)
 #pragma unroll
     for (int k = 0; k < kResBand + 2; ++k) {
       const int gy = y0 - 1 + k;
-      const bool ok = k < nrows && gy >= 0 && gy < H && xin;
-      cp_async_zfill(&tile[k][threadIdx.x + 1], ok ? col + static_cast<ptrdiff_t>(gy) * W : uc,
+      const bool ok = k < nrows && gy >= 0 && gy < H && gy >= srow_lo && gy < srow_hi && xin;
+      cp_async_zfill(&tile[k][threadIdx.x + 1], ok ? col + static_cast<ptrdiff_t>(gy) * W : ustored,
                      sizeof(T), ok);
     }
     {
@@ -137,9 +141,10 @@ __global__ void __launch_bounds__(kRedThreads)
         const int k = west ? t : t - 32;
         const int gy = y0 - 1 + k;
         const int gx = west ? x0 - 1 : x0 + kRedThreads;
-        const bool ok = k < nrows && gy >= 0 && gy < H && gx >= 0 && gx < W;
+        const bool ok = k < nrows && gy >= 0 && gy < H && gy >= srow_lo && gy < srow_hi &&
+                        gx >= 0 && gx < W;
         cp_async_zfill(&tile[k][west ? 0 : kResTileW - 1],
-                       ok ? uc + static_cast<size_t>(gy) * Wz + gx : uc, sizeof(T), ok);
+                       ok ? uc + static_cast<size_t>(gy) * Wz + gx : ustored, sizeof(T), ok);
       }
     }
     asm volatile("cp.async.commit_group;\n" ::);
@@ -147,11 +152,11 @@ __global__ void __launch_bounds__(kRedThreads)
     // loaded while the copies are in flight
     uint8_t mk[kResBand];
     T bv[kResBand];
-    const size_t base = xin ? static_cast<size_t>(y0) * Wz + x : 0;
+    const size_t base = xin ? static_cast<size_t>(y0) * Wz + x : static_cast<size_t>(y0) * Wz;
 #pragma unroll
     for (int k = 0; k < kResBand; ++k) {
       const bool in = xin && k < ny;
-      const size_t i = in ? base + static_cast<size_t>(k) * Wz : 0;
+      const size_t i = in ? base + static_cast<size_t>(k) * Wz : static_cast<size_t>(y0) * Wz;
       const uint8_t m = __ldg(mask + i);
       mk[k] = in ? m : uint8_t(0);
       if (!INV) {
@@ -222,7 +227,8 @@ __global__ void __launch_bounds__(kResTmaThreads)
     residual_sumsq_tma_kernel(const __grid_constant__ CUtensorMap umap,
                               const __grid_constant__ CUtensorMap mmap,
                               const uint8_t* __restrict__ mask, const T* __restrict__ b, int W,
-                              int H, size_t N, int row0, int row1, double* partials) {
+                              int H, size_t N, int row0, int row1, int srow_lo,
+                              double* partials) {
   __shared__ __align__(128) T tile[kResTmaBand + 2][res_tma_box_w<T>()];
   __shared__ __align__(128) uint8_t mtile[kResTmaBand][kResTmaThreads];
   __shared__ uint64_t bar;
@@ -243,16 +249,19 @@ __global__ void __launch_bounds__(kResTmaThreads)
 #endif
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, sizeof(tile) + (MTMA ? sizeof(mtile) : 0));
-    tma_load_3d(&tile[0][0], &umap, x0 - res_tma_lead<T>(), y0 - 1, c, &bar);
-    if (MTMA) tma_load_2d(&mtile[0][0], &mmap, x0, y0, &bar);
+    // the maps cover the storage rows (stripe mode: [srow_lo, ...)): rows
+    // outside it arrive as zeros and are never used for rows in [row0, row1)
+    tma_load_3d(&tile[0][0], &umap, x0 - res_tma_lead<T>(), y0 - 1 - srow_lo, c, &bar);
+    if (MTMA) tma_load_2d(&mtile[0][0], &mmap, x0, y0 - srow_lo, &bar);
   }
   uint8_t mk[kResTmaBand];
   T bv[kResTmaBand];
-  const size_t base = xin ? static_cast<size_t>(y0) * Wz + x : 0;
+  // inactive lanes address row y0 (stored under stripe storage too)
+  const size_t base = xin ? static_cast<size_t>(y0) * Wz + x : static_cast<size_t>(y0) * Wz;
 #pragma unroll
   for (int k = 0; k < kResTmaBand; ++k) {
     const bool in = xin && k < ny;
-    const size_t i = in ? base + static_cast<size_t>(k) * Wz : 0;
+    const size_t i = in ? base + static_cast<size_t>(k) * Wz : static_cast<size_t>(y0) * Wz;
     if (!MTMA) {
       const uint8_t m = __ldg(mask + i);
       mk[k] = in ? m : uint8_t(0);
@@ -447,14 +456,15 @@ __global__ void __launch_bounds__(kScatterWarps * 32) known_scatter_kernel(
 // cell; known = OR; value = mean of known fine values (KnownOnly) or of all
 // of them (AllPixels), accumulated in row-major order like the reference.
 // One thread per coarse pixel; the two fine rows are read as pairs.
+// Stripe mode: coarse rows cy0 + blockIdx.y only; fn / cn are the storage
+// planes of the (pre-offset) fine and coarse buffers.
 template <typename T, bool VEC>
 __global__ void restrict_kernel(const uint8_t* __restrict__ fmask, const T* __restrict__ fval,
                                 int fw, int fh, int C, int averaging, uint8_t* __restrict__ cmask,
-                                T* __restrict__ cval) {
+                                T* __restrict__ cval, int cy0, size_t fn, size_t cn) {
   pdl_wait();
-  const int cw = (fw + 1) / 2, ch = (fh + 1) / 2;
-  const size_t fn = static_cast<size_t>(fw) * fh, cn = static_cast<size_t>(cw) * ch;
-  const int cx = blockIdx.x * blockDim.x + threadIdx.x, cy = blockIdx.y;
+  const int cw = (fw + 1) / 2;
+  const int cx = blockIdx.x * blockDim.x + threadIdx.x, cy = cy0 + static_cast<int>(blockIdx.y);
   if (cx >= cw) return;
   const int fx0 = 2 * cx, fy0 = 2 * cy;
   const bool two_x = fx0 + 1 < fw, two_y = fy0 + 1 < fh;
@@ -505,12 +515,16 @@ template <typename T>
 __global__ void __launch_bounds__(256, SI_PRO_OCC)
     prolong_snap_kernel(const T* __restrict__ coarse, int cw, int ch, int fw, int fh, int C,
                         const uint8_t* __restrict__ fmask, const T* __restrict__ fval,
-                        T* __restrict__ fine) {
+                        T* __restrict__ fine, int fy_lo, int fy_hi, int cs_lo, int cs_hi,
+                        size_t fn, size_t cn) {
+  // Fine rows [fy_lo, fy_hi) only; the coarse buffer holds rows
+  // [cs_lo, cs_hi) (stripe storage; pointers pre-offset, fn / cn the storage
+  // planes).  Whole image: 0, fh, 0, ch, fw*fh, cw*ch.
   constexpr int kCh = 3;  // channels staged per pass
   __shared__ T tile[kCh][kProCY][kProCX];
   pdl_wait();
-  const size_t fn = static_cast<size_t>(fw) * fh, cn = static_cast<size_t>(cw) * ch;
-  const int fx0 = blockIdx.x * kProX, fy0 = blockIdx.y * kProY;
+  const int fx0 = blockIdx.x * kProX, fy0 = fy_lo + static_cast<int>(blockIdx.y) * kProY;
+  fh = fy_hi;  // rows at or beyond fy_hi are neither read nor written
   const int cx0 = fx0 / 2 - 1, cy0 = fy0 / 2 - 1;  // staged window origin
   const int qx = threadIdx.x & 31, qy = threadIdx.x >> 5;
   const int fxq = fx0 + 2 * qx, fyq = fy0 + 2 * qy;
@@ -530,7 +544,7 @@ __global__ void __launch_bounds__(256, SI_PRO_OCC)
     for (int i = threadIdx.x; i < nc * kProCY * kProCX; i += blockDim.x) {
       const int k = i / (kProCY * kProCX), rem = i - k * (kProCY * kProCX);
       const int ly = rem / kProCX, lx = rem - ly * kProCX;
-      const int gy = min(max(cy0 + ly, 0), ch - 1), gx = min(max(cx0 + lx, 0), cw - 1);
+      const int gy = min(max(cy0 + ly, cs_lo), cs_hi - 1), gx = min(max(cx0 + lx, 0), cw - 1);
       tile[k][ly][lx] = __ldg(coarse + (c0 + k) * cn + static_cast<size_t>(gy) * cw + gx);
     }
     // the known pixels' data of my quad, in flight across the barrier
@@ -540,7 +554,8 @@ __global__ void __launch_bounds__(256, SI_PRO_OCC)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const bool on = k < nc && ((snap >> q) & 1u);
-        const size_t i = on ? static_cast<size_t>(fyq + (q >> 1)) * fw + fxq + (q & 1) : 0;
+        const size_t i = on ? static_cast<size_t>(fyq + (q >> 1)) * fw + fxq + (q & 1)
+                            : static_cast<size_t>(fy_lo) * fw;  // a stored row
         sv[k][q] = on ? __ldg(fval + (c0 + k) * fn + i) : T(0);
       }
     __syncthreads();

@@ -188,6 +188,9 @@ struct si_ctx {
   int counters_fresh = 0;                       // host_cnt current (graph-mode frame)
   cudaStream_t cap_stream[2] = {nullptr, nullptr};
   DevBuf lvl_state, lvl_sums;
+  // striped solves (stripes.cuh): per-level storage rows, comm scratch
+  std::vector<LevelBuf> stripe_levels;
+  DevBuf stripe_send, stripe_recv, stripe_in_f, stripe_in_mask, stripe_out;
   unsigned long long* host_state = nullptr;     // mapped: LevelState[SI_MAX_LEVELS]
   unsigned long long* dev_state = nullptr;      // device alias of host_state
   // batch pipelining: a graph-mode frame's outcome lands in frame_host[slot]
@@ -360,12 +363,17 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s,
   CK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
 }
 
+// Stripe storage (srow_lo/srow_hi, see SweepArgs): mask/u/b hold image rows
+// [srow_lo, srow_hi) and are pre-offset by -srow_lo rows; whole image: 0, H.
 template <typename T>
 void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W, int H, int C,
                      int mode, double* out, bool known_invariant = true, int row0 = 0,
-                     int row1 = -1) {
+                     int row1 = -1, int srow_lo = 0, int srow_hi = -1) {
   if (row1 < 0) row1 = H;
-  const size_t N = static_cast<size_t>(W) * H;
+  if (srow_hi < 0) srow_hi = H;
+  const int HS = srow_hi - srow_lo;
+  const size_t N = static_cast<size_t>(W) * HS;
+  const size_t off = static_cast<size_t>(srow_lo) * W;  // storage start = pointer + off
   const int rows = std::max(1, row1 - row0);
   const int gx = (W + kRedThreads - 1) / kRedThreads;
   const int gy = (rows + kResBand - 1) / kResBand;
@@ -376,18 +384,18 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
           static_cast<double>(W) * std::max(0, row1 - row0) * (C * sizeof(T) + (mode == 1 ? 0 : 1)));
   CUtensorMap map;
   if (mode != 1 && !tma_disabled() &&
-      make_plane_map(&map, u, W, H, C, sizeof(T), res_tma_box_w<T>(), kResTmaBand + 2)) {
+      make_plane_map(&map, u + off, W, HS, C, sizeof(T), res_tma_box_w<T>(), kResTmaBand + 2)) {
     const int tx = (W + kResTmaThreads - 1) / kResTmaThreads;
     const int gy = (rows + kResTmaBand - 1) / kResTmaBand;
     x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(tx) * gy * C);
     // the mask band rides on the same barrier when its rows are 16-byte aligned
     CUtensorMap mmap{};
-    const bool mtma = make_mask_map(&mmap, mask, W, H, kResTmaThreads, kResTmaBand);
+    const bool mtma = make_mask_map(&mmap, mask + off, W, HS, kResTmaThreads, kResTmaBand);
     auto launch = [&](auto inv, auto mt) {
       constexpr bool INV = decltype(inv)::value, MT = decltype(mt)::value;
       ++x.c.launch_count;
       launch_pdl(residual_sumsq_tma_kernel<T, INV, MT>, dim3(tx, gy, C), kResTmaThreads, x.s,
-                 map, mmap, mask, b, W, H, N, row0, row1, x.c.red_partials.as<double>());
+                 map, mmap, mask, b, W, H, N, row0, row1, srow_lo, x.c.red_partials.as<double>());
     };
     if (known_invariant) {
       if (mtma) launch(std::true_type{}, std::true_type{});
@@ -403,13 +411,13 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
   } else if (known_invariant) {
     ++x.c.launch_count;
     residual_sumsq_kernel<T, true><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
-        mask, u, b, W, H, N, mode, row0, row1, x.c.red_partials.as<double>(), out,
-        x.c.ticket.as<unsigned int>());
+        mask, u, b, W, H, N, mode, row0, row1, srow_lo, srow_hi, x.c.red_partials.as<double>(),
+        out, x.c.ticket.as<unsigned int>());
   } else {
     ++x.c.launch_count;
     residual_sumsq_kernel<T, false><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
-        mask, u, b, W, H, N, mode, row0, row1, x.c.red_partials.as<double>(), out,
-        x.c.ticket.as<unsigned int>());
+        mask, u, b, W, H, N, mode, row0, row1, srow_lo, srow_hi, x.c.red_partials.as<double>(),
+        out, x.c.ticket.as<unsigned int>());
   }
   CK(cudaGetLastError());
 }
@@ -426,29 +434,45 @@ void launch_sq_error(Ctx& x, const T* u, const double* f, size_t N, int C, doubl
   CK(cudaGetLastError());
 }
 
+// Coarse rows [cy_lo, cy_hi) (stripe mode; -1: all); fn / cn: storage planes
+// of the pre-offset fine / coarse buffers (0: whole-image planes).
 template <typename T>
 void launch_restrict(Ctx& x, const uint8_t* fmask, const T* fval, int fw, int fh, int C,
-                     int averaging, uint8_t* cmask, T* cval) {
+                     int averaging, uint8_t* cmask, T* cval, int cy_lo = 0, int cy_hi = -1,
+                     size_t fn = 0, size_t cn = 0) {
   const int cw = (fw + 1) / 2, ch = (fh + 1) / 2;
-  const dim3 grid((cw + 127) / 128, ch);
-  if (fw % 2 == 0 && reinterpret_cast<uintptr_t>(fval) % 16 == 0) {
-    ++x.c.launch_count;
+  if (cy_hi < 0) cy_hi = ch;
+  if (fn == 0) fn = static_cast<size_t>(fw) * fh;
+  if (cn == 0) cn = static_cast<size_t>(cw) * ch;
+  if (cy_hi <= cy_lo) return;
+  const dim3 grid((cw + 127) / 128, cy_hi - cy_lo);
+  // the vector path needs 16-byte aligned fine rows and planes
+  const bool vec = fw % 2 == 0 && fn % 2 == 0 && reinterpret_cast<uintptr_t>(fval) % 16 == 0;
+  ++x.c.launch_count;
+  if (vec)
     launch_pdl(restrict_kernel<T, true>, grid, 128, x.s, fmask, fval, fw, fh, C, averaging, cmask,
-               cval);
-  } else {
-    ++x.c.launch_count;
+               cval, cy_lo, fn, cn);
+  else
     launch_pdl(restrict_kernel<T, false>, grid, 128, x.s, fmask, fval, fw, fh, C, averaging, cmask,
-               cval);
-  }
+               cval, cy_lo, fn, cn);
   CK(cudaGetLastError());
 }
 
+// Fine rows [fy_lo, fy_hi); coarse storage rows [cs_lo, cs_hi); fn / cn
+// storage planes (stripe mode; defaults: the whole image).
 template <typename T>
 void launch_prolong(Ctx& x, const T* coarse, int cw, int ch, int fw, int fh, int C,
-                    const uint8_t* fmask, const T* fval, T* fine) {
-  const dim3 grid((fw + kProX - 1) / kProX, (fh + kProY - 1) / kProY);
+                    const uint8_t* fmask, const T* fval, T* fine, int fy_lo = 0, int fy_hi = -1,
+                    int cs_lo = 0, int cs_hi = -1, size_t fn = 0, size_t cn = 0) {
+  if (fy_hi < 0) fy_hi = fh;
+  if (cs_hi < 0) cs_hi = ch;
+  if (fn == 0) fn = static_cast<size_t>(fw) * fh;
+  if (cn == 0) cn = static_cast<size_t>(cw) * ch;
+  if (fy_hi <= fy_lo) return;
+  const dim3 grid((fw + kProX - 1) / kProX, (fy_hi - fy_lo + kProY - 1) / kProY);
   ++x.c.launch_count;
-  launch_pdl(prolong_snap_kernel<T>, grid, 256, x.s, coarse, cw, ch, fw, fh, C, fmask, fval, fine);
+  launch_pdl(prolong_snap_kernel<T>, grid, 256, x.s, coarse, cw, ch, fw, fh, C, fmask, fval, fine,
+             fy_lo, fy_hi, cs_lo, cs_hi, fn, cn);
   CK(cudaGetLastError());
 }
 
@@ -484,15 +508,19 @@ void launch_sweep_nw(Ctx& x, const SweepArgs<T>& a, int nblocks, int C) {
 template <typename T>
 void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_new, int W, int H,
                   int C, int block, int overlap, int flavour, double alpha, const LocalCfg& lc,
-                  bool known_invariant, unsigned long long* counters, int by0 = 0, int by1 = -1) {
+                  bool known_invariant, unsigned long long* counters, int by0 = 0, int by1 = -1,
+                  int srow_lo = 0, int srow_hi = -1) {
+  if (srow_hi < 0) srow_hi = H;
   SweepArgs<T> a{};
+  a.srow_lo = srow_lo;
+  a.srow_hi = srow_hi;
   a.mask = mask;
   a.b = b;
   a.u_old = u_old;
   a.u_new = u_new;
   a.W = W;
   a.H = H;
-  a.N = static_cast<size_t>(W) * H;
+  a.N = static_cast<size_t>(W) * (srow_hi - srow_lo);
   a.ax = Axis::make(W, block, overlap);
   a.ay = Axis::make(H, block, overlap);
   a.am1 = static_cast<T>(alpha - 1.0);
@@ -506,7 +534,7 @@ void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_
   a.by0 = by0;
   if (block > kMaxBlock) {  // K2g: blocks beyond 32x32, CG vectors in global scratch
     if (by1 <= by0) return;
-    const double bytes = static_cast<double>(a.N) * (2.0 * C * sizeof(T) + 1.0) * (by1 - by0) /
+    const double bytes = static_cast<double>(W) * H * (2.0 * C * sizeof(T) + 1.0) * (by1 - by0) /
                          a.ay.count;
     Timed t(x, K_SWEEP, bytes);
     const size_t per_row = sizeof(T) * 5 * static_cast<size_t>(block) * block * a.ax.count * C;
@@ -526,10 +554,11 @@ void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_
   // block (tile_lead), so any anchor works; the row pitch must be a multiple
   // of 16 bytes (checked by make_plane_map)
   a.use_tma = !tma_disabled() &&
-              make_plane_map(&a.umap, u_old, W, H, C, sizeof(T), tile_w<T>(), kTileH);
+              make_plane_map(&a.umap, u_old + static_cast<size_t>(srow_lo) * W, W,
+                             srow_hi - srow_lo, C, sizeof(T), tile_w<T>(), kTileH);
   const int nblocks = a.ax.count * (by1 - by0);
   if (nblocks <= 0) return;
-  const double bytes = static_cast<double>(a.N) * (2.0 * C * sizeof(T) + 1.0) * (by1 - by0) /
+  const double bytes = static_cast<double>(W) * H * (2.0 * C * sizeof(T) + 1.0) * (by1 - by0) /
                        a.ay.count;
   Timed t(x, K_SWEEP, bytes);
   const int nw = sizeof(T) == 8 ? x.c.sweep_nw64 : x.c.sweep_nw32;
@@ -2045,6 +2074,11 @@ void si_destroy(si_ctx* c) {
   }
   c->lvl_state.release();
   c->lvl_sums.release();
+  for (auto& l : c->stripe_levels)
+    for (DevBuf* b : {&l.mask, &l.b, &l.u0, &l.u1}) b->release();
+  for (DevBuf* b : {&c->stripe_send, &c->stripe_recv, &c->stripe_in_f, &c->stripe_in_mask,
+                    &c->stripe_out})
+    b->release();
   for (void* b : c->pack_buf)
     if (b) cudaFreeHost(b);
   for (auto& p : c->pending) {
@@ -2083,6 +2117,11 @@ si_status si_trim(si_ctx* c) {
     }
     for (DevBuf* b : {&c->in_f, &c->in_mask, &c->in_ref, &c->out_img, &c->aux}) b->release();
     c->vz.release();
+    for (auto& l : c->stripe_levels)
+      for (DevBuf* b : {&l.mask, &l.b, &l.u0, &l.u1}) b->release();
+    for (DevBuf* b : {&c->stripe_send, &c->stripe_recv, &c->stripe_in_f, &c->stripe_in_mask,
+                      &c->stripe_out})
+      b->release();
   });
 }
 
@@ -2496,191 +2535,6 @@ si_status si_local_operator_apply(si_ctx* ctx, const uint8_t* mask, int w, int h
   });
 }
 
-namespace {
-struct StripeGeom {
-  int nby, k0, k1, own_lo, own_hi, win_lo, win_hi;
-};
-
-StripeGeom stripe_geom(int h, int block, int overlap, int world, int rank) {
-  const Axis ay = Axis::make(h, block, overlap);
-  StripeGeom g;
-  g.nby = ay.count;
-  g.k0 = static_cast<int>(static_cast<long long>(rank) * ay.count / world);
-  g.k1 = static_cast<int>(static_cast<long long>(rank + 1) * ay.count / world);
-  if (g.k0 == g.k1) {
-    g.own_lo = g.own_hi = g.k0 < ay.count ? ay.owned_begin(g.k0) : h;
-    g.win_lo = g.win_hi = g.own_lo;
-    return g;
-  }
-  g.own_lo = ay.owned_begin(g.k0);
-  g.own_hi = ay.owned_end(g.k1 - 1);
-  // rows read by the sweeps of blocks k0..k1-1 (block window + residual ring)
-  // and by the residual stencil of the owned rows
-  g.win_lo = std::max(0, std::min(ay.anchor(g.k0) - 1, g.own_lo - 1));
-  g.win_hi = std::min(h, std::max(ay.anchor(g.k1 - 1) + block + 1, g.own_hi + 1));
-  return g;
-}
-}  // namespace
-
-si_status si_stripe_plan(int h, int block_size, int overlap, int world, int rank, int* out) {
-  return guard([&] {
-    check_arg(out != nullptr, "null argument");
-    check_arg(world >= 1 && rank >= 0 && rank < world, "stripe plan: invalid world/rank");
-    validate_partition(h, h, block_size, overlap);
-    const StripeGeom g = stripe_geom(h, block_size, overlap, world, rank);
-    bool valid = true;
-    if (g.k0 < g.k1) {
-      if (g.win_lo < g.own_lo) {  // halo above must be owned by rank-1
-        const StripeGeom up = stripe_geom(h, block_size, overlap, world, rank - 1);
-        valid &= rank > 0 && up.k0 < up.k1 && up.own_lo <= g.win_lo;
-      }
-      if (g.win_hi > g.own_hi) {
-        const StripeGeom dn = stripe_geom(h, block_size, overlap, world, rank + 1);
-        valid &= rank + 1 < world && dn.k0 < dn.k1 && dn.own_hi >= g.win_hi;
-      }
-    }
-    const int v[8] = {g.nby, g.k0, g.k1, g.own_lo, g.own_hi, g.win_lo, g.win_hi, valid ? 1 : 0};
-    std::memcpy(out, v, sizeof v);
-  });
-}
-
-si_status si_device_ingest(si_ctx* ctx, const double* d_f, const uint8_t* d_mask, int w, int h,
-                           int c, int precision, void* d_b, long long* known, void* stream) {
-  return guard([&] {
-    check_arg(ctx && d_f && d_mask && d_b, "null argument");
-    check_dims(w, h, c);
-    set_device(ctx);
-    Ctx x{*ctx, pick_stream(ctx, stream)};
-    begin_counters(x);
-    const size_t n = static_cast<size_t>(w) * h;
-    if (precision == SI_PRECISION_FP32) {
-      ++x.c.launch_count;
-      ingest_kernel<float><<<grid_for(n, 256, 148 * 16), 256, 0, x.s>>>(
-          d_f, d_mask, n, c, static_cast<float*>(d_b), ctx->counters.as<unsigned long long>() + 2);
-    } else {
-      ++x.c.launch_count;
-      ingest_kernel<double><<<grid_for(n, 256, 148 * 16), 256, 0, x.s>>>(
-          d_f, d_mask, n, c, static_cast<double*>(d_b), ctx->counters.as<unsigned long long>() + 2);
-    }
-    CK(cudaGetLastError());
-    publish_counters(x, 3);
-    if (known) *known = static_cast<long long>(ctx->host_cnt[2]);
-  });
-}
-
-si_status si_device_restrict(si_ctx* ctx, const uint8_t* d_mask, const void* d_values, int w, int h,
-                             int c, int averaging, int precision, uint8_t* d_cmask,
-                             void* d_cvalues, void* stream) {
-  return guard([&] {
-    check_arg(ctx && d_mask && d_values && d_cmask && d_cvalues, "null argument");
-    check_dims(w, h, c);
-    check_arg(w >= 2 && h >= 2, "restrict_level: fine grid must be at least 2x2");
-    set_device(ctx);
-    Ctx x{*ctx, pick_stream(ctx, stream)};
-    if (precision == SI_PRECISION_FP32)
-      launch_restrict<float>(x, d_mask, static_cast<const float*>(d_values), w, h, c, averaging,
-                             d_cmask, static_cast<float*>(d_cvalues));
-    else
-      launch_restrict<double>(x, d_mask, static_cast<const double*>(d_values), w, h, c, averaging,
-                              d_cmask, static_cast<double*>(d_cvalues));
-    sync(x);
-  });
-}
-
-si_status si_device_prolong_snap(si_ctx* ctx, const void* d_coarse, int cw, int ch, int fw, int fh,
-                                 int c, const uint8_t* d_fmask, const void* d_fvalues,
-                                 int precision, void* d_fine, void* stream) {
-  return guard([&] {
-    check_arg(ctx && d_coarse && d_fine, "null argument");
-    check_arg(cw == (fw + 1) / 2 && ch == (fh + 1) / 2,
-              "prolongate: coarse grid is not the dyadic parent of the fine grid");
-    set_device(ctx);
-    Ctx x{*ctx, pick_stream(ctx, stream)};
-    if (precision == SI_PRECISION_FP32)
-      launch_prolong<float>(x, static_cast<const float*>(d_coarse), cw, ch, fw, fh, c, d_fmask,
-                            static_cast<const float*>(d_fvalues), static_cast<float*>(d_fine));
-    else
-      launch_prolong<double>(x, static_cast<const double*>(d_coarse), cw, ch, fw, fh, c, d_fmask,
-                             static_cast<const double*>(d_fvalues), static_cast<double*>(d_fine));
-    sync(x);
-  });
-}
-
-si_status si_device_residual_rows(si_ctx* ctx, const uint8_t* d_mask, const void* d_u,
-                                  const void* d_b, int w, int h, int c, int row0, int row1,
-                                  int mode, int known_invariant, int precision, double* sums,
-                                  void* stream) {
-  return guard([&] {
-    check_arg(ctx && d_mask && d_u && d_b && sums, "null argument");
-    check_dims(w, h, c);
-    check_arg(0 <= row0 && row0 <= row1 && row1 <= h, "residual rows out of range");
-    set_device(ctx);
-    Ctx x{*ctx, pick_stream(ctx, stream)};
-    prepare_red(x, c);
-    if (row0 == row1) {
-      for (int k = 0; k < c; ++k) sums[k] = 0.0;
-      return;
-    }
-    if (precision == SI_PRECISION_FP32)
-      launch_residual<float>(x, d_mask, static_cast<const float*>(d_u),
-                             static_cast<const float*>(d_b), w, h, c, mode, ctx->dev_red,
-                             known_invariant != 0, row0, row1);
-    else
-      launch_residual<double>(x, d_mask, static_cast<const double*>(d_u),
-                              static_cast<const double*>(d_b), w, h, c, mode, ctx->dev_red,
-                              known_invariant != 0, row0, row1);
-    sync(x);
-    std::memcpy(sums, ctx->host_red, sizeof(double) * c);
-  });
-}
-
-si_status si_device_sweep_rows(si_ctx* ctx, const uint8_t* d_mask, const void* d_b,
-                               const void* d_u_old, void* d_u_new, int w, int h, int c,
-                               int block_size, int overlap, int by0, int by1, int flavour,
-                               const si_options* opt, int known_invariant, long long* failures,
-                               long long* cg_iterations, void* stream) {
-  return guard([&] {
-    check_arg(ctx && d_mask && d_b && d_u_old && d_u_new, "null argument");
-    check_dims(w, h, c);
-    validate_partition(w, h, block_size, overlap);
-    const Axis ay = Axis::make(h, block_size, overlap);
-    check_arg(0 <= by0 && by0 <= by1 && by1 <= ay.count, "sweep: block rows out of range");
-    const si_options o = opts_or_default(opt);
-    validate_local(o);
-    if (flavour == SI_FLAVOUR_ORAS)
-      check_arg(std::isfinite(o.alpha), "run_schwarz_level: alpha must be finite");
-    set_device(ctx);
-    Ctx x{*ctx, pick_stream(ctx, stream)};
-    LocalPrecision lp(*ctx, o.precision);
-    begin_counters(x);
-    const LocalCfg lc{o.local_tolerance, o.local_max_iterations, o.local_check_interval};
-    if (o.precision == SI_PRECISION_FP32)
-      launch_sweep<float>(x, d_mask, static_cast<const float*>(d_b),
-                          static_cast<const float*>(d_u_old), static_cast<float*>(d_u_new), w, h,
-                          c, block_size, overlap, flavour, o.alpha, lc, known_invariant != 0,
-                          ctx->counters.as<unsigned long long>(), by0, by1);
-    else
-      launch_sweep<double>(x, d_mask, static_cast<const double*>(d_b),
-                           static_cast<const double*>(d_u_old), static_cast<double*>(d_u_new), w,
-                           h, c, block_size, overlap, flavour, o.alpha, lc, known_invariant != 0,
-                           ctx->counters.as<unsigned long long>(), by0, by1);
-#ifdef SI_PROBE
-    publish_counters(x, 8);
-    const double its = std::max(1.0, static_cast<double>(ctx->host_cnt[1]));
-    const double ctas = static_cast<double>(Axis::make(w, block_size, overlap).count) *
-                        (by1 - by0) * c;
-    std::fprintf(stderr, "probe cycles/CTA-iteration: apply+pAp %.0f, alpha+r+rr %.0f, beta+p %.0f;"
-                 " per CTA: setup %.0f, write-back %.0f\n",
-                 ctx->host_cnt[3] / its, ctx->host_cnt[4] / its, ctx->host_cnt[5] / its,
-                 ctx->host_cnt[6] / ctas, ctx->host_cnt[7] / ctas);
-#else
-    publish_counters(x, 2);
-#endif
-    if (failures) *failures = static_cast<long long>(ctx->host_cnt[0]);
-    if (cg_iterations) *cg_iterations = static_cast<long long>(ctx->host_cnt[1]);
-  });
-}
-
 si_status si_pack_known_samples(const double* f, const uint8_t* mask, int w, int h, int c,
                                 uint32_t* tile_off, double* vals, long long* K) {
   return guard([&] {
@@ -2834,6 +2688,221 @@ si_status si_assign_nearest_site(si_ctx* ctx, const uint8_t* mask, int w, int h,
     sync(x);
     *num_sites = m;
   });
+}
+
+}  // extern "C"
+
+// ====================================================================== stripes
+#include "stripes.cuh"
+
+namespace {
+
+StripeLayout checked_layout(int method, int w, int h, int c, const si_options& o, int world,
+                            int rank) {
+  check_method(method);
+  check_dims(w, h, c);
+  validate_options_common(o);
+  check_arg(world >= 1 && rank >= 0 && rank < world, "stripes: invalid world/rank");
+  if (method == SI_METHOD_CG || method == SI_METHOD_MLCG)
+    fail(SI_ERR_UNSUPPORTED, "stripes: the CG level solver is not striped (Schwarz methods only)");
+  check_arg(levels_for(method, o) >= 1, "build_pyramid: levels must be >= 1");
+  return stripe_layout(w, h, o, levels_for(method, o), world, rank);
+}
+
+// One rank's solve on device rows (see si_run_method_striped_device).
+void run_striped_device(si_ctx* ctx, si_stripe_comm* comm, int method, const double* d_f,
+                        const uint8_t* d_mask, int w, int h, int c, const si_options& o,
+                        double* d_out, si_report* rep, si_trace_fn trace, void* user,
+                        cudaStream_t s) {
+  const StripeLayout P = checked_layout(method, w, h, c, o, comm->world, comm->rank);
+  Ctx x{*ctx, s};
+  LocalPrecision lp(*ctx, o.precision);
+  begin_counters(x);
+  Trace tr{trace, user, Clock::now()};
+  const int flavour = flavour_for(method);
+  if (o.precision == SI_PRECISION_FP32)
+    stripe_solve_device<float>(x, *comm, P, flavour, d_f, d_mask, c, o, d_out, rep, tr);
+  else
+    stripe_solve_device<double>(x, *comm, P, flavour, d_f, d_mask, c, o, d_out, rep, tr);
+  sync(x);
+}
+
+// Host buffers: upload the level-0 store rows, solve, download the own rows.
+void run_striped_host(si_ctx* ctx, si_stripe_comm* comm, int method, const double* f,
+                      const uint8_t* mask, int w, int h, int c, const si_options& o, double* out,
+                      si_report* rep, si_trace_fn trace, void* user) {
+  const StripeLayout P = checked_layout(method, w, h, c, o, comm->world, comm->rank);
+  const Span st = P.L[0].store[comm->rank], own = P.L[0].own[comm->rank];
+  const size_t W = static_cast<size_t>(w), N = W * h;
+  const size_t rows = std::max(0, st.hi - st.lo), orows = std::max(0, own.hi - own.lo);
+  set_device(ctx);
+  Ctx x{*ctx, ctx->own_stream};
+  ctx->stripe_in_f.ensure(std::max<size_t>(1, rows * W * c) * sizeof(double));
+  ctx->stripe_in_mask.ensure(std::max<size_t>(1, rows * W));
+  ctx->stripe_out.ensure(std::max<size_t>(1, orows * W * c) * sizeof(double));
+  const auto t0 = Clock::now();
+  for (int k = 0; k < c && rows; ++k)
+    h2d(x, ctx->stripe_in_f.as<double>() + k * rows * W, f + k * N + st.lo * W,
+        rows * W * sizeof(double));
+  if (rows) h2d(x, ctx->stripe_in_mask.ptr, mask + st.lo * W, rows * W);
+  run_striped_device(ctx, comm, method, ctx->stripe_in_f.as<double>(),
+                     ctx->stripe_in_mask.as<uint8_t>(), w, h, c, o, ctx->stripe_out.as<double>(),
+                     rep, trace, user, ctx->own_stream);
+  for (int k = 0; k < c && orows; ++k)
+    d2h(x, out + k * N + own.lo * W, ctx->stripe_out.as<double>() + k * orows * W,
+        orows * W * sizeof(double));
+  rep->h2d_bytes = static_cast<long long>(rows * W * (c * sizeof(double) + 1));
+  rep->d2h_bytes = static_cast<long long>(orows * W * c * sizeof(double));
+  rep->elapsed_ms = ms_since(t0);
+}
+
+}  // namespace
+
+extern "C" {
+
+si_status si_stripe_level_plan(int method, int w, int h, int c, const si_options* opt, int world,
+                               int rank, int* depth, int* out) {
+  return guard([&] {
+    check_arg(depth && out, "null argument");
+    const si_options o = opts_or_default(opt);
+    const StripeLayout P = checked_layout(method, w, h, c, o, world, rank);
+    *depth = P.depth;
+    for (int l = 0; l < P.depth; ++l) {
+      const StripeLevel& S = P.L[l];
+      const int v[SI_STRIPE_PLAN_INTS] = {S.k0, S.k1, S.own[rank].lo, S.own[rank].hi,
+                                         S.win[rank].lo, S.win[rank].hi, S.need[rank].lo,
+                                         S.need[rank].hi, S.store[rank].lo, S.store[rank].hi,
+                                         S.block, S.overlap};
+      std::memcpy(out + l * SI_STRIPE_PLAN_INTS, v, sizeof v);
+    }
+  });
+}
+
+si_status si_nccl_unique_id(unsigned char* id) {
+  return guard([&] {
+    check_arg(id != nullptr, "null argument");
+    static_assert(sizeof(ncclUniqueId) == SI_NCCL_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId u;
+    nccl_check(nccl().GetUniqueId(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof u);
+  });
+}
+
+si_status si_stripe_comm_init_nccl(si_ctx* ctx, int world, int rank, const unsigned char* id,
+                                   si_stripe_comm** out) {
+  return guard([&] {
+    check_arg(ctx && id && out, "null argument");
+    check_arg(world >= 1 && rank >= 0 && rank < world, "stripes: invalid world/rank");
+    set_device(ctx);
+    auto comm = std::make_unique<NcclComm>();
+    comm->world = world;
+    comm->rank = rank;
+    comm->device = ctx->device;
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    nccl_check(nccl().CommInitRank(&comm->comm, world, u, rank), "ncclCommInitRank");
+    *out = comm.release();
+  });
+}
+
+si_status si_stripe_comm_init_local(si_ctx* const* ctxs, int world, si_stripe_comm** out) {
+  return guard([&] {
+    check_arg(ctxs && out && world >= 1, "null argument");
+    auto grp = std::make_shared<LocalGroup>();
+    grp->world = world;
+    grp->ready.assign(world, nullptr);
+    grp->done.assign(world, nullptr);
+    grp->posted.resize(world);
+    grp->posted_vals.assign(world, nullptr);
+    for (int r = 0; r < world; ++r) {
+      check_arg(ctxs[r] != nullptr, "null context");
+      set_device(ctxs[r]);
+      CK(cudaEventCreateWithFlags(&grp->ready[r], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&grp->done[r], cudaEventDisableTiming));
+    }
+    for (int r = 0; r < world; ++r) {
+      auto comm = new LocalComm();
+      comm->world = world;
+      comm->rank = r;
+      comm->device = ctxs[r]->device;
+      comm->g = grp;
+      out[r] = comm;
+    }
+  });
+}
+
+void si_stripe_comm_destroy(si_stripe_comm* comm) { delete comm; }
+
+si_status si_run_method_striped(si_ctx* ctx, si_stripe_comm* comm, int method, const double* f,
+                                const uint8_t* mask, int w, int h, int c, const si_options* opt,
+                                double* out, si_report* report, si_trace_fn trace, void* user) {
+  si_report scratch;
+  si_report* rep = report ? report : &scratch;
+  clear_report(rep);
+  const si_status st = guard([&] {
+    check_arg(ctx && comm && f && mask && out, "null argument");
+    run_striped_host(ctx, comm, method, f, mask, w, h, c, opts_or_default(opt), out, rep, trace,
+                     user);
+  });
+  if (st != SI_OK)
+    if (auto* lc = dynamic_cast<LocalComm*>(comm)) lc->g->abort();  // release waiting peers
+  return st;
+}
+
+si_status si_run_method_striped_device(si_ctx* ctx, si_stripe_comm* comm, int method,
+                                       const double* d_f_rows, const uint8_t* d_mask_rows, int w,
+                                       int h, int c, const si_options* opt, double* d_out_rows,
+                                       si_report* report, void* stream) {
+  si_report scratch;
+  si_report* rep = report ? report : &scratch;
+  clear_report(rep);
+  const si_status st = guard([&] {
+    check_arg(ctx && comm && d_f_rows && d_mask_rows && d_out_rows, "null argument");
+    set_device(ctx);
+    const auto t0 = Clock::now();
+    run_striped_device(ctx, comm, method, d_f_rows, d_mask_rows, w, h, c, opts_or_default(opt),
+                       d_out_rows, rep, nullptr, nullptr, pick_stream(ctx, stream));
+    rep->elapsed_ms = ms_since(t0);
+  });
+  if (st != SI_OK)
+    if (auto* lc = dynamic_cast<LocalComm*>(comm)) lc->g->abort();
+  return st;
+}
+
+si_status si_run_method_striped_group(si_ctx* const* ctxs, int world, int method, const double* f,
+                                      const uint8_t* mask, int w, int h, int c,
+                                      const si_options* opt, double* out, si_report* reports) {
+  std::vector<si_stripe_comm*> comms(std::max(world, 1), nullptr);
+  si_status st = si_stripe_comm_init_local(ctxs, world, comms.data());
+  if (st != SI_OK) return st;
+  std::vector<si_status> sts(world, SI_OK);
+  std::vector<std::string> errs(world);
+  std::vector<si_report> reps(world);
+  {
+    std::vector<std::thread> th;
+    for (int r = 0; r < world; ++r)
+      th.emplace_back([&, r] {
+        sts[r] = si_run_method_striped(ctxs[r], comms[r], method, f, mask, w, h, c, opt, out,
+                                       &reps[r], nullptr, nullptr);
+        if (sts[r] != SI_OK) errs[r] = g_last_error;
+      });
+    for (auto& t : th) t.join();
+  }
+  for (auto* cm : comms) si_stripe_comm_destroy(cm);
+  if (reports)
+    for (int r = 0; r < world; ++r) reports[r] = reps[r];
+  // the first failing rank's status (an aborted peer reports SI_ERR_RUNTIME)
+  for (int r = 0; r < world; ++r)
+    if (sts[r] != SI_OK && errs[r].find("aborted by another rank") == std::string::npos) {
+      g_last_error = errs[r];
+      return sts[r];
+    }
+  for (int r = 0; r < world; ++r)
+    if (sts[r] != SI_OK) {
+      g_last_error = errs[r];
+      return sts[r];
+    }
+  return SI_OK;
 }
 
 }  // extern "C"

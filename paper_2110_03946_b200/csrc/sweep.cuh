@@ -76,6 +76,12 @@ struct SweepArgs {
                        // known pixels (so r = 0 there); b is never read
   unsigned long long* counters;  // [0] failures, [1] CG iterations (may be null)
   int by0;             // first block row of this launch (stripe mode; 0 otherwise)
+  // Stripe storage: the buffers hold only image rows [srow_lo, srow_hi) (the
+  // pointers above are pre-offset by -srow_lo rows, N is the storage plane);
+  // the TMA map covers the storage, so tile rows outside it read as zeros --
+  // only the discarded ghost-row residuals (tile rows 0 and B+3) can fall
+  // there.  Whole-image solves: 0 and H.
+  int srow_lo, srow_hi;
   T* scratch;          // K2g (blocks > 32): per-CTA CG vectors in global memory
 };
 
@@ -208,7 +214,7 @@ struct Cell {
 // coalesced row segments, every load independent and issued up front).
 template <typename T, int NW>
 __device__ __forceinline__ void stage_u_tile(T (*ut)[tile_w<T>()], const T* __restrict__ u, int x0,
-                                             int y0, int B, int W, int H) {
+                                             int y0, int B, int W, int row_lo, int row_hi) {
   // Warp w stages tile rows w, w+NW, ...: lanes 0..B load columns x0..x0+B
   // (one coalesced row segment), lanes 30/31 the ring columns x0-1 and x0+32.
   constexpr int kRows = (kTileH + NW - 1) / NW;
@@ -223,8 +229,8 @@ __device__ __forceinline__ void stage_u_tile(T (*ut)[tile_w<T>()], const T* __re
   for (int i = 0; i < kRows; ++i) {
     const int tr = warp + i * NW;
     const int gy = y0 - 2 + tr;
-    const bool row_ok = tr < kTileH && tr <= B + 3 && gy >= 0 && gy < H;
-    const T* row = u + static_cast<size_t>(row_ok ? gy : 0) * Wz;
+    const bool row_ok = tr < kTileH && tr <= B + 3 && gy >= row_lo && gy < row_hi;
+    const T* row = u + static_cast<size_t>(row_ok ? gy : row_lo) * Wz;  // a stored row
     v[i] = (row_ok && col_ok) ? row[gx] : T(0);
     e[i] = (row_ok && ecol_ok) ? row[ex] : T(0);
   }
@@ -259,8 +265,10 @@ __device__ __forceinline__ void load_rows(const Cell<T, R>& c, uint64_t& kbits, 
     const int ly = c.row0 - 1 + j;
     const int gy = c.y0 + ly;
     const bool in_blk = c.col_ok && ly >= 0 && ly < c.B;
-    const size_t p = in_blk ? static_cast<size_t>(gy) * W + c.gx : 0;
-    const uint8_t mv = c.mask[p];  // unconditional: issued together
+    // lanes outside the block read the block's first pixel (always stored,
+    // also under stripe storage), so every load is issued unconditionally
+    const size_t p = in_blk ? static_cast<size_t>(gy) * W + c.gx : static_cast<size_t>(c.y0) * W + c.x0;
+    const uint8_t mv = c.mask[p];
     kbits |= static_cast<uint64_t>(in_blk && mv != 0) << j;
     if (!INV) {
       const T bb = c.b[p];
@@ -410,14 +418,14 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
       if (tid == 0) {
         mbar_init(&S.bar, 1);
         mbar_expect_tx(&S.bar, sizeof(S.ut));
-        tma_load_3d(&S.ut[0][0], &a.umap, c.x0 - c.tl, c.y0 - 2, ch, &S.bar);
+        tma_load_3d(&S.ut[0][0], &a.umap, c.x0 - c.tl, c.y0 - 2 - a.srow_lo, ch, &S.bar);
       }
       load_rows<T, R, INV>(c, kb, bv);
       __syncthreads();
       mbar_wait(&S.bar, 0);
     } else {
       load_rows<T, R, INV>(c, kb, bv);
-      stage_u_tile<T, NW>(S.ut, c.u, c.x0, c.y0, B, c.W, c.H);
+      stage_u_tile<T, NW>(S.ut, c.u, c.x0, c.y0, B, c.W, a.srow_lo, a.srow_hi);
       __syncthreads();
     }
 #ifdef SI_PROBE_SETUP
@@ -658,7 +666,8 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
     const int ly = c.row0 + i;
     const int gy = c.y0 + ly;
     const bool own = col_own && ly < B && gy >= oy0 && gy < oy1;
-    const size_t pix = own ? static_cast<size_t>(gy) * c.W + c.gx : 0;
+    const size_t pix = own ? static_cast<size_t>(gy) * c.W + c.gx
+                           : static_cast<size_t>(c.y0) * c.W + c.x0;  // a stored pixel
     const T uo = S.ut[ly + 2][lane + c.tl];
     T v = static_cast<T>(x[i]);
     if (!c.known_invariant) {

@@ -1,360 +1,168 @@
 """One very large image over G GPUs: horizontal stripes with halo exchange
-(BASELINE.json configs[4]).
+(BASELINE.json configs[4]) -- Python mirror of the C ABI.
 
-Every level of the pyramid is split by block rows of its own (clamped)
-partition: rank g owns block rows [k0, k1) and the pixel rows those blocks own
-(`si_stripe_plan`).  Each rank keeps full-size level buffers but only computes
-its stripe, so the per-block arithmetic is identical to the single-GPU solve
-and the result is bit-identical to it whenever the stop decisions agree (the
-only difference is the summation order of the global residual norm).
+The solve itself is C++ and CUDA (`csrc/stripes.cuh`, `si_run_method_striped*`):
+every pyramid level is split into G stripes of whole block rows of that
+level's own partition (partition_domain, partition.hpp:46-106); each rank
+allocates, ingests, restricts, sweeps and prolongs only its rows (plus
+halos).  Per outer iteration (run_schwarz_level, schwarz.hpp:288-320) the
+G x C partial residual sums are all-gathered, every rank takes the same stop
+decision (fixed rank order), sweeps its block rows and exchanges halo rows
+with the owners.  The image equals the single-GPU solve bit for bit whenever
+the stop decisions agree.
 
-Per outer iteration of a level (run_schwarz_level, schwarz.hpp:288-320):
-  1. partial per-channel sums of (b - A u)^2 over the owned rows,
-  2. all-reduce(sum) -> every rank takes the same rel <= tol decision,
-  3. sweep of the owned block rows (u_old -> u_new on owned rectangles),
-  4. halo exchange: the window rows owned by the neighbours g-1 / g+1.
-Between levels the coarse iterate is all-gathered (coarse levels are 4x and
-16x smaller), then prolongated and snapped locally.
-
-The orchestration is written once against two small interfaces:
-  * a communicator (`TorchComm` over torch.distributed — NCCL on B200s, gloo on
-    CPU — or `ThreadComm`, G ranks as threads of one process), and
-  * a compute backend (`DeviceBackend`: the CUDA kernels of libschwarz_b200.so
-    on torch CUDA tensors; the CPU tests plug in a numpy/oracle backend).
+Communicators:
+  * `nccl_comm(solver, dist)`: one process per GPU; rank 0 makes the NCCL
+    id, torch.distributed broadcasts it, the library drives NCCL
+    (ncclAllGather + grouped ncclSend/ncclRecv on the solve stream);
+  * `local_comms(solvers)`: G ranks as host threads of this process (any
+    devices, including G ranks on one GPU); device copies ordered by events.
 """
 from __future__ import annotations
 
 import ctypes as C
 import threading
 from dataclasses import dataclass
-from typing import List, Optional
+from typing import List, Optional, Sequence
 
 import numpy as np
 
 from . import _lib as L
-from .api import RunOptions, _check
+from .api import (ConvergenceTrace, ImageBuffer, InpaintingMask, InvalidArgument, Method,
+                  RunOptions, SolveResult, Solver, _check, _report, _require_same_grid)
+
+PLAN_INTS = 12
 
 
 @dataclass
-class StripePlan:
-    blocks_y: int
+class StripeLevel:
+    """Rows of one level held by one rank (global row coordinates)."""
     k0: int
-    k1: int
+    k1: int            # block rows [k0, k1)
     own_lo: int
-    own_hi: int
+    own_hi: int        # rows the rank owns (owned rows of all ranks tile the level)
     win_lo: int
-    win_hi: int
-    valid: bool
+    win_hi: int        # rows its sweeps and residual stencil read
+    need_lo: int
+    need_hi: int       # rows of this level its prolongation onto the finer window reads
+    store_lo: int
+    store_hi: int      # rows it allocates / ingests / restricts
+    block: int
+    overlap: int       # clamped partition (multilevel.hpp:146-150)
 
 
-def stripe_plan(h: int, block: int, overlap: int, world: int, rank: int) -> StripePlan:
-    out = (C.c_int * 8)()
-    _check(L.load().si_stripe_plan(h, block, overlap, world, rank, out))
-    return StripePlan(*out[:7], bool(out[7]))
+def level_plan(method: Method, w: int, h: int, c: int, options: Optional[RunOptions],
+               world: int, rank: int) -> List[StripeLevel]:
+    """si_stripe_level_plan: the decomposition the C++ executor uses (index 0 =
+    finest).  Host only."""
+    o = (options or RunOptions()).to_c()
+    depth = C.c_int()
+    out = (C.c_int * (L.SI_MAX_LEVELS * PLAN_INTS))()
+    _check(L.load().si_stripe_level_plan(int(method), w, h, c, C.byref(o), world, rank,
+                                         C.byref(depth), out))
+    return [StripeLevel(*out[l * PLAN_INTS:(l + 1) * PLAN_INTS]) for l in range(depth.value)]
 
 
-def clamped(w: int, h: int, block: int, overlap: int):
-    """clamped_partition (multilevel.hpp:146-150)."""
-    be = min(block, min(w, h))
-    return be, max(0, min(overlap, be - 1))
+class StripeComm:
+    """Owns an si_stripe_comm handle."""
 
-
-def level_shapes(w: int, h: int, levels: int):
-    """build_pyramid's level sizes (multilevel.hpp:90-93)."""
-    shapes = [(w, h)]
-    while len(shapes) < levels:
-        cw, ch = shapes[-1]
-        if cw < 2 or ch < 2:
-            break
-        shapes.append(((cw + 1) // 2, (ch + 1) // 2))
-    return shapes
-
-
-def joint_norm(sums) -> float:
-    """sqrt(sum_c sqrt(s_c)^2) with the reference's fma accumulate
-    (schwarz.hpp:290-295), computed by the library's host code."""
-    arr = np.ascontiguousarray(sums, dtype=np.float64)
-    return L.load().si_joint_norm(arr.ctypes.data_as(C.POINTER(C.c_double)), arr.size)
-
-
-# ----------------------------------------------------------------- communicators
-class TorchComm:
-    """torch.distributed (NCCL between B200s, gloo on CPU)."""
-
-    def __init__(self, dist, device=None):
-        self.dist = dist
-        self.rank = dist.get_rank()
-        self.world = dist.get_world_size()
-        self.device = device
-
-    def allreduce_sum(self, vals: np.ndarray) -> np.ndarray:
-        import torch
-        t = torch.tensor(vals, dtype=torch.float64, device=self.device)
-        self.dist.all_reduce(t)
-        return t.cpu().numpy()
-
-    def exchange(self, sends: dict, recv_shapes: dict, like):
-        """sends: {peer: tensor}; recv_shapes: {peer: shape} -> {peer: tensor}."""
-        ops, out = [], {}
-        for peer, shape in recv_shapes.items():
-            out[peer] = like.new_empty(shape)
-            ops.append(self.dist.P2POp(self.dist.irecv, out[peer], peer))
-        for peer, t in sends.items():
-            ops.append(self.dist.P2POp(self.dist.isend, t.contiguous(), peer))
-        if ops:
-            for req in self.dist.batch_isend_irecv(ops):
-                req.wait()
-        return out
-
-    def allgather_rows(self, arr, lo: int, hi: int, spans):
-        """Fill rows [lo_r, hi_r) of every rank r into arr (C, H, W) in place."""
-        import torch
-        parts = []
-        for r, (a, b) in enumerate(spans):
-            parts.append(arr[:, a:b, :].contiguous() if r == self.rank else
-                         arr.new_empty((arr.shape[0], b - a, arr.shape[2])))
-        for r, (a, b) in enumerate(spans):
-            if b > a:
-                self.dist.broadcast(parts[r], src=r)
-                if r != self.rank:
-                    arr[:, a:b, :] = parts[r]
-        return arr
-
-
-class ThreadComm:
-    """G ranks as threads of one process (single GPU or CPU emulation)."""
-
-    class _Shared:
-        def __init__(self, world):
-            self.world = world
-            self.barrier = threading.Barrier(world)
-            self.slots = {}
-
-    def __init__(self, shared: "ThreadComm._Shared", rank: int):
-        self.s = shared
+    def __init__(self, handle, world: int, rank: int, kind: str):
+        self.handle = handle
+        self.world = world
         self.rank = rank
-        self.world = shared.world
+        self.kind = kind
 
-    @classmethod
-    def group(cls, world: int) -> List["ThreadComm"]:
-        sh = cls._Shared(world)
-        return [cls(sh, r) for r in range(world)]
+    def close(self):
+        if self.handle:
+            L.load().si_stripe_comm_destroy(self.handle)
+            self.handle = None
 
-    def _publish(self, key, value):
-        self.s.slots[(key, self.rank)] = value
-        self.s.barrier.wait()
-
-    def _done(self):
-        self.s.barrier.wait()
-
-    def allreduce_sum(self, vals: np.ndarray) -> np.ndarray:
-        self._publish("ar", np.asarray(vals, dtype=np.float64).copy())
-        tot = np.zeros_like(np.asarray(vals, dtype=np.float64))
-        for r in range(self.world):  # fixed order: identical on every rank
-            tot = tot + self.s.slots[("ar", r)]
-        self._done()
-        return tot
-
-    def exchange(self, sends: dict, recv_shapes: dict, like):
-        self._publish("x", {peer: _copy(t) for peer, t in sends.items()})
-        out = {peer: self.s.slots[("x", peer)][self.rank] for peer in recv_shapes}
-        self._done()
-        return out
-
-    def allgather_rows(self, arr, lo: int, hi: int, spans):
-        self._publish("ag", _copy(arr[:, lo:hi, :]))
-        for r, (a, b) in enumerate(spans):
-            if r != self.rank and b > a:
-                arr[:, a:b, :] = self.s.slots[("ag", r)]
-        self._done()
-        return arr
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
-def _copy(t):
-    return t.clone() if hasattr(t, "clone") else np.array(t, copy=True)
+def nccl_comm(solver: Solver, dist, device=None) -> StripeComm:
+    """NCCL communicator over the ranks of torch.distributed `dist` (one
+    process per GPU): rank 0's id is broadcast through `dist`."""
+    import torch
+    lib = L.load()
+    world, rank = dist.get_world_size(), dist.get_rank()
+    idbuf = (C.c_ubyte * L.SI_NCCL_ID_BYTES)()
+    if rank == 0:
+        _check(lib.si_nccl_unique_id(idbuf))
+    dev = device if device is not None else (
+        torch.device("cuda", solver.device) if dist.get_backend() == "nccl" else None)
+    t = torch.tensor(list(bytes(idbuf)), dtype=torch.uint8, device=dev)
+    dist.broadcast(t, src=0)
+    idbuf = (C.c_ubyte * L.SI_NCCL_ID_BYTES)(*t.cpu().tolist())
+    h = C.c_void_p()
+    _check(lib.si_stripe_comm_init_nccl(solver.handle, world, rank, idbuf, C.byref(h)))
+    return StripeComm(h, world, rank, "nccl")
 
 
-# ----------------------------------------------------------------- device backend
-class DeviceBackend:
-    """The CUDA kernels of libschwarz_b200.so on torch CUDA tensors."""
-
-    def __init__(self, solver, precision: int = 0, stream=None):
-        import torch
-        self.torch = torch
-        self.solver = solver
-        self.lib = solver._lib
-        self.h = solver.handle
-        self.precision = precision
-        self.dtype = torch.float64 if precision == 0 else torch.float32
-        self.dev = torch.device("cuda", solver.device)
-        self.stream = stream
-
-    def _pre(self):
-        # torch work issued by the orchestrator (copies, halo writes) is on
-        # torch's current stream; the library runs on its own stream and
-        # returns synchronised, so ordering needs only this wait.
-        self.torch.cuda.current_stream(self.dev).synchronize()
-
-    def empty(self, c, h, w):
-        return self.torch.empty((c, h, w), dtype=self.dtype, device=self.dev)
-
-    def empty_mask(self, h, w):
-        return self.torch.empty((h, w), dtype=self.torch.uint8, device=self.dev)
-
-    def ingest(self, f, mask):
-        self._pre()
-        c, h, w = f.shape
-        b = self.empty(c, h, w)
-        known = C.c_longlong()
-        _check(self.lib.si_device_ingest(self.h, f.data_ptr(), mask.data_ptr(), w, h, c,
-                                         self.precision, b.data_ptr(), C.byref(known),
-                                         self.stream))
-        return b, known.value
-
-    def restrict(self, mask, vals, averaging):
-        self._pre()
-        c, h, w = vals.shape
-        cw, ch = (w + 1) // 2, (h + 1) // 2
-        cm, cv = self.empty_mask(ch, cw), self.empty(c, ch, cw)
-        _check(self.lib.si_device_restrict(self.h, mask.data_ptr(), vals.data_ptr(), w, h, c,
-                                           averaging, self.precision, cm.data_ptr(),
-                                           cv.data_ptr(), self.stream))
-        return cm, cv
-
-    def prolong_snap(self, coarse, fmask, fvals):
-        self._pre()
-        c, ch, cw = coarse.shape
-        _, fh, fw = fvals.shape
-        fine = self.empty(c, fh, fw)
-        _check(self.lib.si_device_prolong_snap(self.h, coarse.data_ptr(), cw, ch, fw, fh, c,
-                                               fmask.data_ptr(), fvals.data_ptr(), self.precision,
-                                               fine.data_ptr(), self.stream))
-        return fine
-
-    def residual_rows(self, mask, u, b, row0, row1, mode=0):
-        self._pre()
-        c, h, w = u.shape
-        sums = np.zeros(c)
-        _check(self.lib.si_device_residual_rows(self.h, mask.data_ptr(), u.data_ptr(),
-                                                b.data_ptr(), w, h, c, row0, row1, mode, 1,
-                                                self.precision,
-                                                sums.ctypes.data_as(C.POINTER(C.c_double)),
-                                                self.stream))
-        return sums
-
-    def sweep_rows(self, mask, b, u_old, u_new, block, overlap, by0, by1, flavour, opts):
-        self._pre()
-        c, h, w = u_old.shape
-        o = opts.to_c()
-        fails, its = C.c_longlong(), C.c_longlong()
-        _check(self.lib.si_device_sweep_rows(self.h, mask.data_ptr(), b.data_ptr(),
-                                             u_old.data_ptr(), u_new.data_ptr(), w, h, c, block,
-                                             overlap, by0, by1, flavour, C.byref(o), 1,
-                                             C.byref(fails), C.byref(its), self.stream))
-        return fails.value, its.value
-
-    def copy(self, t):
-        return t.clone()
+def local_comms(solvers: Sequence[Solver]) -> List[StripeComm]:
+    """G = len(solvers) ranks as threads of this process (rank r on solvers[r])."""
+    world = len(solvers)
+    ctxs = (C.c_void_p * world)(*[s.handle for s in solvers])
+    hs = (C.c_void_p * world)()
+    _check(L.load().si_stripe_comm_init_local(ctxs, world, hs))
+    return [StripeComm(C.c_void_p(hs[r]), world, r, "local") for r in range(world)]
 
 
-# ----------------------------------------------------------------- the solve
-@dataclass
-class StripeReport:
-    level_iterations: List[int]
-    trace: List[float]
-    converged: bool
-    local_failures: int
-    local_cg_iterations: int
-    plans: List[StripePlan]
+def run_method_striped(solver: Solver, comm: StripeComm, method: Method, f: ImageBuffer,
+                       mask: InpaintingMask, options: Optional[RunOptions] = None,
+                       out: Optional[ImageBuffer] = None, trace: Optional[ConvergenceTrace] = None
+                       ) -> SolveResult:
+    """Collective run_method over comm's ranks (every rank calls it with the
+    full host image; only its rows are uploaded).  The returned image holds
+    this rank's own finest rows (others untouched); the report carries the
+    global counts."""
+    options = options or RunOptions()
+    _require_same_grid(f, mask)
+    out = out or ImageBuffer(data=np.zeros_like(f.data))
+    if out.data.shape != f.data.shape:
+        raise InvalidArgument("run_method_striped: output shape differs from the image")
+    rep = L.si_report()
+    o = options.to_c()
+    tr = trace if trace is not None else ConvergenceTrace()
+    cb = Solver._sink(tr, False)
+    _check(L.load().si_run_method_striped(solver.handle, comm.handle, int(method),
+                                          f.data.ctypes.data, mask.known.ctypes.data, f.width,
+                                          f.height, f.channels, C.byref(o), out.data.ctypes.data,
+                                          C.byref(rep), cb, None))
+    return SolveResult(out, tr, _report(rep))
 
 
-def solve_striped(f, mask, comm, backend, options: Optional[RunOptions] = None,
-                  flavour: int = 1):
-    """multilevel_solve (multilevel.hpp:239-310) with every level striped over
-    comm.world ranks.  f: (C, H, W) float64 and mask (H, W) uint8 on the
-    backend's device, replicated on every rank.  Returns (u, report): u holds
-    the finest solution on the rank's owned rows; use gather_full() for all."""
-    o = options or RunOptions()
-    C_, H, W = f.shape
-    shapes = level_shapes(W, H, o.levels)
-    depth = len(shapes)
-    b0, known = backend.ingest(f, mask)
-    if known == 0:
-        raise ValueError("build_rhs: mask has no known pixels")
-    masks, vals = [mask], [b0]
-    for l in range(1, depth):
-        cm, cv = backend.restrict(masks[-1], vals[-1], int(o.averaging))
-        masks.append(cm)
-        vals.append(cv)
-    rep = StripeReport([0] * depth, [], False, 0, 0, [])
-    u = None
-    for level in range(depth - 1, -1, -1):
-        w, h = shapes[level]
-        be, oe = clamped(w, h, o.block_size, o.overlap)
-        plan = stripe_plan(h, be, oe, comm.world, comm.rank)
-        if not plan.valid:
-            raise ValueError(f"level {level}: stripes too thin for {comm.world} ranks")
-        rep.plans.insert(0, plan)
-        m, b = masks[level], vals[level]
-        if level == depth - 1:
-            u = backend.copy(b)  # canonical start u0 = b (multilevel.hpp:267-273)
-        finest = level == 0
-        tol = o.tolerance if finest else o.coarse_tolerance
-        plans = [stripe_plan(h, be, oe, comm.world, r) for r in range(comm.world)]
-        spans = [(p.own_lo, p.own_hi) for p in plans]
-        r0 = joint_norm(comm.allreduce_sum(
-            backend.residual_rows(m, b, b, plan.own_lo, plan.own_hi,
-                                  1 if int(o.normalizer) == 1 else 0)))
-        u_alt = backend.copy(u)
-        outer = 0
-        while True:
-            sums = comm.allreduce_sum(backend.residual_rows(m, u, b, plan.own_lo, plan.own_hi))
-            rel = joint_norm(sums) / r0 if r0 > 0 else 0.0
-            if finest:
-                rep.trace.append(rel)
-            rep.level_iterations[level] = outer
-            if rel <= tol:
-                if finest:
-                    rep.converged = True
-                break
-            if outer >= o.max_outer_iterations:
-                break
-            fails, its = backend.sweep_rows(m, b, u, u_alt, be, oe, plan.k0, plan.k1, flavour, o)
-            rep.local_failures += fails
-            rep.local_cg_iterations += its
-            u, u_alt = u_alt, u
-            _exchange_halos(comm, u, plans)
-            outer += 1
-        if not finest:
-            comm.allgather_rows(u, plan.own_lo, plan.own_hi, spans)
-            fw, fh = shapes[level - 1]
-            u = backend.prolong_snap(u, masks[level - 1], vals[level - 1])
-    return u, rep
+def run_method_striped_device(solver: Solver, comm: StripeComm, method: Method, f_rows_ptr: int,
+                              mask_rows_ptr: int, w: int, h: int, c: int, out_rows_ptr: int,
+                              options: Optional[RunOptions] = None, stream=None):
+    """Device-resident: rows [store_lo, store_hi) of f / mask in, rows
+    [own_lo, own_hi) of the result out (level_plan(...)[0])."""
+    options = options or RunOptions()
+    rep = L.si_report()
+    o = options.to_c()
+    _check(L.load().si_run_method_striped_device(solver.handle, comm.handle, int(method),
+                                                 f_rows_ptr, mask_rows_ptr, w, h, c, C.byref(o),
+                                                 out_rows_ptr, C.byref(rep), stream))
+    return _report(rep)
 
 
-def _exchange_halos(comm, u, plans: List[StripePlan]):
-    """Rows of my window owned by rank-1 / rank+1 come from them; I send them
-    the rows I own inside their windows (stripe_plan guarantees no other rank
-    is involved)."""
-    r = comm.rank
-    me = plans[r]
-    sends, recv = {}, {}
-    for peer in (r - 1, r + 1):
-        if not 0 <= peer < comm.world:
-            continue
-        pp = plans[peer]
-        lo, hi = max(pp.win_lo, me.own_lo), min(pp.win_hi, me.own_hi)
-        if hi > lo:
-            sends[peer] = u[:, lo:hi, :]
-        lo2, hi2 = max(me.win_lo, pp.own_lo), min(me.win_hi, pp.own_hi)
-        if hi2 > lo2:
-            recv[peer] = (lo2, hi2)
-    got = comm.exchange(sends, {p: (u.shape[0], b - a, u.shape[2]) for p, (a, b) in recv.items()},
-                        u)
-    for p, (a, b) in recv.items():
-        u[:, a:b, :] = got[p]
-
-
-def gather_full(comm, u, plan: StripePlan, spans):
-    """All ranks end with the full finest image."""
-    return comm.allgather_rows(u, plan.own_lo, plan.own_hi, spans)
+def run_method_striped_group(solvers: Sequence[Solver], method: Method, f: ImageBuffer,
+                             mask: InpaintingMask, options: Optional[RunOptions] = None):
+    """G = len(solvers) ranks as threads of this process: the whole image and
+    every rank's report."""
+    options = options or RunOptions()
+    _require_same_grid(f, mask)
+    world = len(solvers)
+    out = ImageBuffer(data=np.zeros_like(f.data))
+    ctxs = (C.c_void_p * world)(*[s.handle for s in solvers])
+    reps = (L.si_report * world)()
+    o = options.to_c()
+    _check(L.load().si_run_method_striped_group(ctxs, world, int(method), f.data.ctypes.data,
+                                                mask.known.ctypes.data, f.width, f.height,
+                                                f.channels, C.byref(o), out.data.ctypes.data,
+                                                reps))
+    return out, [_report(reps[r]) for r in range(world)]

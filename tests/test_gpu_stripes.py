@@ -1,0 +1,175 @@
+"""GPU: the C++ stripe engine (csrc/stripes.cuh, BASELINE configs[4]).
+
+G ranks run as host threads of this process on ONE B200 over the local
+communicator (device copies ordered by events: no kernel waits on another
+rank's kernel).  Every case must reproduce the single-GPU run_method:
+  * per-level outer counts, local solves and local failures equal;
+  * the image bit-identical (the only difference is the summation order of
+    the global residual norm, which can only change a stop decision at the
+    threshold itself);
+  * trace rows within 1e-12 relative.
+The single-GPU solve is itself pinned to the reference (test_gpu_headline.py).
+"""
+import numpy as np
+import pytest
+
+import paper_2110_03946_b200 as si
+from paper_2110_03946_b200 import stripes as S
+
+pytestmark = pytest.mark.gpu
+
+_SOLVERS = []
+
+
+def solvers(n):
+    while len(_SOLVERS) < n:
+        _SOLVERS.append(si.Solver(0))
+    return _SOLVERS[:n]
+
+
+def check_same(single, img, reps, G):
+    for r in reps:
+        assert list(r.level_iterations) == list(single.report.level_iterations)
+        assert r.iterations == single.report.iterations
+        assert r.converged == single.report.converged
+        assert r.local_solves == single.report.local_solves
+        assert r.local_failures == single.report.local_failures
+        assert r.local_cg_iterations == single.report.local_cg_iterations
+        assert abs(r.final_relative_residual - single.report.final_relative_residual) <= \
+            1e-12 * abs(single.report.final_relative_residual) + 1e-18
+    assert np.array_equal(img.data, single.image.data), np.abs(img.data - single.image.data).max()
+
+
+CASES = [
+    # w, h, c, density, method, options
+    (640, 480, 3, 0.05, si.Method.MultilevelOras, dict(levels=3)),
+    (1000, 600, 3, 0.04, si.Method.MultilevelOras, dict(tolerance=1e-6)),
+    (777, 333, 3, 0.04, si.Method.MultilevelOras, dict()),          # odd widths: cp.async paths
+    (512, 700, 1, 0.03, si.Method.Oras, dict(tolerance=1e-5)),
+    (400, 300, 2, 0.05, si.Method.Ras, dict(tolerance=1e-5)),
+    (300, 200, 3, 0.05, si.Method.MultilevelOras, dict(block_size=16, overlap=3, levels=4)),
+    (260, 190, 3, 0.04, si.Method.MultilevelOras, dict(block_size=64, overlap=10)),  # K2g
+    (640, 360, 3, 0.04, si.Method.MultilevelOras, dict(precision=si.Precision.FP32)),
+    (640, 360, 3, 0.04, si.Method.MultilevelOras, dict(precision=si.Precision.MIXED)),
+    (200, 150, 3, 0.05, si.Method.MultilevelOras,
+     dict(averaging=si.CoarseAveraging.AllPixels, normalizer=si.ResidualNormalizer.RhsNorm)),
+]
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_striped_group_matches_single_gpu(solver, case, G):
+    w, h, c, d, method, kw = CASES[case]
+    f = si.synthetic_test_image(w, h, c, 100 + case)
+    m = si.random_mask(w, h, d, 200 + case)
+    o = si.RunOptions(**kw)
+    single = solver.run_method(method, f, m, o)
+    img, reps = S.run_method_striped_group(solvers(G), method, f, m, o)
+    check_same(single, img, reps, G)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_c5_striped_matches_single_gpu(solver, G):
+    """configs[4]: 7680x4320 RGB, 2% (0 finest sweeps)."""
+    f = si.synthetic_test_image(7680, 4320, 3, 7)
+    m = si.random_mask(7680, 4320, 0.02, 11)
+    o = si.RunOptions(levels=3)
+    single = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    img, reps = S.run_method_striped_group(solvers(G), si.Method.MultilevelOras, f, m, o)
+    check_same(single, img, reps, G)
+
+
+@pytest.mark.parametrize("G", [2, 8])
+def test_c5_forced_sweeps_striped_matches_single_gpu(solver, G):
+    """configs[4] forced-sweep variant: two sweeps on every level, so the
+    finest-level halo exchange runs."""
+    f = si.synthetic_test_image(7680, 4320, 3, 7)
+    m = si.random_mask(7680, 4320, 0.02, 11)
+    o = si.RunOptions(levels=3, tolerance=1e-12, max_outer_iterations=2)
+    single = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    assert single.report.level_iterations[0] == 2
+    img, reps = S.run_method_striped_group(solvers(G), si.Method.MultilevelOras, f, m, o)
+    check_same(single, img, reps, G)
+
+
+def test_more_ranks_than_block_rows(solver):
+    """Ranks without blocks on a level still join every collective."""
+    f = si.synthetic_test_image(96, 70, 2, 3)
+    m = si.random_mask(96, 70, 0.08, 4)
+    o = si.RunOptions(levels=3)
+    single = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    img, reps = S.run_method_striped_group(solvers(8), si.Method.MultilevelOras, f, m, o)
+    check_same(single, img, reps, 8)
+
+
+def test_nccl_comm_single_rank(solver):
+    """The NCCL communicator at world 1 (the only NCCL shape one GPU can run:
+    ranks of a multi-rank NCCL group would wait on each other's kernels)."""
+    import ctypes as C
+    import torch  # noqa: F401  (its NCCL is loaded first and reused by the library)
+    from paper_2110_03946_b200 import _lib as L
+    lib = L.load()
+    idbuf = (C.c_ubyte * L.SI_NCCL_ID_BYTES)()
+    assert lib.si_nccl_unique_id(idbuf) == 0
+    h = C.c_void_p()
+    assert lib.si_stripe_comm_init_nccl(solver.handle, 1, 0, idbuf, C.byref(h)) == 0, \
+        lib.si_last_error()
+    comm = S.StripeComm(h, 1, 0, "nccl")
+    f = si.synthetic_test_image(640, 480, 3, 9)
+    m = si.random_mask(640, 480, 0.05, 10)
+    o = si.RunOptions(levels=3, tolerance=1e-5)
+    single = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    res = S.run_method_striped(solver, comm, si.Method.MultilevelOras, f, m, o)
+    check_same(single, res.image, [res.report], 1)
+    assert len(res.trace.rows) == single.report.iterations + 1
+    comm.close()
+
+
+def test_striped_device_entry_rows(solver):
+    """si_run_method_striped_device: store rows in, own rows out, on a
+    2-rank local group driven from two threads."""
+    import threading
+    import torch
+    w, h, c = 640, 480, 3
+    f = si.synthetic_test_image(w, h, c, 31)
+    m = si.random_mask(w, h, 0.05, 32)
+    o = si.RunOptions(levels=3)
+    single = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    sv = solvers(2)
+    comms = S.local_comms(sv)
+    out = np.zeros_like(f.data)
+    reps = [None, None]
+
+    def rank(r):
+        pl = S.level_plan(si.Method.MultilevelOras, w, h, c, o, 2, r)[0]
+        df = torch.from_numpy(np.ascontiguousarray(f.data[:, pl.store_lo:pl.store_hi])).cuda()
+        dm = torch.from_numpy(np.ascontiguousarray(m.known[pl.store_lo:pl.store_hi])).cuda()
+        do = torch.empty((c, pl.own_hi - pl.own_lo, w), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        reps[r] = S.run_method_striped_device(sv[r], comms[r], si.Method.MultilevelOras,
+                                              df.data_ptr(), dm.data_ptr(), w, h, c,
+                                              do.data_ptr(), o)
+        out[:, pl.own_lo:pl.own_hi] = do.cpu().numpy()
+
+    ts = [threading.Thread(target=rank, args=(r,)) for r in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for cm in comms:
+        cm.close()
+    check_same(single, si.ImageBuffer(data=out), reps, 2)
+
+
+def test_cg_methods_are_not_striped(solver):
+    f = si.synthetic_test_image(64, 64, 1, 1)
+    m = si.random_mask(64, 64, 0.05, 2)
+    with pytest.raises(si.SolverError):
+        S.run_method_striped_group(solvers(2), si.Method.MultilevelCg, f, m, si.RunOptions())
+
+
+def test_empty_mask_fails_on_every_rank(solver):
+    f = si.synthetic_test_image(64, 64, 1, 1)
+    m = si.InpaintingMask(64, 64, 0)
+    with pytest.raises(si.InvalidArgument, match="no known pixels"):
+        S.run_method_striped_group(solvers(2), si.Method.MultilevelOras, f, m, si.RunOptions())
