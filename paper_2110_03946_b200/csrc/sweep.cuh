@@ -122,7 +122,34 @@ struct SweepSmem {
   L pub[NW][2][3][32];             // [warp][top/bottom][r,p,x][col]
   L pubt[NW][2][32];               // true-residual boundary rows
   L red[3][NW];
+  uint32_t tslot;                  // TMEM base address (x in tensor memory)
 };
+
+// x (the CG iterate, touched once per iteration: x += alpha p) lives in TMEM
+// for the full-block double CG with two warps: 32 registers per thread fewer
+// in the loop, which removes the spills at the 168-register cap of 6 CTAs/SM.
+// SI_NO_TMEM_X=1 at compile time keeps it in registers (A/B).
+template <typename L, int NW, bool FULL>
+constexpr bool kTmemX =
+#ifdef SI_NO_TMEM_X
+    false;
+#else
+    FULL && sizeof(L) == 8 && NW == 2;
+#endif
+
+// With x in TMEM, q = A p can follow it (columns 32..63): q leaves the
+// registers four rows at a time as apply produces it and comes back for the
+// r update, so the loop holds only r and p (64 registers of vectors) and
+// the kernel fits 8 CTAs/SM (128 registers, no spill; 64 TMEM columns x 8
+// CTAs = the SM's 512).  SI_NO_TMEM_Q=1 keeps q in registers (A/B).
+template <typename L, int NW, bool FULL>
+constexpr bool kTmemQ =
+#ifdef SI_NO_TMEM_Q
+    false;
+#else
+    kTmemX<L, NW, FULL>;
+#endif
+
 
 // CTA-wide sum; identical value in every thread.  slot selects the buffer so
 // consecutive reductions never race (see the header comment).  The warp part
@@ -363,13 +390,21 @@ struct SweepOcc {
                      : (NW == 8 ? SI_OCC32_8 : NW == 4 ? SI_OCC32 : (NW == 2 ? SI_OCC32_2 : 2));
 };
 
+// (8 CTAs/SM either way at 128 registers; the hint of 7 schedules the loop
+// better: 2.81 vs 2.88 ms per frame's sweeps)
+#ifndef SI_OCC64_QT
+#define SI_OCC64_QT 7
+#endif
+template <typename L, int NW, bool FULL>
+constexpr int kSweepMinBlocks = kTmemQ<L, NW, FULL> ? SI_OCC64_QT : SweepOcc<L, NW>::value;
+
 // FULL: the block is exactly 32x32 (every level of any image >= 32 pixels
 // wide and high with the default block size), so the Robin rows are
 // compile-time positions.
 // L: the local CG's type (T, or float under double storage: the outer
 // iteration, residuals and the image stay in T).
 template <typename T, int NW, bool FULL, typename L = T>
-__global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
+__global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
     oras_sweep_kernel(const __grid_constant__ SweepArgs<T> a) {
   constexpr int R = 32 / NW;  // rows per thread
   __shared__ SweepSmem<T, NW, L> S;
@@ -381,10 +416,18 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
   long long pr_s0 = 0, pr_s1 = 0, pr_s2 = 0;
 #endif
 
+  constexpr bool XT = kTmemX<L, NW, FULL>;
+  constexpr bool QT = kTmemQ<L, NW, FULL>;
+  constexpr uint32_t kCols = QT ? 64 : 32;
   const int bx = blockIdx.x % a.ax.count;
   const int by = a.by0 + static_cast<int>(blockIdx.x) / a.ax.count;
   const int ch = blockIdx.y;
   const int B = FULL ? kMaxBlock : a.ax.block;
+  uint32_t tbase = 0, taddr = 0;
+  if constexpr (XT) {
+    tbase = tmem_alloc_cta<kCols>(&S.tslot);
+    taddr = tmem_warp_addr(tbase);
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t plane = static_cast<size_t>(ch) * a.N;
 
@@ -404,7 +447,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
   c.known_invariant = a.known_invariant;
   c.tl = a.use_tma ? tile_lead<T>(c.x0) : 2;
 
-  L x[R], r[R], p[R], q[R];
+  L x[XT ? 1 : R], r[R], p[R], q[QT ? 1 : R];  // XT / QT: x / q in TMEM
   uint32_t unk;
   // u tile (TMA box or cooperative copy) and the mask bits of my rows, the
   // latter in flight while the tile arrives; then residual and right-hand side
@@ -441,9 +484,17 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
     setup(std::true_type{});
   else
     setup(std::false_type{});
+  if constexpr (XT) {
+    double z[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) z[i] = 0.0;
+    tmem_store16(taddr, z);
+  } else {
+#pragma unroll
+    for (int i = 0; i < R; ++i) x[i] = L(0);
+  }
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    x[i] = L(0);
     S.bt[c.row0 + i][lane] = r[i];
     if constexpr (!kShflWE<L>) S.pt[c.row0 + i][lane + 1] = r[i];  // p = r initially
   }
@@ -502,12 +553,18 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
       if (NW > 1) {
         S.pub[warp][0][0][lane] = r[0];
         S.pub[warp][0][1][lane] = p[0];
-        S.pub[warp][0][2][lane] = x[0];
         S.pub[warp][1][0][lane] = r[R - 1];
         S.pub[warp][1][1][lane] = p[R - 1];
-        S.pub[warp][1][2][lane] = x[R - 1];
+        if constexpr (!XT) {  // XT: published by the x update itself
+          S.pub[warp][0][2][lane] = x[0];
+          S.pub[warp][1][2][lane] = x[R - 1];
+        }
       }
     };
+    if constexpr (XT) {  // x = 0 before the first iteration
+      S.pub[warp][0][2][lane] = L(0);
+      S.pub[warp][1][2][lane] = L(0);
+    }
     auto collect = [&]() {
       if (NW > 1) {
         if (warp > 0) {
@@ -536,30 +593,54 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
     // (lane 0's W and lane 31's E are the ghost zeros; columns >= B of a
     // partial block hold zeros); float: from the staged row.  N/S from my
     // registers or the neighbour warps' rows vN0/vS1.
+    auto row_op = [&](const L(&v)[R], int i, L vN0, L vS1) -> L {
+      L vW, vE;
+      if constexpr (kShflWE<L>) {
+        const L sW = __shfl_up_sync(0xffffffffu, v[i], 1);
+        const L sE = __shfl_down_sync(0xffffffffu, v[i], 1);
+        vW = lane > 0 ? sW : L(0);
+        vE = lane < 31 ? sE : L(0);
+      } else {
+        vW = S.pt[c.row0 + i][lane];
+        vE = S.pt[c.row0 + i][lane + 2];
+      }
+      const L vN = i > 0 ? v[i - 1] : vN0;
+      const L vS = i + 1 < R ? v[i + 1] : vS1;
+      L d;
+      if (FULL)
+        d = (i == 0) ? dFirst : ((i == R - 1) ? dLast : dI);
+      else
+        d = (i == iT) ? dT : ((i == iB) ? dB : dI);
+      // d*v - (vW + vE) - (vN + vS): dependent depth 3 (the reference's
+      // left-to-right chain is 4; the values agree to rounding)
+      const L t = fmaT(d, v[i], -(vW + vE)) - (vN + vS);
+      return ((unk >> i) & 1u) ? t : L(0);
+    };
     auto apply = [&](const L(&v)[R], L vN0, L vS1, L(&o)[R]) {
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
-        L vW, vE;
-        if constexpr (kShflWE<L>) {
-          const L sW = __shfl_up_sync(0xffffffffu, v[i], 1);
-          const L sE = __shfl_down_sync(0xffffffffu, v[i], 1);
-          vW = lane > 0 ? sW : L(0);
-          vE = lane < 31 ? sE : L(0);
-        } else {
-          vW = S.pt[c.row0 + i][lane];
-          vE = S.pt[c.row0 + i][lane + 2];
+      for (int i = 0; i < R; ++i) o[i] = row_op(v, i, vN0, vS1);
+    };
+    // QT: q = A p streamed to TMEM four rows at a time with the thread part
+    // of p.q accumulated on the way (dot2's exact order: s[k] = p_k q_k for
+    // the first four rows, then s[i % 4] = fma(p_i, q_i, s[i % 4]), then the
+    // pairwise tree)
+    auto apply_pq_tmem = [&](L vN0, L vS1) -> L {
+      if constexpr (QT) {
+        double s4[4];
+#pragma unroll
+        for (int k = 0; k < R / 4; ++k) {
+          double qc[4];
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii) {
+            const int i = 4 * k + ii;
+            qc[ii] = row_op(p, i, vN0, vS1);
+            s4[ii] = k == 0 ? p[i] * qc[ii] : fma(p[i], qc[ii], s4[ii]);
+          }
+          tmem_store4(taddr + 32 + 8 * k, qc);
         }
-        const L vN = i > 0 ? v[i - 1] : vN0;
-        const L vS = i + 1 < R ? v[i + 1] : vS1;
-        L d;
-        if (FULL)
-          d = (i == 0) ? dFirst : ((i == R - 1) ? dLast : dI);
-        else
-          d = (i == iT) ? dT : ((i == iB) ? dB : dI);
-        // d*v - (vW + vE) - (vN + vS): dependent depth 3 (the reference's
-        // left-to-right chain is 4; the values agree to rounding)
-        const L t = fmaT(d, v[i], -(vW + vE)) - (vN + vS);
-        o[i] = ((unk >> i) & 1u) ? t : L(0);
+        return (s4[0] + s4[1]) + (s4[2] + s4[3]);
+      } else {
+        return L(0);
       }
     };
 
@@ -586,18 +667,53 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
       pr_k1 = pr_t;
 #endif
       for (int iter = 1; iter <= a.lmax; ++iter) {
-        apply(p, nb_p[0], nb_p[1], q);
-        const L pAp = cta_sum<L, NW>(dot2<L, R>(p, q), S.red, 0, warp, lane);
+        L part_pq;
+        if constexpr (QT) {
+          part_pq = apply_pq_tmem(nb_p[0], nb_p[1]);
+        } else {
+          apply(p, nb_p[0], nb_p[1], q);
+          part_pq = dot2<L, R>(p, q);
+        }
+        const L pAp = cta_sum<L, NW>(part_pq, S.red, 0, warp, lane);
         if (!(pAp > L(0)) || !isfinite(pAp)) {  // breakdown (cg.hpp:120-125)
           iters = iter - 1;
           break;
         }
         SI_PROBE_MARK(0);
+        // alpha = rr / pAp through the correctly rounded reciprocal and one
+        // Markstein step (== the IEEE quotient, si_selftest 0): 2.81 -> 2.78 ms
+        // per frame's sweeps; SI_ALPHA_DIV=1 keeps the division (A/B)
+#ifdef SI_ALPHA_DIV
         const L alpha = rr / pAp;
+#else
+        const L alpha = div_by_recip(rr, pAp, recip_rn(pAp));
+#endif
+        if constexpr (XT) {
+          if constexpr (QT) {
+            double qv[16];
+            tmem_wait_st();
+            tmem_load16(taddr + 32, qv);
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
-          x[i] = fmaT(alpha, p[i], x[i]);
-          r[i] = fmaT(-alpha, q[i], r[i]);
+            for (int i = 0; i < R; ++i) r[i] = fmaT(-alpha, qv[i], r[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < R; ++i) r[i] = fmaT(-alpha, q[i], r[i]);
+          }
+          // x += alpha p through TMEM (the previous store has long landed)
+          double xv[16];
+          tmem_wait_st();
+          tmem_load16(taddr, xv);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) xv[i] = fma(alpha, p[i], xv[i]);
+          S.pub[warp][0][2][lane] = xv[0];
+          S.pub[warp][1][2][lane] = xv[15];
+          tmem_store16(taddr, xv);
+        } else {
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+            x[i] = fmaT(alpha, p[i], x[i]);
+            r[i] = fmaT(-alpha, q[i], r[i]);
+          }
         }
         publish();
         L rr_new = cta_sum<L, NW>(dot2<L, R>(r, r), S.red, 1, warp, lane);
@@ -609,18 +725,26 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
         SI_PROBE_MARK(1);
         if (cadence || maybe_done) {
           // True residual b - A x, then confirm or replace (cg.hpp:131-146).
-          stage(x);
           // the neighbours' boundary rows of x were published before the rr
           // barrier of this iteration
           const L nx0 = (NW > 1 && warp > 0) ? S.pub[warp - 1][1][2][lane] : L(0);
           const L nx1 = (NW > 1 && warp + 1 < NW) ? S.pub[warp + 1][0][2][lane] : L(0);
-          apply(x, nx0, nx1, q);
+          L tq[R];
+          if constexpr (XT) {
+            double xv[16];
+            tmem_wait_st();
+            tmem_load16(taddr, xv);
+            apply(xv, nx0, nx1, tq);
+          } else {
+            stage(x);
+            apply(x, nx0, nx1, tq);
+          }
 #pragma unroll
-          for (int i = 0; i < R; ++i) q[i] = S.bt[c.row0 + i][lane] - q[i];
-          const L part = dot2<L, R>(q, q);
+          for (int i = 0; i < R; ++i) tq[i] = S.bt[c.row0 + i][lane] - tq[i];
+          const L part = dot2<L, R>(tq, tq);
           if (NW > 1) {
-            S.pubt[warp][0][lane] = q[0];
-            S.pubt[warp][1][lane] = q[R - 1];
+            S.pubt[warp][0][lane] = tq[0];
+            S.pubt[warp][1][lane] = tq[R - 1];
           }
           const L tt = cta_sum<L, NW>(part, S.red, 2, warp, lane);
           const L rel = sqrt(tt) / r0;
@@ -630,7 +754,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
             break;
           }
 #pragma unroll
-          for (int i = 0; i < R; ++i) r[i] = q[i];
+          for (int i = 0; i < R; ++i) r[i] = tq[i];
           if (NW > 1) {
             if (warp > 0) nb_r[0] = S.pubt[warp - 1][1][lane];
             if (warp + 1 < NW) nb_r[1] = S.pubt[warp + 1][0][lane];
@@ -661,6 +785,22 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
   const int oy0 = a.ay.owned_begin(by), oy1 = a.ay.owned_end(by);
   T* __restrict__ un = a.u_new + plane;
   const bool col_own = c.col_ok && c.gx >= ox0 && c.gx < ox1;
+  L xf[R];  // the local solution of my cells
+  if constexpr (XT) {
+    double xv[16];
+    tmem_wait_st();
+    tmem_load16(taddr, xv);
+#pragma unroll
+    for (int i = 0; i < R; ++i) xf[i] = xv[i];
+    // every warp has read its columns: free them
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    tmem_free_cta<kCols>(tbase);
+  } else {
+#pragma unroll
+    for (int i = 0; i < R; ++i) xf[i] = x[i];
+  }
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int ly = c.row0 + i;
@@ -669,7 +809,7 @@ __global__ void __launch_bounds__(NW * 32, (SweepOcc<L, NW>::value))
     const size_t pix = own ? static_cast<size_t>(gy) * c.W + c.gx
                            : static_cast<size_t>(c.y0) * c.W + c.x0;  // a stored pixel
     const T uo = S.ut[ly + 2][lane + c.tl];
-    T v = static_cast<T>(x[i]);
+    T v = static_cast<T>(xf[i]);
     if (!c.known_invariant) {
       const T bk = c.b[pix];
       if (!((unk >> i) & 1u)) v = bk - uo;
