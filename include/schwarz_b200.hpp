@@ -9,19 +9,33 @@
 //   * RunOptions / SolverConfig / Method methods.hpp:13-55, cg.hpp:23-27
 //   * SolveResult / ConvergenceTrace    metrics.hpp:58-105
 //   * SubdomainPartition                partition.hpp:21-106
+//   * the lower seams: multilevel_solve + MultilevelSolveOptions /
+//     LevelSolver (multilevel.hpp:130-310), solve_schwarz + SchwarzOptions /
+//     SchwarzSolveOptions (schwarz.hpp:20-45, 325-389), run_schwarz_level +
+//     LevelRunStats (schwarz.hpp:252-323), canonical_r0 (schwarz.hpp:333-345)
 // Errors: SI_ERR_INVALID_ARGUMENT -> std::invalid_argument (same message the
 // reference throws); other failures -> std::runtime_error.  Non-convergence
 // is reported in SolveReport, never thrown.
-// Link with libschwarz_b200.so.
+// C++17 or later (the reference itself is C++20; under C++20 channel()
+// returns std::span like image.hpp:44-52).  Link with libschwarz_b200.so.
 #pragma once
 
 #include <cmath>
+#include <cstddef>
 #include <cstdint>
+#include <cstdio>
+#include <algorithm>
 #include <optional>
+#include <type_traits>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <utility>
 #include <vector>
+#if __cplusplus >= 202002L && __has_include(<span>)
+#include <span>
+#define SCHWARZ_B200_HAS_SPAN 1
+#endif
 
 #include "schwarz_b200.h"
 
@@ -39,6 +53,27 @@ inline void check_arg(bool ok, const std::string& msg) {
 }
 }  // namespace detail
 
+using ChannelVector = std::vector<double>;  // image.hpp:14
+
+#ifdef SCHWARZ_B200_HAS_SPAN
+template <typename T>
+using Span = std::span<T>;
+#else
+// Minimal contiguous view for C++17 callers (std::span under C++20).
+template <typename T>
+struct Span {
+  T* ptr = nullptr;
+  std::size_t n = 0;
+  Span(T* p, std::size_t count) : ptr(p), n(count) {}
+  T* data() const { return ptr; }
+  std::size_t size() const { return n; }
+  T& operator[](std::size_t i) const { return ptr[i]; }
+  T* begin() const { return ptr; }
+  T* end() const { return ptr + n; }
+};
+#endif
+
+// Planar image, channel c at [c*w*h, (c+1)*w*h) row-major (image.hpp:24-63).
 struct ImageBuffer {
   int width = 0, height = 0, channels = 1;
   std::vector<double> data;
@@ -48,10 +83,19 @@ struct ImageBuffer {
     data.assign(static_cast<size_t>(w) * h * ch, fill);
   }
   size_t pixel_count() const { return static_cast<size_t>(width) * height; }
+  Span<double> channel(int c) {
+    detail::check_arg(c >= 0 && c < channels, "ImageBuffer::channel: index out of range");
+    return {data.data() + static_cast<size_t>(c) * pixel_count(), pixel_count()};
+  }
+  Span<const double> channel(int c) const {
+    detail::check_arg(c >= 0 && c < channels, "ImageBuffer::channel: index out of range");
+    return {data.data() + static_cast<size_t>(c) * pixel_count(), pixel_count()};
+  }
   double& at(int x, int y, int c = 0) { return data[c * pixel_count() + static_cast<size_t>(y) * width + x]; }
   double at(int x, int y, int c = 0) const { return data[c * pixel_count() + static_cast<size_t>(y) * width + x]; }
 };
 
+// uint8 per pixel, nonzero = known (image.hpp:67-94).
 struct InpaintingMask {
   int width = 0, height = 0;
   std::vector<uint8_t> known;
@@ -62,11 +106,51 @@ struct InpaintingMask {
   }
   size_t size() const { return static_cast<size_t>(width) * height; }
   bool is_known(int x, int y) const { return known[static_cast<size_t>(y) * width + x] != 0; }
+  size_t known_count() const {
+    size_t n = 0;
+    for (uint8_t k : known) n += k != 0;
+    return n;
+  }
+  double density() const {
+    return size() == 0 ? 0.0 : static_cast<double>(known_count()) / static_cast<double>(size());
+  }
 };
+
+// image.hpp:96-99
+inline void require_same_grid(const ImageBuffer& image, const InpaintingMask& mask) {
+  detail::check_arg(image.width == mask.width && image.height == mask.height,
+                    "image and mask dimensions differ");
+}
 
 enum class Method { Cg = 0, MultilevelCg = 1, Ras = 2, Oras = 3, MultilevelOras = 4 };
 enum class CoarseAveraging { KnownOnly = 0, AllPixels = 1 };
 enum class ResidualNormalizer { InitialGuess = 0, RhsNorm = 1 };
+enum class SchwarzFlavour { Ras = 0, Oras = 1 };   // schwarz.hpp:29
+enum class LevelSolver { Cg, Ras, Oras };          // multilevel.hpp:130
+
+// methods.hpp:15-40
+inline const char* method_name(Method m) {
+  switch (m) {
+    case Method::Cg: return "cg";
+    case Method::MultilevelCg: return "mlcg";
+    case Method::Ras: return "ras";
+    case Method::Oras: return "oras";
+    case Method::MultilevelOras: return "mloras";
+  }
+  return "?";
+}
+inline Method parse_method(const std::string& name) {
+  if (name == "cg") return Method::Cg;
+  if (name == "mlcg") return Method::MultilevelCg;
+  if (name == "ras") return Method::Ras;
+  if (name == "oras") return Method::Oras;
+  if (name == "mloras") return Method::MultilevelOras;
+  throw std::invalid_argument("unknown method '" + name +
+                              "' (expected cg, mlcg, ras, oras or mloras)");
+}
+inline bool is_multilevel(Method m) {
+  return m == Method::MultilevelCg || m == Method::MultilevelOras;
+}
 enum class Precision { FP64 = 0, FP32 = 1, MIXED = 2 };  // MIXED: float local CG, double outer iteration
 
 inline constexpr double kDefaultOrasAlpha = 0.25;
@@ -75,6 +159,14 @@ struct SolverConfig {
   double tolerance = 1e-6;
   int max_iterations = 10000;
   int residual_check_interval = 1;
+};
+
+// schwarz.hpp:38-45
+struct SchwarzOptions {
+  SchwarzFlavour flavour = SchwarzFlavour::Oras;
+  double alpha = kDefaultOrasAlpha;
+  SolverConfig local{1e-2, 30, 30};
+  int max_outer_iterations = 1000;
 };
 
 struct RunOptions {
@@ -113,6 +205,37 @@ struct RunOptions {
   }
 };
 
+// schwarz.hpp:325-329 (+ device precision)
+struct SchwarzSolveOptions {
+  SchwarzOptions schwarz;
+  double tolerance = 1e-3;
+  ResidualNormalizer normalizer = ResidualNormalizer::InitialGuess;
+  Precision precision = Precision::FP64;
+};
+
+// multilevel.hpp:132-142 (+ device precision)
+struct MultilevelSolveOptions {
+  int levels = 3;
+  double tolerance = 1e-3;         // finest level
+  double coarse_tolerance = 1e-2;  // every level above the finest
+  CoarseAveraging averaging = CoarseAveraging::KnownOnly;
+  int block_size = 32;
+  int overlap = 6;
+  SchwarzOptions schwarz;              // flavour is overridden by the solver choice
+  SolverConfig cg{1e-3, 100000, 4};    // tolerance field is overridden per level
+  ResidualNormalizer normalizer = ResidualNormalizer::InitialGuess;
+  Precision precision = Precision::FP64;
+};
+
+// run_schwarz_level's statistics (schwarz.hpp:254-260).
+struct LevelRunStats {
+  int iterations = 0;
+  double final_rel = 0.0;
+  bool converged = false;
+  long long local_solves = 0;
+  long long local_failures = 0;
+};
+
 struct TraceRow {
   int iteration = 0;
   double time_ms = 0.0;
@@ -120,10 +243,32 @@ struct TraceRow {
   std::optional<double> psnr;
 };
 
+// metrics.hpp:67-97
 struct ConvergenceTrace {
+  static constexpr const char* kCsvHeader = "iter,time_ms,rel_residual,psnr";
   std::vector<TraceRow> rows;
   void append(int it, double ms, double rel, std::optional<double> q = std::nullopt) {
     rows.push_back({it, ms, rel, q});
+  }
+  void write_csv(std::ostream& os) const {
+    os << kCsvHeader << '\n';
+    char buf[160];
+    for (const auto& row : rows) {
+      std::snprintf(buf, sizeof buf, "%d,%.3f,%.9e", row.iteration, row.time_ms,
+                    row.rel_residual);
+      os << buf;
+      if (row.psnr) {
+        if (std::isinf(*row.psnr)) {
+          os << ",inf";
+        } else {
+          std::snprintf(buf, sizeof buf, ",%.4f", *row.psnr);
+          os << buf;
+        }
+      } else {
+        os << ',';
+      }
+      os << '\n';
+    }
   }
 };
 
@@ -195,8 +340,11 @@ inline SolveReport to_report(const si_report& r) {
 inline SolveResult run_method(Method method, const ImageBuffer& f, const InpaintingMask& mask,
                               const RunOptions& options, const ImageBuffer* reference = nullptr,
                               Context& ctx = Context::thread_default()) {
-  detail::check_arg(f.width == mask.width && f.height == mask.height,
-                    "image and mask dimensions differ");
+  require_same_grid(f, mask);
+  if (reference)  // mse_per_channel's check (metrics.hpp:30-35), before any copy
+    detail::check_arg(reference->width == f.width && reference->height == f.height &&
+                          reference->channels == f.channels,
+                      "mse_per_channel: image dimensions differ");
   SolveResult res;
   res.image = ImageBuffer(f.width, f.height, f.channels);
   si_report rep;
@@ -269,11 +417,172 @@ inline ImageBuffer synthetic_test_image(int w, int h, int c, uint64_t seed) {
   return img;
 }
 
+// random_mask (masks.hpp:25-43), with the reference's checks and messages.
 inline InpaintingMask random_mask(int w, int h, double density, uint64_t seed) {
+  detail::check_arg(w > 0 && h > 0, "random_mask: dimensions must be positive");
+  detail::check_arg(density > 0.0 && density <= 1.0, "random_mask: density must lie in (0, 1]");
+  const size_t n = static_cast<size_t>(w) * h;
+  detail::check_arg(std::llround(density * static_cast<double>(n)) >= 1,
+                    "random_mask: density rounds to zero known pixels");
   InpaintingMask m(w, h);
-  const si_status s = si_random_mask(w, h, density, seed, m.known.data());
-  if (s != SI_OK) throw std::invalid_argument("random_mask: invalid dimensions or density");
+  detail::throw_status(si_random_mask(w, h, density, seed, m.known.data()));
   return m;
+}
+
+// clamped_partition (multilevel.hpp:146-150).
+inline SubdomainPartition clamped_partition(int w, int h, int block, int overlap) {
+  const int be = std::min(block, std::min(w, h));
+  const int oe = std::max(0, std::min(overlap, be - 1));
+  return partition_domain(w, h, be, oe);
+}
+
+// multilevel_solve (multilevel.hpp:239-310).  LevelSolver::Ras on a pyramid
+// runs the ORAS kernels with alpha = 1, whose Robin diagonal is exactly the
+// RAS one (deg + 0 * cut, schwarz.hpp:12-15, 106-108).
+inline SolveResult multilevel_solve(const ImageBuffer& f, const InpaintingMask& mask,
+                                    LevelSolver solver, const MultilevelSolveOptions& options,
+                                    const ImageBuffer* reference = nullptr,
+                                    Context& ctx = Context::thread_default()) {
+  RunOptions ro;
+  ro.tolerance = options.tolerance;
+  ro.levels = options.levels;
+  ro.block_size = options.block_size;
+  ro.overlap = options.overlap;
+  ro.alpha = options.schwarz.alpha;
+  ro.coarse_tolerance = options.coarse_tolerance;
+  ro.averaging = options.averaging;
+  ro.local = options.schwarz.local;
+  ro.max_outer_iterations = options.schwarz.max_outer_iterations;
+  ro.cg_max_iterations = options.cg.max_iterations;
+  ro.cg_check_interval = options.cg.residual_check_interval;
+  ro.normalizer = options.normalizer;
+  ro.precision = options.precision;
+  Method m = Method::MultilevelOras;
+  if (solver == LevelSolver::Cg) {
+    m = Method::MultilevelCg;
+  } else if (solver == LevelSolver::Ras) {
+    if (options.levels == 1) {
+      m = Method::Ras;
+    } else {
+      ro.alpha = 1.0;
+    }
+  }
+  return run_method(m, f, mask, ro, reference, ctx);
+}
+
+// solve_schwarz (schwarz.hpp:349-389): single level on an explicit partition.
+inline SolveResult solve_schwarz(const ImageBuffer& f, const InpaintingMask& mask,
+                                 const SubdomainPartition& partition,
+                                 const SchwarzSolveOptions& options,
+                                 const ImageBuffer* reference = nullptr,
+                                 Context& ctx = Context::thread_default()) {
+  require_same_grid(f, mask);
+  if (reference)
+    detail::check_arg(reference->width == f.width && reference->height == f.height &&
+                          reference->channels == f.channels,
+                      "mse_per_channel: image dimensions differ");
+  RunOptions ro;
+  ro.tolerance = options.tolerance;
+  ro.levels = 1;
+  ro.alpha = options.schwarz.alpha;
+  ro.local = options.schwarz.local;
+  ro.max_outer_iterations = options.schwarz.max_outer_iterations;
+  ro.normalizer = options.normalizer;
+  ro.precision = options.precision;
+  const si_options o = ro.to_c();
+  SolveResult res;
+  res.image = ImageBuffer(f.width, f.height, f.channels);
+  si_report rep;
+  detail::throw_status(si_solve_schwarz(
+      ctx.get(), f.data.data(), mask.known.data(), f.width, f.height, f.channels,
+      partition.block_size, partition.overlap, static_cast<int>(options.schwarz.flavour), &o,
+      reference ? reference->data.data() : nullptr, res.image.data.data(), &rep,
+      &detail::trace_sink, &res.trace));
+  res.report = detail::to_report(rep);
+  return res;
+}
+
+// InpaintingOperator (operators.hpp:21-97), constructed from the mask as the
+// reference does (InpaintingOperator op(mask)); the device applies it.
+class InpaintingOperator {
+ public:
+  explicit InpaintingOperator(const InpaintingMask& mask) : mask_(&mask) {}
+  int width() const { return mask_->width; }
+  int height() const { return mask_->height; }
+  const InpaintingMask& mask() const { return *mask_; }
+
+ private:
+  const InpaintingMask* mask_;
+};
+
+namespace detail {
+// vector<ChannelVector> <-> planar buffer
+inline std::vector<double> planar(const std::vector<ChannelVector>& v, size_t n) {
+  std::vector<double> out;
+  out.reserve(v.size() * n);
+  for (const auto& c : v) {
+    check_arg(c.size() == n, "run_schwarz_level: vector length mismatch");
+    out.insert(out.end(), c.begin(), c.end());
+  }
+  return out;
+}
+template <class Sink>
+void row_thunk(int it, double, double rel, double, void* user) {
+  (*static_cast<Sink*>(user))(it, rel);
+}
+}  // namespace detail
+
+// canonical_r0 (schwarz.hpp:333-345): ||b - A b|| (u0 = b) or ||b||.
+inline double canonical_r0(const InpaintingOperator& op, const std::vector<ChannelVector>& b,
+                           ResidualNormalizer normalizer,
+                           Context& ctx = Context::thread_default()) {
+  const size_t n = static_cast<size_t>(op.width()) * op.height();
+  const std::vector<double> bp = detail::planar(b, n);
+  double r0 = 0.0;
+  detail::throw_status(si_canonical_r0(ctx.get(), op.mask().known.data(), op.width(),
+                                       op.height(), static_cast<int>(b.size()), bp.data(),
+                                       static_cast<int>(normalizer), &r0));
+  return r0;
+}
+
+// run_schwarz_level (schwarz.hpp:266-323): the outer ORAS/RAS loop of one
+// level, u updated in place; row(iteration, rel) is called for every outer
+// iteration, iteration 0 included.
+template <class RowSink>
+LevelRunStats run_schwarz_level(const InpaintingOperator& op, const SubdomainPartition& part,
+                                const std::vector<ChannelVector>& b,
+                                std::vector<ChannelVector>& u, double r0_norm, double tolerance,
+                                const SchwarzOptions& opt, RowSink&& row,
+                                Context& ctx = Context::thread_default()) {
+  detail::check_arg(part.image_width == op.width() && part.image_height == op.height(),
+                    "run_schwarz_level: partition and operator dimensions differ");
+  detail::check_arg(!b.empty() && b.size() == u.size(),
+                    "run_schwarz_level: channel count mismatch");
+  const size_t n = static_cast<size_t>(op.width()) * op.height();
+  const std::vector<double> bp = detail::planar(b, n);
+  std::vector<double> up = detail::planar(u, n);
+  RunOptions ro;
+  ro.alpha = opt.alpha;
+  ro.local = opt.local;
+  ro.max_outer_iterations = opt.max_outer_iterations;
+  const si_options o = ro.to_c();
+  si_report rep;
+  using Sink = std::remove_reference_t<RowSink>;
+  detail::throw_status(si_run_schwarz_level(
+      ctx.get(), op.mask().known.data(), op.width(), op.height(), static_cast<int>(b.size()),
+      bp.data(), up.data(), part.block_size, part.overlap, r0_norm, tolerance,
+      static_cast<int>(opt.flavour), &o, &rep, &detail::row_thunk<Sink>,
+      const_cast<void*>(static_cast<const void*>(&row))));
+  for (size_t c = 0; c < u.size(); ++c)
+    std::copy(up.begin() + static_cast<std::ptrdiff_t>(c * n),
+              up.begin() + static_cast<std::ptrdiff_t>((c + 1) * n), u[c].begin());
+  LevelRunStats st;
+  st.iterations = rep.iterations;
+  st.final_rel = rep.final_relative_residual;
+  st.converged = rep.converged != 0;
+  st.local_solves = rep.local_solves;
+  st.local_failures = rep.local_failures;
+  return st;
 }
 
 // VoronoiAssignment / assign_nearest_site (masks.hpp:45-139).

@@ -179,6 +179,8 @@ def _ml_run_options(o: MultilevelSolveOptions) -> "RunOptions":
                       overlap=o.overlap, alpha=o.schwarz.alpha,
                       coarse_tolerance=o.coarse_tolerance, averaging=o.averaging,
                       local=o.schwarz.local, max_outer_iterations=o.schwarz.max_outer_iterations,
+                      cg_max_iterations=o.cg.max_iterations,
+                      cg_check_interval=o.cg.residual_check_interval,
                       normalizer=o.normalizer, precision=o.precision)
 
 

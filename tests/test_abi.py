@@ -212,3 +212,57 @@ def test_batch_outputs_are_validated_before_the_abi():
                          "run_batch")
     with pytest.raises(si.InvalidArgument):
         _require_outputs([np.empty((4, 5, 3), np.uint8)], 1, (4, 5, 3), np.float64, "run_pnm_batch")
+
+
+def test_cpp_dropin_types_and_messages(tmp_path):
+    """C++20 drop-in (include/schwarz_b200.hpp): the reference's type members
+    (ImageBuffer::channel as std::span, InpaintingMask::known_count/density,
+    image.hpp:44-93), method names (methods.hpp:15-40) and the exact
+    std::invalid_argument messages of random_mask (masks.hpp:26-31),
+    require_same_grid (image.hpp:96-99) and channel(); host-only calls."""
+    src = tmp_path / "t.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include <span>
+#include "schwarz_b200.hpp"
+namespace sb = schwarz_b200;
+template <class F> void expect(F&& f) {
+  try { f(); std::printf("no-throw\n"); }
+  catch (const std::invalid_argument& e) { std::printf("%s\n", e.what()); }
+}
+int main() {
+  sb::ImageBuffer f(5, 4, 2, 0.5);
+  std::span<double> c1 = f.channel(1);
+  c1[3] = 2.0;
+  std::printf("%zu %g %g\n", c1.size(), f.at(3, 0, 1), f.channel(0)[0]);
+  auto m = sb::random_mask(5, 4, 0.25, 3);
+  std::printf("%zu %.3f\n", m.known_count(), m.density());
+  std::printf("%s %d\n", sb::method_name(sb::parse_method("mloras")),
+              (int)sb::is_multilevel(sb::Method::MultilevelCg));
+  expect([] { sb::random_mask(0, 4, 0.5, 1); });
+  expect([] { sb::random_mask(4, 4, 1.5, 1); });
+  expect([] { sb::random_mask(4, 4, 0.01, 1); });
+  expect([&] { sb::require_same_grid(f, sb::InpaintingMask(4, 4)); });
+  expect([&] { (void)f.channel(2); });
+  expect([] { sb::parse_method("foo"); });
+  return 0;
+}
+''')
+    exe = tmp_path / "t"
+    out = subprocess.run(["g++", "-std=c++20", "-Wall", "-I", os.path.join(ROOT, "include"),
+                          str(src), L.lib_path(), "-o", str(exe),
+                          f"-Wl,-rpath,{os.path.dirname(L.lib_path())}"],
+                         capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    run = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert run.returncode == 0, run.stderr
+    lines = run.stdout.strip().splitlines()
+    assert lines[0] == "20 2 0.5"
+    assert lines[1] == "5 0.250"
+    assert lines[2] == "mloras 1"
+    assert lines[3:] == ["random_mask: dimensions must be positive",
+                         "random_mask: density must lie in (0, 1]",
+                         "random_mask: density rounds to zero known pixels",
+                         "image and mask dimensions differ",
+                         "ImageBuffer::channel: index out of range",
+                         "unknown method 'foo' (expected cg, mlcg, ras, oras or mloras)"]

@@ -707,3 +707,104 @@ def test_many_channels(solver, oracle):
         res = solver.run_method(si.Method.MultilevelOras, f, m, o)
         ora = oracle.oracle_solve(f.data, m.known, **opts_dict(o, si.Method.MultilevelOras))
         compare(res, ora, FP64)
+
+
+def test_cpp_dropin_lower_seams(tmp_path, solver, oracle):
+    """The C++ drop-in's lower seams, called the way the reference's own
+    callers call them: tools/alpha_calibrate.cpp's body (solve_schwarz on
+    partition_domain, SchwarzSolveOptions, alpha_calibrate.cpp:17-30),
+    multilevel_solve with each LevelSolver (multilevel.hpp:239-241), and
+    canonical_r0 + run_schwarz_level with a row sink (schwarz.hpp:266-270,
+    333-345).  Counts equal the Python/C-ABI path and the oracle; images
+    equal the Python path bit for bit (same library)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "t.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include <vector>
+#include "schwarz_b200.hpp"
+namespace si = schwarz_b200;
+static double sum(const si::ImageBuffer& a) { double s = 0; for (double v : a.data) s += v; return s; }
+int main() {
+  // alpha_calibrate.cpp:17-30, verbatim call shapes
+  const si::ImageBuffer image = si::synthetic_test_image(256, 256, 3, 7);
+  const si::InpaintingMask mask = si::random_mask(256, 256, 0.05, 11);
+  const auto partition = si::partition_domain(256, 256, 32, 6);
+  auto outer_iterations = [&](si::SchwarzFlavour flavour, double alpha) {
+    si::SchwarzSolveOptions opt;
+    opt.schwarz.flavour = flavour;
+    opt.schwarz.alpha = alpha;
+    opt.schwarz.max_outer_iterations = 5000;
+    opt.tolerance = 1e-6;
+    const auto result = si::solve_schwarz(image, mask, partition, opt);
+    return result.report.converged ? result.report.iterations : -1;
+  };
+  std::printf("%d %d %d\n", outer_iterations(si::SchwarzFlavour::Ras, 1.0),
+              outer_iterations(si::SchwarzFlavour::Oras, 0.25),
+              outer_iterations(si::SchwarzFlavour::Oras, 2.0));
+  // multilevel_solve with every level solver
+  si::MultilevelSolveOptions ml;
+  ml.levels = 3;
+  for (si::LevelSolver s : {si::LevelSolver::Oras, si::LevelSolver::Ras, si::LevelSolver::Cg}) {
+    const auto r = si::multilevel_solve(image, mask, s, ml);
+    std::printf("%d %.17g %d\n", r.report.iterations, sum(r.image), (int)r.trace.rows.size());
+  }
+  // canonical_r0 + run_schwarz_level: the finest seam with u in/out
+  si::InpaintingOperator op(mask);
+  std::vector<si::ChannelVector> b(3, si::ChannelVector(256 * 256, 0.0)), u;
+  for (int c = 0; c < 3; ++c)
+    for (size_t i = 0; i < b[c].size(); ++i) b[c][i] = mask.known[i] ? image.channel(c)[i] : 0.0;
+  u = b;
+  const double r0 = si::canonical_r0(op, b, si::ResidualNormalizer::InitialGuess);
+  int rows = 0;
+  double last = -1;
+  si::SchwarzOptions so;
+  const auto st = si::run_schwarz_level(op, partition, b, u, r0, 1e-4, so,
+                                        [&](int it, double rel) { rows = it + 1; last = rel; });
+  double su = 0;
+  for (auto& c : u) for (double v : c) su += v;
+  std::printf("%.17g %d %d %d %.17g %lld %.17g\n", r0, st.iterations, (int)st.converged, rows,
+              last, st.local_solves, su);
+  return 0;
+}
+''')
+    lib_dir = os.path.join(root, "paper_2110_03946_b200")
+    exe = str(tmp_path / "t")
+    cc = subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(root, "include"), str(src),
+                         os.path.join(lib_dir, "libschwarz_b200.so"), f"-Wl,-rpath,{lib_dir}",
+                         "-o", exe], capture_output=True, text=True)
+    assert cc.returncode == 0, cc.stderr
+    run = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert run.returncode == 0, run.stderr
+    lines = run.stdout.strip().splitlines()
+    f = si.synthetic_test_image(256, 256, 3, 7)
+    m = si.random_mask(256, 256, 0.05, 11)
+    part = si.partition_domain(256, 256, 32, 6)
+    # alpha_calibrate: outer counts vs the Python path and the oracle
+    want = []
+    for flav, alpha in ((si.SchwarzFlavour.Ras, 1.0), (si.SchwarzFlavour.Oras, 0.25),
+                        (si.SchwarzFlavour.Oras, 2.0)):
+        opt = si.SchwarzSolveOptions(tolerance=1e-6)
+        opt.schwarz.flavour, opt.schwarz.alpha, opt.schwarz.max_outer_iterations = flav, alpha, 5000
+        r = solver.solve_schwarz(f, m, part, opt)
+        ora = oracle.oracle_solve(f.data, m.known, levels=1, tolerance=1e-6, alpha=alpha,
+                                  flavour=int(flav), max_outer_iterations=5000)
+        assert r.report.iterations == ora.iterations
+        want.append(r.report.iterations if r.report.converged else -1)
+    assert [int(v) for v in lines[0].split()] == want
+    for line, ls in zip(lines[1:4], (si.LevelSolver.Oras, si.LevelSolver.Ras, si.LevelSolver.Cg)):
+        r = solver.multilevel_solve(f, m, ls, si.MultilevelSolveOptions(levels=3))
+        it, s, rows = line.split()
+        assert int(it) == r.report.iterations and int(rows) == len(r.trace.rows)
+        assert float(s) == pytest.approx(float(r.image.data.sum()), rel=1e-13)
+    r0, its, conv, rows, last, solves, su = lines[4].split()
+    b = np.where(m.known[None] != 0, f.data, 0.0)
+    assert float(r0) == pytest.approx(solver.canonical_r0(m, b), rel=1e-14)
+    u = b.copy()
+    tr = si.ConvergenceTrace()
+    rep = solver.run_schwarz_level(m, part, b, u, float(r0), 1e-4, si.SchwarzOptions(), trace=tr)
+    assert int(its) == rep.iterations and int(rows) == len(tr.rows) == rep.iterations + 1
+    assert bool(int(conv)) == rep.converged and int(solves) == rep.local_solves
+    assert float(last) == pytest.approx(tr.rows[-1].rel_residual, rel=1e-14)
+    assert float(su) == pytest.approx(float(u.sum()), rel=1e-13)
