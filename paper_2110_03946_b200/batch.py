@@ -2,8 +2,9 @@
 
 Independent frames shard with no data-path collective: frame k goes to rank
 k mod G, every rank solves its frames on its own GPU (one si_ctx per rank,
-host<->device copies overlapped with the solves), and the only communication
-is bookkeeping (which frames, how long) over torch.distributed.
+Solver.run_batch overlapping host<->device copies with the solves), and the
+only communication is bookkeeping (which frames, how long) over
+torch.distributed.  bench.py's end-to-end leg runs through run_sharded.
 """
 from __future__ import annotations
 
@@ -38,7 +39,10 @@ def run_sharded(n_frames: int, make_frame: Callable[[int], object],
     slowest = elapsed
     if dist is not None:
         import torch
-        t = torch.tensor([elapsed], dtype=torch.float64)
+        dev = None
+        if dist.get_backend() == "nccl":  # NCCL reduces device tensors only
+            dev = torch.device("cuda", torch.cuda.current_device())
+        t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         slowest = float(t.item())
     return {"rank": rank, "world": world, "frames": dict(zip(mine, results)),
