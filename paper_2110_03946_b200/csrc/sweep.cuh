@@ -142,6 +142,19 @@ constexpr bool kTmemX =
 // r update, so the loop holds only r and p (64 registers of vectors) and
 // the kernel fits 8 CTAs/SM (128 registers, no spill; 64 TMEM columns x 8
 // CTAs = the SM's 512).  SI_NO_TMEM_Q=1 keeps q in registers (A/B).
+// Full blocks: the W/E ghost zeros of lanes 0 and 31 are folded into the
+// diagonal instead of selected: a shuffle past the warp edge returns the
+// lane's own value v, and (d + 1) v - (v + vE) == d v - vE exactly in real
+// arithmetic (rounding differs only in those two columns).  Saves 4 selects
+// per row.  SI_NO_EDGE_FOLD=1 keeps the selects (A/B).
+template <bool FULL>
+constexpr bool kEdgeFold =
+#if defined(SI_EDGE_FOLD) && !defined(SI_NO_EDGE_FOLD)
+    FULL;
+#else
+    false;
+#endif
+
 template <typename L, int NW, bool FULL>
 constexpr bool kTmemQ =
 #ifdef SI_NO_TMEM_Q
@@ -521,6 +534,13 @@ __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
     dT = robin_diag<L>(c.gx, c.y0, lane, 0, B, c.W, c.H, am1, a.ras);
     dB = robin_diag<L>(c.gx, c.y0 + B - 1, lane, B - 1, B, c.W, c.H, am1, a.ras);
   }
+  if constexpr (kShflWE<L> && kEdgeFold<FULL>) {
+    if (lane == 0 || lane == 31) {  // see kEdgeFold
+      dI += L(1);
+      dT += L(1);
+      dB += L(1);
+    }
+  }
   const L dFirst = (warp == 0) ? dT : dI;        // FULL: row i = 0
   const L dLast = (warp == NW - 1) ? dB : dI;    // FULL: row i = R-1
   const int iT = -c.row0;            // generic: local index of block row 0
@@ -595,7 +615,11 @@ __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
     // registers or the neighbour warps' rows vN0/vS1.
     auto row_op = [&](const L(&v)[R], int i, L vN0, L vS1) -> L {
       L vW, vE;
-      if constexpr (kShflWE<L>) {
+      if constexpr (kShflWE<L> && kEdgeFold<FULL>) {
+        // lanes 0 / 31 receive their own value; their diagonal carries +1
+        vW = __shfl_up_sync(0xffffffffu, v[i], 1);
+        vE = __shfl_down_sync(0xffffffffu, v[i], 1);
+      } else if constexpr (kShflWE<L>) {
         const L sW = __shfl_up_sync(0xffffffffu, v[i], 1);
         const L sE = __shfl_down_sync(0xffffffffu, v[i], 1);
         vW = lane > 0 ? sW : L(0);
