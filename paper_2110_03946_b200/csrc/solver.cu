@@ -34,6 +34,7 @@
 #include "host_copy.h"
 
 #include <cub/cub.cuh>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost ~ns without a tool attached
 
 using namespace sib;
 
@@ -60,6 +61,20 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 
 #define CK(x) cuda_check((x), #x)
+
+// NVTX range for the enclosing scope (solve, level, outer iteration, sweep):
+// visible in Nsight Systems / ncu --nvtx timelines.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* fmt, int a) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, fmt, a);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 using Clock = std::chrono::steady_clock;
 
@@ -679,6 +694,7 @@ LevelOutcome run_level(Ctx& x, LevelView<T>& L, int C, int block, int overlap, d
   const Axis ax = Axis::make(L.w, block, overlap), ay = Axis::make(L.h, block, overlap);
   const long long nblocks = static_cast<long long>(ax.count) * ay.count;
   for (int outer = 0;; ++outer) {
+    NvtxRange nv_outer("outer %d", outer);
     launch_residual<T>(x, L.mask, L.u[L.cur], L.b, L.w, L.h, C, 0, d_out, known_invariant);
     if (sink && d_ref) launch_sq_error<T>(x, L.u[L.cur], d_ref, N, C, d_out + 2 * C);
     sync(x);
@@ -704,6 +720,7 @@ LevelOutcome run_level(Ctx& x, LevelView<T>& L, int C, int block, int overlap, d
       local_checked = true;
     }
     const LocalCfg lc{o.local_tolerance, o.local_max_iterations, o.local_check_interval};
+    NvtxRange nv_sweep("sweep");
     launch_sweep<T>(x, L.mask, L.b, L.u[L.cur], L.u[L.cur ^ 1], L.w, L.h, C, block, overlap,
                     flavour, o.alpha, lc, known_invariant, d_cnt);
     L.cur ^= 1;
@@ -1164,6 +1181,7 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
                        const double* d_ref, double* d_out, si_report* rep, const Trace& tr,
                        int fixed_block = -1, int fixed_overlap = 0,
                        const KnownSamples* ks = nullptr) {
+  NvtxRange nv_solve("multilevel_solve");
   prepare_red(x, C);
   check_arg(levels_req >= 1, "build_pyramid: levels must be >= 1");
   // Level geometry: halve (ceil) until the requested depth or a level that
@@ -1228,6 +1246,7 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
     x.c.lvl_sums.ensure(sizeof(double) * 2 * C * SI_MAX_LEVELS);
   }
   for (int level = depth - 1; level >= 0; --level) {
+    NvtxRange nv_level("level %d", level);
     LevelView<T>& V = L[level];
     const size_t n = static_cast<size_t>(V.w) * V.h;
     if (level == depth - 1) {
@@ -1666,6 +1685,7 @@ void run_batch(si_ctx* ctx, int method, int n, const void* const* in, const uint
     P.rep->elapsed_ms = ms_since(t_start[j]);
   };
   for (int k = 0; k < n; ++k) {
+    NvtxRange nv_frame("batch frame %d", k);
     const int s = k & 1;
     // the other slot's input was consumed by frame k-1 (solved synchronously)
     if (k + 1 < n) {

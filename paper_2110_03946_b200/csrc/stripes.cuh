@@ -511,7 +511,9 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
   std::vector<RowXfer> sends, recvs;
   std::vector<std::vector<Span>> want(G);
 
+  NvtxRange nv_solve("striped multilevel_solve");
   for (int level = depth - 1; level >= 0; --level) {
+    NvtxRange nv_level("stripe level %d", level);
     const StripeLevel& S = P.L[level];
     View& v = V[level];
     const Span own = S.own[me];
@@ -568,6 +570,7 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
         break;
       }
       if (outer >= o.max_outer_iterations) break;
+      NvtxRange nv_sweep("stripe sweep + halo");
       if (S.k1 > S.k0)
         launch_sweep<T>(x, v.mask, v.b, v.u[cur], v.u[cur ^ 1], S.w, S.h, C, S.block, S.overlap,
                         flavour, o.alpha, lc, true, d_cnt, S.k0, S.k1, v.st.lo, v.st.hi);

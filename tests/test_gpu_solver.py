@@ -808,3 +808,36 @@ int main() {
     assert bool(int(conv)) == rep.converged and int(solves) == rep.local_solves
     assert float(last) == pytest.approx(tr.rows[-1].rel_residual, rel=1e-14)
     assert float(su) == pytest.approx(float(u.sum()), rel=1e-13)
+
+
+def test_repeated_headline_solves_are_bit_identical(solver):
+    """Race check in place of compute-sanitizer (closed on this GPU pool):
+    the 4K frame solved repeatedly, and on a second context running
+    concurrently on its own host thread, gives bit-identical images, trace
+    rows, PSNR rows and counters -- any race in K2's barrier-free
+    warp-boundary exchange, the TMEM-resident CG vectors or the reductions
+    would show up as a difference."""
+    import threading
+    f = si.synthetic_test_image(3840, 2160, 3, 8)
+    m = si.random_mask(3840, 2160, 0.04, 12)
+    o = si.RunOptions(levels=3)
+    runs = [solver.run_method(si.Method.MultilevelOras, f, m, o, reference=f) for _ in range(3)]
+    other = si.Solver(0)
+    conc = [None, None]
+
+    def go(k, s):
+        conc[k] = s.run_method(si.Method.MultilevelOras, f, m, o, reference=f)
+
+    ts = [threading.Thread(target=go, args=(0, solver)), threading.Thread(target=go, args=(1, other))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    other.close()
+    base = runs[0]
+    for r in runs[1:] + conc:
+        assert np.array_equal(r.image.data, base.image.data)
+        assert [x.rel_residual for x in r.trace.rows] == [x.rel_residual for x in base.trace.rows]
+        assert [x.psnr for x in r.trace.rows] == [x.psnr for x in base.trace.rows]
+        assert r.report.local_cg_iterations == base.report.local_cg_iterations
+        assert r.report.local_failures == base.report.local_failures
