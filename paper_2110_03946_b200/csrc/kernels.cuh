@@ -315,6 +315,101 @@ __global__ void __launch_bounds__(kResTmaThreads)
   pdl_trigger();
 }
 
+// K1 pair: the residual of the level's start iterate u0 AND canonical_r0's
+// residual of u = b (schwarz.hpp:333-345) in one pass, under the multilevel
+// invariant (b never read at unknown pixels, r = 0 at known ones): two TMA
+// tiles (u0, b) and the mask band on one barrier; partials for u0 at
+// [c][blk], for b at [C + c][blk] -- one finish over 2C "channels" leaves
+// the sums at out[0..C) and r0's at out[C..2C).  Saves one launch pair and
+// one mask pass per level against two separate K1 launches.
+template <typename T, bool MTMA>
+__global__ void __launch_bounds__(kResTmaThreads)
+    residual_pair_tma_kernel(const __grid_constant__ CUtensorMap umap,
+                             const __grid_constant__ CUtensorMap bmap,
+                             const __grid_constant__ CUtensorMap mmap,
+                             const uint8_t* __restrict__ mask, int W, int H, int row0, int row1,
+                             int srow_lo, double* partials) {
+  // each TMA destination 128-byte aligned (a bare [2][18][w] array would put
+  // the second tile at a 64-byte offset)
+  struct __align__(128) Tile {
+    T v[kResTmaBand + 2][res_tma_box_w<T>()];
+  };
+  __shared__ Tile tiles[2];
+  __shared__ __align__(128) uint8_t mtile[kResTmaBand][kResTmaThreads];
+  __shared__ uint64_t bar;
+  const int c = blockIdx.z;
+  const int x0 = blockIdx.x * kResTmaThreads;
+  const int x = x0 + threadIdx.x;
+  const int y0 = row0 + static_cast<int>(blockIdx.y) * kResTmaBand;
+  const int ny = min(kResTmaBand, row1 - y0);
+  const bool xin = x < W;
+  const size_t Wz = static_cast<size_t>(W);
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, 2 * sizeof(tiles[0].v) + (MTMA ? sizeof(mtile) : 0));
+    tma_load_3d(&tiles[0].v[0][0], &umap, x0 - res_tma_lead<T>(), y0 - 1 - srow_lo, c, &bar);
+    tma_load_3d(&tiles[1].v[0][0], &bmap, x0 - res_tma_lead<T>(), y0 - 1 - srow_lo, c, &bar);
+    if (MTMA) tma_load_2d(&mtile[0][0], &mmap, x0, y0 - srow_lo, &bar);
+  }
+  uint8_t mk[kResTmaBand];
+  if (!MTMA) {
+    const size_t base = xin ? static_cast<size_t>(y0) * Wz + x : static_cast<size_t>(y0) * Wz;
+#pragma unroll
+    for (int k = 0; k < kResTmaBand; ++k) {
+      const bool in = xin && k < ny;
+      const uint8_t m = __ldg(mask + (in ? base + static_cast<size_t>(k) * Wz
+                                          : static_cast<size_t>(y0) * Wz));
+      mk[k] = in ? m : uint8_t(0);
+    }
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  if (MTMA) {
+#pragma unroll
+    for (int k = 0; k < kResTmaBand; ++k)
+      mk[k] = (xin && k < ny) ? mtile[k][threadIdx.x] : uint8_t(0);
+  }
+  const int t = threadIdx.x + res_tma_lead<T>();
+  const int deg_x = (x > 0) + (x + 1 < W);
+  const T deg_in = T(deg_x + 2);
+  double acc[2] = {0.0, 0.0};
+#pragma unroll
+  for (int v = 0; v < 2; ++v) {
+    const auto& tile = tiles[v].v;
+    T up = tile[0][t], ctr = tile[1][t];
+#pragma unroll
+    for (int k = 0; k < kResTmaBand; ++k) {
+      const int y = y0 + k;
+      const T dn = tile[k + 2][t];
+      const T sum = ((tile[k + 1][t - 1] + tile[k + 1][t + 1]) + up) + dn;
+      const T deg = (y > 0 && y + 1 < H) ? deg_in : T(deg_x + (y > 0) + (y + 1 < H));
+      const T au = fma(deg, ctr, -sum);
+      const T r = mk[k] ? T(0) : au;
+      const double rd = (xin && k < ny) ? static_cast<double>(r) : 0.0;
+      acc[v] = fma(rd, rd, acc[v]);
+      up = ctr;
+      ctr = dn;
+    }
+  }
+  __shared__ double wsum[2][kResTmaThreads / 32];
+#pragma unroll
+  for (int v = 0; v < 2; ++v) {
+    const double a = warp_sum(acc[v]);
+    if ((threadIdx.x & 31) == 0) wsum[v][threadIdx.x >> 5] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kResTmaThreads / 32; ++w) s += wsum[threadIdx.x][w];
+    const size_t nblk = static_cast<size_t>(gridDim.x) * gridDim.y;
+    partials[(threadIdx.x * gridDim.z + blockIdx.z) * nblk + blockIdx.y * gridDim.x +
+             blockIdx.x] = s;
+  }
+  pdl_trigger();
+}
+
 // Fixed-order sum of nblk partials per channel (grid: one CTA per channel).
 __global__ void __launch_bounds__(kRedThreads)
     finish_partials_kernel(const double* __restrict__ partials, int nblk, double* out) {

@@ -437,6 +437,46 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
   CK(cudaGetLastError());
 }
 
+// The start of a level: sums of u0 -> out[0..C) and canonical_r0's sums of
+// u = b -> out[C..2C) (normalizer InitialGuess, multilevel invariant), in one
+// K1 pass when TMA can address the buffers, else as two K1 launches.
+template <typename T>
+void launch_residual_pair(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W, int H,
+                          int C, double* out, int row0 = 0, int row1 = -1, int srow_lo = 0,
+                          int srow_hi = -1) {
+  if (row1 < 0) row1 = H;
+  if (srow_hi < 0) srow_hi = H;
+  const int HS = srow_hi - srow_lo;
+  const size_t off = static_cast<size_t>(srow_lo) * W;
+  CUtensorMap umap, bmap, mmap{};
+  if (!tma_disabled() &&
+      make_plane_map(&umap, u + off, W, HS, C, sizeof(T), res_tma_box_w<T>(), kResTmaBand + 2) &&
+      make_plane_map(&bmap, b + off, W, HS, C, sizeof(T), res_tma_box_w<T>(), kResTmaBand + 2)) {
+    const int rows = std::max(1, row1 - row0);
+    const int tx = (W + kResTmaThreads - 1) / kResTmaThreads;
+    const int gy = (rows + kResTmaBand - 1) / kResTmaBand;
+    x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(tx) * gy * 2 * C);
+    const bool mtma = make_mask_map(&mmap, mask + off, W, HS, kResTmaThreads, kResTmaBand);
+    Timed t(x, K_RESIDUAL,
+            static_cast<double>(W) * std::max(0, row1 - row0) * (2.0 * C * sizeof(T) + 1));
+    ++x.c.launch_count;
+    if (mtma)
+      launch_pdl(residual_pair_tma_kernel<T, true>, dim3(tx, gy, C), kResTmaThreads, x.s, umap,
+                 bmap, mmap, mask, W, H, row0, row1, srow_lo, x.c.red_partials.as<double>());
+    else
+      launch_pdl(residual_pair_tma_kernel<T, false>, dim3(tx, gy, C), kResTmaThreads, x.s, umap,
+                 bmap, mmap, mask, W, H, row0, row1, srow_lo, x.c.red_partials.as<double>());
+    CK(cudaGetLastError());
+    ++x.c.launch_count;
+    launch_pdl(finish_partials_kernel, dim3(2 * C), kRedThreads, x.s,
+               static_cast<const double*>(x.c.red_partials.as<double>()), tx * gy, out);
+    CK(cudaGetLastError());
+    return;
+  }
+  launch_residual<T>(x, mask, u, b, W, H, C, 0, out, true, row0, row1, srow_lo, srow_hi);
+  launch_residual<T>(x, mask, b, b, W, H, C, 0, out + C, true, row0, row1, srow_lo, srow_hi);
+}
+
 template <typename T>
 void launch_sq_error(Ctx& x, const T* u, const double* f, size_t N, int C, double* out) {
   const int g = grid_for(N, kRedThreads, kRedBlocksMax);
@@ -681,11 +721,19 @@ double joint_norm(const double* sums, int C) {
 // run_schwarz_level (schwarz.hpp:266-323) on device buffers.  When
 // r0_slot_pending, the r0 reduction was already launched into host_red[C..2C)
 // and is read at the first synchronisation.
+// r0_mode (how the level's canonical r0 arrives at the first synchronisation):
+enum R0Mode {
+  kR0Launched = 0,  // already launched into host_red[C..2C) (launch_r0)
+  kR0Pair = 1,      // launched together with the first residual (launch_residual_pair)
+  kR0Same = 2       // u0 is a copy of b (the coarsest level): r0's sums are the first
+                    // residual's, bit for bit, so nothing extra runs
+};
+
 template <typename T>
 LevelOutcome run_level(Ctx& x, LevelView<T>& L, int C, int block, int overlap, double* r0,
                        bool r0_pending, double tol, int flavour, const si_options& o,
                        bool known_invariant, bool sink, const Trace& tr, const double* d_ref,
-                       si_report* rep) {
+                       si_report* rep, int r0_mode = kR0Launched, bool check_known = false) {
   LevelOutcome out;
   const size_t N = static_cast<size_t>(L.w) * L.h;
   double* d_out = x.c.dev_red;  // mapped: results land in host_red
@@ -695,11 +743,16 @@ LevelOutcome run_level(Ctx& x, LevelView<T>& L, int C, int block, int overlap, d
   const long long nblocks = static_cast<long long>(ax.count) * ay.count;
   for (int outer = 0;; ++outer) {
     NvtxRange nv_outer("outer %d", outer);
-    launch_residual<T>(x, L.mask, L.u[L.cur], L.b, L.w, L.h, C, 0, d_out, known_invariant);
+    if (outer == 0 && r0_mode == kR0Pair)
+      launch_residual_pair<T>(x, L.mask, L.u[L.cur], L.b, L.w, L.h, C, d_out);
+    else
+      launch_residual<T>(x, L.mask, L.u[L.cur], L.b, L.w, L.h, C, 0, d_out, known_invariant);
     if (sink && d_ref) launch_sq_error<T>(x, L.u[L.cur], d_ref, N, C, d_out + 2 * C);
     sync(x);
+    if (check_known && outer == 0)  // deferred build_rhs check (multilevel_device)
+      check_arg(x.c.host_cnt[2] > 0, "build_rhs: mask has no known pixels");
     if (r0_pending) {
-      *r0 = joint_norm(x.c.host_red + C, C);
+      *r0 = joint_norm(x.c.host_red + (r0_mode == kR0Same ? 0 : C), C);
       r0_pending = false;
     }
     const double rel = *r0 > 0.0 ? joint_norm(x.c.host_red, C) / *r0 : 0.0;
@@ -877,7 +930,7 @@ bool graph_eligible(const Ctx& x, const si_options& o, const Trace& tr, const do
 template <typename T>
 GraphCounts launch_level_graph(Ctx& x, LevelView<T>& L, int C, int level, int block,
                                              int overlap, double tol, int flavour,
-                                             const si_options& o) {
+                                             const si_options& o, bool coarsest) {
   si_ctx& c = x.c;
   LevelState* st = c.lvl_state.as<LevelState>() + level;
   double* sums = c.lvl_sums.as<double>() + static_cast<size_t>(level) * 2 * C;
@@ -885,7 +938,7 @@ GraphCounts launch_level_graph(Ctx& x, LevelView<T>& L, int C, int level, int bl
   // every buffer the captured kernels touch must stay put: size the shared
   // partials for this level first (launch_residual never grows it then)
   const size_t parts = static_cast<size_t>((L.w + kResTmaThreads - 1) / kResTmaThreads + 1) *
-                       ((L.h + kResBand - 1) / kResBand + 1) * C;
+                       ((L.h + kResBand - 1) / kResBand + 1) * 2 * C;  // x2: the pair pass
   c.red_partials.ensure(sizeof(double) * parts);
   c.ticket.ensure(sizeof(unsigned int) * 4);
   const double alpha = o.alpha;
@@ -905,7 +958,8 @@ GraphCounts launch_level_graph(Ctx& x, LevelView<T>& L, int C, int level, int bl
       reinterpret_cast<uint64_t>(st), reinterpret_cast<uint64_t>(sums),
       reinterpret_cast<uint64_t>(c.red_partials.ptr), reinterpret_cast<uint64_t>(c.ticket.ptr),
       reinterpret_cast<uint64_t>(c.counters.ptr), static_cast<uint64_t>(tma_disabled()),
-      static_cast<uint64_t>(sizeof(T) == 8 ? c.sweep_nw64 : c.sweep_nw32)};
+      static_cast<uint64_t>(sizeof(T) == 8 ? c.sweep_nw64 : c.sweep_nw32),
+      static_cast<uint64_t>(coarsest)};
   for (auto& g : c.graphs)
     if (g.key == key) {
       g.stamp = ++c.graph_clock;
@@ -919,13 +973,23 @@ GraphCounts launch_level_graph(Ctx& x, LevelView<T>& L, int C, int level, int bl
   const long long lc_before = c.launch_count;
   unsigned long long* cnt = c.counters.as<unsigned long long>();
   CK(cudaStreamBeginCapture(x.s, cudaStreamCaptureModeThreadLocal));
-  launch_residual<T>(x, L.mask, L.b, L.b, L.w, L.h, C, o.normalizer == 1 ? 1 : 0, r0s);
-  launch_residual<T>(x, L.mask, L.u[0], L.b, L.w, L.h, C, 0, sums, true);
+  // canonical r0 and the first residual (see R0Mode): one pair pass, or on
+  // the coarsest level (u0 = b) one pass whose sums are both
+  const double* first_r0 = r0s;
+  if (o.normalizer == 1) {
+    launch_residual<T>(x, L.mask, L.b, L.b, L.w, L.h, C, 1, r0s);
+    launch_residual<T>(x, L.mask, L.u[0], L.b, L.w, L.h, C, 0, sums, true);
+  } else if (coarsest) {
+    launch_residual<T>(x, L.mask, L.u[0], L.b, L.w, L.h, C, 0, sums, true);
+    first_r0 = sums;
+  } else {
+    launch_residual_pair<T>(x, L.mask, L.u[0], L.b, L.w, L.h, C, sums);  // r0s = sums + C
+  }
   cudaGraphConditionalHandle hw;
   CK(cudaGraphConditionalHandleCreate(&hw, capturing_graph(x.s), 0, cudaGraphCondAssignDefault));
   ++c.launch_count;
-  level_decide_kernel<<<1, 32, 0, x.s>>>(sums, r0s, C, tol, o.max_outer_iterations, st, hw, 0, 1,
-                                         0);
+  level_decide_kernel<<<1, 32, 0, x.s>>>(sums, first_r0, C, tol, o.max_outer_iterations, st, hw,
+                                         0, 1, 0);
   CK(cudaGetLastError());
   const long long lc_loop = c.launch_count;
   {
@@ -1265,9 +1329,18 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
     if (flavour == SI_FLAVOUR_ORAS)
       check_arg(std::isfinite(o.alpha), "run_schwarz_level: alpha must be finite");
     const bool by_graph = graph_eligible(x, o, tr, d_ref, flavour, cp.block);
-    if (!known_checked && !by_graph) {
-      // build_rhs rejects an empty mask (operators.hpp:83): read the count
-      // taken by the ingest kernel.
+    bool known_deferred = false;
+    if (!known_checked && !by_graph && !cg_level) {
+      // build_rhs rejects an empty mask (operators.hpp:83): the count taken by
+      // the ingest kernel goes to mapped memory now and is checked at the
+      // level's first synchronisation (no extra host round trip; an empty
+      // mask gives r0 = 0 and the level returns at once)
+      ++x.c.launch_count;
+      copy_u64_kernel<<<1, 32, 0, x.s>>>(x.c.counters.as<unsigned long long>(), x.c.dev_cnt, 3,
+                                         false);
+      CK(cudaGetLastError());
+      known_deferred = true;
+    } else if (!known_checked && !by_graph) {
       publish_counters(x, 3);
       // reduce_structure's singularity check (reduction.hpp:84-112) can only
       // fail when no pixel is known (a component of the unknown region that
@@ -1282,7 +1355,7 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
     if (by_graph) {
       graph_level[level] = 1;
       graph_counts[level] = launch_level_graph<T>(x, V, C, level, cp.block, cp.overlap, tol,
-                                                  flavour, o);
+                                                  flavour, o, level == depth - 1);
       graph_blocks[level] = static_cast<long long>(Axis::make(V.w, cp.block, cp.overlap).count) *
                             Axis::make(V.h, cp.block, cp.overlap).count * C;
       V.cur = 0;  // the parity fixup leaves the level's iterate in u[0]
@@ -1290,10 +1363,15 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
       oc = run_cg_level<T>(x, V, C, tol, o, finest, tr, finest ? d_ref : nullptr);
     } else {
       double r0 = 0.0;
-      launch_r0<T>(x, V, C, o.normalizer);
+      int r0_mode = kR0Launched;
+      if (o.normalizer == 1)
+        launch_r0<T>(x, V, C, o.normalizer);
+      else
+        r0_mode = level == depth - 1 ? kR0Same : kR0Pair;
       oc = run_level<T>(x, V, C, cp.block, cp.overlap, &r0, true, tol, flavour, o, true, finest,
-                        tr, finest ? d_ref : nullptr, rep);
+                        tr, finest ? d_ref : nullptr, rep, r0_mode, known_deferred);
     }
+    if (known_deferred) known_checked = true;
     rep->level_iterations[level] = oc.iterations;
     rep->level_final_rel[level] = oc.final_rel;
     rep->level_converged[level] = oc.converged;

@@ -542,12 +542,15 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
       // residual of my own rows (+ r0 with u = b the first time)
       if (own.empty()) {
         CK(cudaMemsetAsync(d_send, 0, sizeof(double) * 2 * C, x.s));
+      } else if (r0_pending && o.normalizer != 1) {  // u0 and r0 in one pass
+        launch_residual_pair<T>(x, v.mask, v.u[cur], v.b, S.w, S.h, C, d_send, own.lo, own.hi,
+                                v.st.lo, v.st.hi);
       } else {
         launch_residual<T>(x, v.mask, v.u[cur], v.b, S.w, S.h, C, 0, d_send, true, own.lo, own.hi,
                            v.st.lo, v.st.hi);
         if (r0_pending)
-          launch_residual<T>(x, v.mask, v.b, v.b, S.w, S.h, C, o.normalizer == 1 ? 1 : 0,
-                             d_send + C, true, own.lo, own.hi, v.st.lo, v.st.hi);
+          launch_residual<T>(x, v.mask, v.b, v.b, S.w, S.h, C, 1, d_send + C, true, own.lo,
+                             own.hi, v.st.lo, v.st.hi);
       }
       gather(2 * C);
       // fixed rank order: identical sums (and decisions) on every rank
