@@ -445,6 +445,12 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     v.base_mask = l == 0 ? const_cast<uint8_t*>(d_mask) : lb.mask.as<uint8_t>();
     v.base_b = lb.b.as<T>();
     v.base_u[0] = lb.u0.as<T>();
+    // fp64, finest level, store rows == own rows (one rank, or no halo): the
+    // caller's output is one of the ping-pong iterates, as in the direct solve
+    if constexpr (std::is_same<T, double>::value)
+      if (l == 0 && d_out != nullptr && S.store[me].lo == S.own[me].lo &&
+          S.store[me].hi == S.own[me].hi && rows > 0)
+        v.base_u[0] = d_out;
     v.base_u[1] = lb.u1.as<T>();
     v.mask = v.base_mask - off;
     v.b = v.base_b - off;
@@ -452,11 +458,11 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     v.u[1] = v.base_u[1] - off;
   }
   // comm scratch: [sums C | r0 C] per rank, gathered G x 2C
-  c.stripe_send.ensure(sizeof(double) * 2 * C);
-  c.stripe_recv.ensure(sizeof(double) * 2 * C * G + sizeof(double) * 4);
+  c.stripe_send.ensure(sizeof(double) * (2 * C + 4));
+  c.stripe_recv.ensure(sizeof(double) * (2 * C + 4) * G);
   double* d_send = c.stripe_send.as<double>();
   double* d_recv = c.stripe_recv.as<double>();
-  prepare_red(x, (2 * C * G + 3) / 4 + 1);  // mapped slots for the G x 2C gathers
+  prepare_red(x, ((2 * C + 4) * G + 3) / 4 + 1);  // mapped slots for the G x (2C+4) gathers
 
   // ---- K5 ingest of the store rows, K3 restriction store -> store
   {
@@ -477,31 +483,36 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     launch_restrict<T>(x, V[l - 1].mask, V[l - 1].b, F.w, F.h, C, o.averaging, V[l].mask, V[l].b,
                        cs.lo, cs.hi, V[l - 1].rows_n, V[l].rows_n);
   }
-  auto gather = [&](int n) {
-    comm.allgather(d_send, d_recv, n, x.s);
+  // One all-gather per outer iteration carries everything the host needs,
+  // per rank: [sums C | r0 C | known | failures | CG iterations | solves].
+  const int NG = 2 * C + 4;
+  auto gather = [&](double solves) {
     ++c.launch_count;
-    stripe_decide_copy_kernel<<<1, 256, 0, x.s>>>(d_recv, c.dev_red, n * G);
+    stripe_stats_kernel<<<1, 32, 0, x.s>>>(c.counters.as<unsigned long long>(), solves,
+                                           d_send + 2 * C + 1);
+    CK(cudaGetLastError());
+    if (G > 1) comm.allgather(d_send, d_recv, NG, x.s);  // one rank: nothing to gather
+    ++c.launch_count;
+    stripe_decide_copy_kernel<<<1, 256, 0, x.s>>>(G > 1 ? d_recv : d_send, c.dev_red, NG * G);
     CK(cudaGetLastError());
     sync(x);
   };
-  // known count: the rows this rank owns at level 0 (own rows tile the image)
+  // known count of the rows this rank owns at level 0 (own rows tile the
+  // image), checked at the first gather (build_rhs, operators.hpp:83)
+  CK(cudaMemsetAsync(d_send, 0, sizeof(double) * NG, x.s));
   {
     const StripeLevel& S = P.L[0];
     const Span own = S.own[me];
-    CK(cudaMemsetAsync(d_send, 0, sizeof(double) * 2 * C, x.s));
     if (!own.empty()) {
-      c.counters.ensure(sizeof(unsigned long long) * 8);
       ++c.launch_count;
       count_known_rows_kernel<<<grid_for(static_cast<size_t>(own.hi - own.lo) * S.w, 256, 148 * 8),
                                 256, 0, x.s>>>(V[0].mask + static_cast<size_t>(own.lo) * S.w,
-                                               static_cast<size_t>(own.hi - own.lo) * S.w, d_send);
+                                               static_cast<size_t>(own.hi - own.lo) * S.w,
+                                               d_send + 2 * C);
       CK(cudaGetLastError());
     }
-    gather(2 * C);
-    double known = 0.0;
-    for (int g = 0; g < G; ++g) known += c.host_red[g * 2 * C];
-    check_arg(known > 0.0, "build_rhs: mask has no known pixels");
   }
+  bool known_checked = false;
 
   validate_local(o);  // checked before any sweep on every rank alike
   if (flavour == SI_FLAVOUR_ORAS)
@@ -552,13 +563,19 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
           launch_residual<T>(x, v.mask, v.b, v.b, S.w, S.h, C, 1, d_send + C, true, own.lo,
                              own.hi, v.st.lo, v.st.hi);
       }
-      gather(2 * C);
+      gather(static_cast<double>(rep->local_solves));
+      if (!known_checked) {
+        double known = 0.0;
+        for (int g = 0; g < G; ++g) known += c.host_red[g * NG + 2 * C];
+        check_arg(known > 0.0, "build_rhs: mask has no known pixels");
+        known_checked = true;
+      }
       // fixed rank order: identical sums (and decisions) on every rank
       std::vector<double> sums(C, 0.0), r0s(C, 0.0);
       for (int g = 0; g < G; ++g)
         for (int k = 0; k < C; ++k) {
-          sums[k] += c.host_red[g * 2 * C + k];
-          r0s[k] += c.host_red[g * 2 * C + C + k];
+          sums[k] += c.host_red[g * NG + k];
+          r0s[k] += c.host_red[g * NG + C + k];
         }
       if (r0_pending) {
         r0 = joint_norm(r0s.data(), C);
@@ -588,7 +605,7 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
       rep->iterations = oc.iterations;
       rep->final_relative_residual = oc.final_rel;
       rep->converged = oc.converged;
-      if (!own.empty()) {
+      if (!own.empty() && static_cast<const void*>(v.base_u[cur]) != static_cast<const void*>(d_out)) {
         const size_t rows_px = static_cast<size_t>(own.hi - own.lo) * S.w;
         Timed t(x, K_INGEST, static_cast<double>(rows_px) * C * (8.0 + sizeof(T)));
         for (int k = 0; k < C; ++k) {  // own rows of each plane -> compact output
@@ -618,16 +635,13 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
       }
     }
   }
-  // local statistics summed over ranks: failures, CG iterations, solves
-  ++c.launch_count;
-  stripe_stats_kernel<<<1, 32, 0, x.s>>>(d_cnt, static_cast<double>(rep->local_solves), d_send);
-  CK(cudaGetLastError());
-  gather(3);
+  // local statistics summed over ranks (the finest level's last gather came
+  // after the last sweep): failures, CG iterations, solves
   rep->local_failures = rep->local_cg_iterations = rep->local_solves = 0;
   for (int g = 0; g < G; ++g) {
-    rep->local_failures += static_cast<long long>(c.host_red[3 * g]);
-    rep->local_cg_iterations += static_cast<long long>(c.host_red[3 * g + 1]);
-    rep->local_solves += static_cast<long long>(c.host_red[3 * g + 2]);
+    rep->local_failures += static_cast<long long>(c.host_red[g * NG + 2 * C + 1]);
+    rep->local_cg_iterations += static_cast<long long>(c.host_red[g * NG + 2 * C + 2]);
+    rep->local_solves += static_cast<long long>(c.host_red[g * NG + 2 * C + 3]);
   }
   write_diagnostic(rep, depth, -1);
 }
