@@ -38,6 +38,9 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--no-ref", action="store_true")
     args = ap.parse_args()
+    from oracle import pyoracle as P
+    if P.ref_available():
+        P.use_tuned_reference()  # -march tuned for the host CPU when supported
     solver = si.Solver(0)
     stream = torch.cuda.current_stream()
     for name in args.configs.split(","):
