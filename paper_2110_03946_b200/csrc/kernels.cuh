@@ -221,7 +221,8 @@ __host__ __device__ constexpr int res_tma_box_w() {
 // MTMA: the mask band arrives by a second TMA box on the same barrier (row
 // pitch a multiple of 16 bytes), else per-thread byte loads.  The CTA writes
 // its partial sum; finish_partials_kernel adds them in a fixed order (no
-// fence or ticket in this kernel).
+// fence or ticket in this kernel: a last-CTA ticket finish measured 0.245 ->
+// 0.306 ms of K1 per 4K frame, round 2, as in round 1).
 template <typename T, bool INV, bool MTMA>
 __global__ void __launch_bounds__(kResTmaThreads)
     residual_sumsq_tma_kernel(const __grid_constant__ CUtensorMap umap,
@@ -322,6 +323,7 @@ __global__ void __launch_bounds__(kResTmaThreads)
 // [c][blk], for b at [C + c][blk] -- one finish over 2C "channels" leaves
 // the sums at out[0..C) and r0's at out[C..2C).  Saves one launch pair and
 // one mask pass per level against two separate K1 launches.
+constexpr int kResPairBand = 16;  // rows per CTA of the pair pass (two tiles in smem)
 template <typename T, bool MTMA>
 __global__ void __launch_bounds__(kResTmaThreads)
     residual_pair_tma_kernel(const __grid_constant__ CUtensorMap umap,
@@ -332,16 +334,16 @@ __global__ void __launch_bounds__(kResTmaThreads)
   // each TMA destination 128-byte aligned (a bare [2][18][w] array would put
   // the second tile at a 64-byte offset)
   struct __align__(128) Tile {
-    T v[kResTmaBand + 2][res_tma_box_w<T>()];
+    T v[kResPairBand + 2][res_tma_box_w<T>()];
   };
   __shared__ Tile tiles[2];
-  __shared__ __align__(128) uint8_t mtile[kResTmaBand][kResTmaThreads];
+  __shared__ __align__(128) uint8_t mtile[kResPairBand][kResTmaThreads];
   __shared__ uint64_t bar;
   const int c = blockIdx.z;
   const int x0 = blockIdx.x * kResTmaThreads;
   const int x = x0 + threadIdx.x;
-  const int y0 = row0 + static_cast<int>(blockIdx.y) * kResTmaBand;
-  const int ny = min(kResTmaBand, row1 - y0);
+  const int y0 = row0 + static_cast<int>(blockIdx.y) * kResPairBand;
+  const int ny = min(kResPairBand, row1 - y0);
   const bool xin = x < W;
   const size_t Wz = static_cast<size_t>(W);
   pdl_wait();
@@ -352,11 +354,11 @@ __global__ void __launch_bounds__(kResTmaThreads)
     tma_load_3d(&tiles[1].v[0][0], &bmap, x0 - res_tma_lead<T>(), y0 - 1 - srow_lo, c, &bar);
     if (MTMA) tma_load_2d(&mtile[0][0], &mmap, x0, y0 - srow_lo, &bar);
   }
-  uint8_t mk[kResTmaBand];
+  uint8_t mk[kResPairBand];
   if (!MTMA) {
     const size_t base = xin ? static_cast<size_t>(y0) * Wz + x : static_cast<size_t>(y0) * Wz;
 #pragma unroll
-    for (int k = 0; k < kResTmaBand; ++k) {
+    for (int k = 0; k < kResPairBand; ++k) {
       const bool in = xin && k < ny;
       const uint8_t m = __ldg(mask + (in ? base + static_cast<size_t>(k) * Wz
                                           : static_cast<size_t>(y0) * Wz));
@@ -367,7 +369,7 @@ __global__ void __launch_bounds__(kResTmaThreads)
   mbar_wait(&bar, 0);
   if (MTMA) {
 #pragma unroll
-    for (int k = 0; k < kResTmaBand; ++k)
+    for (int k = 0; k < kResPairBand; ++k)
       mk[k] = (xin && k < ny) ? mtile[k][threadIdx.x] : uint8_t(0);
   }
   const int t = threadIdx.x + res_tma_lead<T>();
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(kResTmaThreads)
     const auto& tile = tiles[v].v;
     T up = tile[0][t], ctr = tile[1][t];
 #pragma unroll
-    for (int k = 0; k < kResTmaBand; ++k) {
+    for (int k = 0; k < kResPairBand; ++k) {
       const int y = y0 + k;
       const T dn = tile[k + 2][t];
       const T sum = ((tile[k + 1][t - 1] + tile[k + 1][t + 1]) + up) + dn;

@@ -450,13 +450,13 @@ void launch_residual_pair(Ctx& x, const uint8_t* mask, const T* u, const T* b, i
   const size_t off = static_cast<size_t>(srow_lo) * W;
   CUtensorMap umap, bmap, mmap{};
   if (!tma_disabled() &&
-      make_plane_map(&umap, u + off, W, HS, C, sizeof(T), res_tma_box_w<T>(), kResTmaBand + 2) &&
-      make_plane_map(&bmap, b + off, W, HS, C, sizeof(T), res_tma_box_w<T>(), kResTmaBand + 2)) {
+      make_plane_map(&umap, u + off, W, HS, C, sizeof(T), res_tma_box_w<T>(), kResPairBand + 2) &&
+      make_plane_map(&bmap, b + off, W, HS, C, sizeof(T), res_tma_box_w<T>(), kResPairBand + 2)) {
     const int rows = std::max(1, row1 - row0);
     const int tx = (W + kResTmaThreads - 1) / kResTmaThreads;
-    const int gy = (rows + kResTmaBand - 1) / kResTmaBand;
+    const int gy = (rows + kResPairBand - 1) / kResPairBand;
     x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(tx) * gy * 2 * C);
-    const bool mtma = make_mask_map(&mmap, mask + off, W, HS, kResTmaThreads, kResTmaBand);
+    const bool mtma = make_mask_map(&mmap, mask + off, W, HS, kResTmaThreads, kResPairBand);
     Timed t(x, K_RESIDUAL,
             static_cast<double>(W) * std::max(0, row1 - row0) * (2.0 * C * sizeof(T) + 1));
     ++x.c.launch_count;

@@ -43,11 +43,16 @@ for _ in range(reps):
     frame.append(e0.elapsed_time(e1))
 s.set_profiling(True)
 sw = []
+kinds = {}
 for _ in range(reps):
     s.kernel_stats(reset=True)
     run()
     torch.cuda.synchronize()
-    sw.append(s.kernel_stats(reset=True)["sweep"]["device_ms"])
+    ks = s.kernel_stats(reset=True)
+    sw.append(ks["sweep"]["device_ms"])
+    for k, v in ks.items():
+        if isinstance(v, dict) and v["launches"]:
+            kinds.setdefault(k, []).append(v["device_ms"])
 s.set_profiling(False)
 img = out.cpu().numpy()
 ok = (list(rep.level_iterations) == [int(v) for v in g["level_iterations"]] and
@@ -56,4 +61,5 @@ ok = (list(rep.level_iterations) == [int(v) for v in g["level_iterations"]] and
       np.abs(img.reshape(-1)[g["sample_index"]] - g["sample_value"]).max() <= 1e-9)
 print(f"{os.environ.get('SI_LIB_PATH', 'default')}: frame {statistics.median(frame):.3f} ms, "
       f"sweeps {statistics.median(sw):.3f} ms, cg_its {rep.local_cg_iterations}, "
-      f"fails {rep.local_failures}, parity {'OK' if ok else 'FAIL'}")
+      f"fails {rep.local_failures}, parity {'OK' if ok else 'FAIL'}; "
+      + ", ".join(f"{k} {statistics.median(v):.3f}" for k, v in kinds.items()))
