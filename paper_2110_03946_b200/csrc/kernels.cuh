@@ -472,36 +472,66 @@ __global__ void __launch_bounds__(kRedThreads)
 
 // K5: level-0 values = f at known pixels, 0 elsewhere (build_pyramid,
 // multilevel.hpp:84-88); also counts known pixels for build_rhs's check.
+// f is read only where a pixel pair has a known pixel (at sparse masks most
+// 32-byte sectors of f are never fetched).  Each thread takes kIngestPairs
+// pixel pairs, one CTA-width apart (coalesced), and issues every mask load,
+// then a channel's f loads for all of them, before storing: the dependent
+// mask -> f chain of a pair overlaps the other pairs' (the one-pair-per-
+// iteration loop ran at 3.9 TB/s, latency-bound).
+constexpr int kIngestPairs = 4;
 template <typename T>
-__global__ void ingest_kernel(const double* __restrict__ f, const uint8_t* __restrict__ mask,
-                              size_t N, int C, T* __restrict__ b, unsigned long long* known) {
+__global__ void __launch_bounds__(256)
+    ingest_kernel(const double* __restrict__ f, const uint8_t* __restrict__ mask, size_t N,
+                  int C, T* __restrict__ b, unsigned long long* known) {
   unsigned int cnt = 0;
-  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-  const size_t pairs = N / 2;
   if (N % 2 == 0) {
-    for (size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < pairs; j += stride) {
-      const uchar2 m = reinterpret_cast<const uchar2*>(mask)[j];
-      cnt += (m.x != 0) + (m.y != 0);
-      // f is read only where a pixel of the pair is known: at sparse masks
-      // most 32-byte sectors of f are never fetched
-      const bool any = m.x || m.y;
-      for (int c = 0; c < C; ++c) {
-        double2 v = make_double2(0.0, 0.0);
-        if (any) v = __ldg(reinterpret_cast<const double2*>(f + c * N) + j);
-        T* dst = b + c * N + 2 * j;
-        dst[0] = m.x ? static_cast<T>(v.x) : T(0);
-        dst[1] = m.y ? static_cast<T>(v.y) : T(0);
+    const size_t pairs = N / 2;
+    const size_t j0 = static_cast<size_t>(blockIdx.x) * blockDim.x * kIngestPairs + threadIdx.x;
+    uchar2 m[kIngestPairs];
+#pragma unroll
+    for (int k = 0; k < kIngestPairs; ++k) {
+      const size_t j = j0 + static_cast<size_t>(k) * blockDim.x;
+      m[k] = j < pairs ? reinterpret_cast<const uchar2*>(mask)[j] : make_uchar2(0, 0);
+      cnt += (m[k].x != 0) + (m[k].y != 0);
+    }
+    for (int c = 0; c < C; ++c) {
+      double2 v[kIngestPairs];
+#pragma unroll
+      for (int k = 0; k < kIngestPairs; ++k) {
+        const size_t j = j0 + static_cast<size_t>(k) * blockDim.x;
+        v[k] = make_double2(0.0, 0.0);
+        if (j < pairs && (m[k].x || m[k].y))
+          v[k] = __ldg(reinterpret_cast<const double2*>(f + c * N) + j);
+      }
+#pragma unroll
+      for (int k = 0; k < kIngestPairs; ++k) {
+        const size_t j = j0 + static_cast<size_t>(k) * blockDim.x;
+        if (j < pairs) {
+          T* dst = b + c * N + 2 * j;
+          dst[0] = m[k].x ? static_cast<T>(v[k].x) : T(0);
+          dst[1] = m[k].y ? static_cast<T>(v[k].y) : T(0);
+        }
       }
     }
   } else {
-    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < N; i += stride) {
-      const bool k = mask[i] != 0;
-      cnt += k;
-      for (int c = 0; c < C; ++c) b[c * N + i] = k ? static_cast<T>(f[c * N + i]) : T(0);
+    const size_t i0 = static_cast<size_t>(blockIdx.x) * blockDim.x * kIngestPairs + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < kIngestPairs; ++k) {
+      const size_t i = i0 + static_cast<size_t>(k) * blockDim.x;
+      if (i >= N) break;
+      const bool kn = mask[i] != 0;
+      cnt += kn;
+      for (int c = 0; c < C; ++c) b[c * N + i] = kn ? static_cast<T>(f[c * N + i]) : T(0);
     }
   }
   cnt = __reduce_add_sync(0xffffffffu, cnt);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(known, static_cast<unsigned long long>(cnt));
+}
+
+// Grid of ingest_kernel for N pixels.
+inline unsigned ingest_grid(size_t N) {
+  const size_t units = N % 2 == 0 ? N / 2 : N;
+  return static_cast<unsigned>((units + 256 * kIngestPairs - 1) / (256 * kIngestPairs));
 }
 
 // K5s: the same level-0 values from the known samples alone (the batch
@@ -709,6 +739,146 @@ __global__ void __launch_bounds__(256, SI_PRO_OCC)
       }
     }
   }
+}
+
+// K4 with the coarse windows fetched by TMA into a two-stage ring: a
+// persistent CTA walks fine tiles of kProX x kProY; thread 0 issues the next
+// tile's window (one box of kProBoxW x kProCY per channel; columns or rows
+// outside the coarse level arrive as zeros and are never read: the sample
+// coordinates are clamped to the level, multilevel.hpp:109-115) while the
+// CTA computes the current one from shared memory.  The one-shot kernel
+// above loaded its window with per-thread loads, then waited at a barrier
+// (long-scoreboard bound, 3.0 TB/s on the finest 4K level).
+// The box must start at a 16-byte aligned column (a misaligned start raises
+// an illegal-instruction fault on B200, cf. tile_lead in sweep.cuh): it
+// starts pro_lead columns left of the tile's first coarse column and is
+// wide enough for its kProCX - 1 columns right of it.
+template <typename T>
+__host__ __device__ constexpr int pro_lead() {
+  return 16 / static_cast<int>(sizeof(T));
+}
+template <typename T>
+__host__ __device__ constexpr int pro_box_w() {
+  return sizeof(T) == 8 ? kProCX + 2 : kProCX + 6;  // 36 x 8 B / 40 x 4 B rows
+}
+constexpr int kProMaxC = 4;  // channels per tile window (more: the one-shot kernel)
+template <typename T>
+struct __align__(128) ProSlice {  // one channel's window, a 128-byte multiple
+  T v[kProCY][pro_box_w<T>()];
+  char pad[(128 - (sizeof(T) * kProCY * pro_box_w<T>()) % 128) % 128];
+};
+
+// MT: the tile's fine mask bytes ride on the same barrier (a 2-D box of
+// kProX x kProY; needs a 16-byte multiple mask row pitch), else byte loads.
+template <typename T, bool MT>
+__global__ void __launch_bounds__(256, 4)
+    prolong_snap_tma_kernel(const __grid_constant__ CUtensorMap cmap,
+                            const __grid_constant__ CUtensorMap mmap, int cw, int ch, int fw,
+                            int C, const uint8_t* __restrict__ fmask, const T* __restrict__ fval,
+                            T* __restrict__ fine, int fy_lo, int fy_hi, int cs_lo, int fs_lo,
+                            size_t fn, int tiles_x, int ntiles) {
+  __shared__ ProSlice<T> ring[2][kProMaxC];
+  __shared__ __align__(128) uint8_t mring[2][kProY][kProX];
+  __shared__ uint64_t bar[2];
+  const int tid = threadIdx.x;
+  const int qx = tid & 31, qy = tid >> 5;
+  const uint32_t box_bytes = static_cast<uint32_t>(sizeof(T) * kProCY * pro_box_w<T>()) * C +
+                             (MT ? static_cast<uint32_t>(kProX * kProY) : 0u);
+  pdl_wait();
+  // (no lambda here: the tensor map must be addressed in parameter space;
+  // a by-reference capture can make the compiler spill it to the stack)
+#define SI_PRO_ISSUE(t_, stage_)                                                              \
+  do {                                                                                        \
+    const int ifx0 = ((t_) % tiles_x) * kProX, ify0 = fy_lo + ((t_) / tiles_x) * kProY;         \
+    mbar_expect_tx(&bar[(stage_)], box_bytes);                                                \
+    for (int kc = 0; kc < C; ++kc)                                                            \
+      tma_load_3d(&ring[(stage_)][kc].v[0][0], &cmap, ifx0 / 2 - pro_lead<T>(),                \
+                  ify0 / 2 - 1 - cs_lo, kc, &bar[(stage_)]);                                  \
+    if (MT) tma_load_2d(&mring[(stage_)][0][0], &mmap, ifx0, ify0 - fs_lo, &bar[(stage_)]);    \
+  } while (0)
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    if (static_cast<int>(blockIdx.x) < ntiles) SI_PRO_ISSUE(static_cast<int>(blockIdx.x), 0);
+  }
+  __syncthreads();
+  int k = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int stage = k & 1;
+    if (tid == 0 && t + static_cast<int>(gridDim.x) < ntiles)
+      SI_PRO_ISSUE(t + static_cast<int>(gridDim.x), stage ^ 1);
+    const int fx0 = (t % tiles_x) * kProX, fy0 = fy_lo + (t / tiles_x) * kProY;
+    const int cx0 = fx0 / 2 - pro_lead<T>(), cy0 = fy0 / 2 - 1;  // window origin
+    const int fxq = fx0 + 2 * qx, fyq = fy0 + 2 * qy;
+    unsigned snap = 0;
+    if (!MT && fmask != nullptr) {
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx)
+          if (fyq + dy < fy_hi && fxq + dx < fw &&
+              fmask[static_cast<size_t>(fyq + dy) * fw + fxq + dx])
+            snap |= 1u << (2 * dy + dx);
+    }
+    double txd[2];
+    int xb0[2], xb1[2];
+#pragma unroll
+    for (int dx = 0; dx < 2; ++dx) {
+      int xa, xb;
+      prolong_axis<T>(min(fxq + dx, fw - 1), cw, txd[dx], xa, xb);
+      xb0[dx] = xa - cx0;
+      xb1[dx] = xb - cx0;
+    }
+    const bool pair_store = (fw % 2 == 0) && fxq + 1 < fw;
+    mbar_wait(&bar[stage], (k >> 1) & 1);
+    if (MT) {  // rows / columns past the level arrive as zeros: no snap there
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx)
+          if (fyq + dy < fy_hi && mring[stage][2 * qy + dy][2 * qx + dx])
+            snap |= 1u << (2 * dy + dx);
+    }
+    for (int c = 0; c < C; ++c) {
+      const auto& tile = ring[stage][c].v;
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy) {
+        const int fy = fyq + dy;
+        if (fy >= fy_hi || fxq >= fw) continue;
+        double tyd;
+        int ya, yb;
+        prolong_axis<T>(fy, ch, tyd, ya, yb);
+        const T ty = static_cast<T>(tyd);
+        const int a0 = ya - cy0, a1 = yb - cy0;
+        const size_t i = static_cast<size_t>(fy) * fw + fxq;
+        T v[2];
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+          const T tx = static_cast<T>(txd[dx]);
+          const int b0 = xb0[dx], b1 = xb1[dx];
+          const T v00 = tile[a0][b0], v01 = tile[a0][b1];
+          const T v10 = tile[a1][b0], v11 = tile[a1][b1];
+          // gcc -O3's contraction of the reference expression (see above)
+          const T p0 = fma(T(1) - tx, v00, tx * v01);
+          const T p1 = fma(T(1) - tx, v10, tx * v11);
+          v[dx] = fma(T(1) - ty, p0, ty * p1);
+          if ((snap >> (2 * dy + dx)) & 1u) v[dx] = __ldg(fval + c * fn + i + dx);
+        }
+        T* dst = fine + c * fn + i;
+        if (pair_store) {
+          if constexpr (sizeof(T) == 8)
+            *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[1]);
+          else
+            *reinterpret_cast<float2*>(dst) = make_float2(v[0], v[1]);
+        } else {
+          dst[0] = v[0];
+          if (fxq + 1 < fw) dst[1] = v[1];
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with this stage before it is refilled
+  }
+#undef SI_PRO_ISSUE
 }
 
 // read_pnm / read_mask_pbm payloads (pnm.hpp:98-188): interleaved bytes ->

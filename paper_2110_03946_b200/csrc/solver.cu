@@ -514,17 +514,52 @@ void launch_restrict(Ctx& x, const uint8_t* fmask, const T* fval, int fw, int fh
 }
 
 // Fine rows [fy_lo, fy_hi); coarse storage rows [cs_lo, cs_hi); fn / cn
-// storage planes (stripe mode; defaults: the whole image).
+// storage planes; fine storage starts at row fs_lo_arg (stripe mode;
+// defaults: the whole image).
 template <typename T>
 void launch_prolong(Ctx& x, const T* coarse, int cw, int ch, int fw, int fh, int C,
                     const uint8_t* fmask, const T* fval, T* fine, int fy_lo = 0, int fy_hi = -1,
-                    int cs_lo = 0, int cs_hi = -1, size_t fn = 0, size_t cn = 0) {
+                    int cs_lo = 0, int cs_hi = -1, size_t fn = 0, size_t cn = 0,
+                    int fs_lo_arg = 0) {
   if (fy_hi < 0) fy_hi = fh;
   if (cs_hi < 0) cs_hi = ch;
   if (fn == 0) fn = static_cast<size_t>(fw) * fh;
   if (cn == 0) cn = static_cast<size_t>(cw) * ch;
   if (fy_hi <= fy_lo) return;
-  const dim3 grid((fw + kProX - 1) / kProX, (fy_hi - fy_lo + kProY - 1) / kProY);
+  const int tiles_x = (fw + kProX - 1) / kProX, tiles_y = (fy_hi - fy_lo + kProY - 1) / kProY;
+  CUtensorMap cmap;
+  if (C <= kProMaxC && !tma_disabled() &&
+      make_plane_map(&cmap, coarse + static_cast<size_t>(cs_lo) * cw, cw, cs_hi - cs_lo, C,
+                     sizeof(T), pro_box_w<T>(), kProCY) &&
+      reinterpret_cast<uintptr_t>(coarse + static_cast<size_t>(cs_lo) * cw) % 16 == 0 &&
+      (cn * sizeof(T)) % 16 == 0) {
+    // persistent CTAs, 4 per SM, each walking tiles with a 2-stage TMA ring
+    static int sms = [] {
+      int d = 0, n = 148;
+      if (cudaGetDevice(&d) == cudaSuccess)
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+      return n;
+    }();
+    const int ntiles = tiles_x * tiles_y;
+    const int grid = std::min(ntiles, sms * 4);
+    // the fine mask tile by TMA too when its rows are 16-byte aligned (the
+    // map covers the fine storage rows [fs_lo, fs_lo + fn / fw))
+    const int fs_lo = fs_lo_arg;
+    CUtensorMap mmap{};
+    const bool mt = fmask != nullptr &&
+                    make_mask_map(&mmap, fmask + static_cast<size_t>(fs_lo) * fw, fw,
+                                  static_cast<int>(fn / fw), kProX, kProY);
+    ++x.c.launch_count;
+    if (mt)
+      launch_pdl(prolong_snap_tma_kernel<T, true>, dim3(grid), 256, x.s, cmap, mmap, cw, ch, fw, C,
+                 fmask, fval, fine, fy_lo, fy_hi, cs_lo, fs_lo, fn, tiles_x, ntiles);
+    else
+      launch_pdl(prolong_snap_tma_kernel<T, false>, dim3(grid), 256, x.s, cmap, mmap, cw, ch, fw,
+                 C, fmask, fval, fine, fy_lo, fy_hi, cs_lo, fs_lo, fn, tiles_x, ntiles);
+    CK(cudaGetLastError());
+    return;
+  }
+  const dim3 grid(tiles_x, tiles_y);
   ++x.c.launch_count;
   launch_pdl(prolong_snap_kernel<T>, grid, 256, x.s, coarse, cw, ch, fw, fh, C, fmask, fval, fine,
              fy_lo, fy_hi, cs_lo, cs_hi, fn, cn);
@@ -1288,7 +1323,7 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
   } else {
     Timed t(x, K_INGEST, static_cast<double>(n0) * (C * (8.0 + sizeof(T)) + 1.0));
     ++x.c.launch_count;
-    ingest_kernel<T><<<grid_for(n0, 256, 148 * 16), 256, 0, x.s>>>(
+    ingest_kernel<T><<<ingest_grid(n0), 256, 0, x.s>>>(
         d_f, d_mask, n0, C, x.c.levels[0].b.as<T>(), x.c.counters.as<unsigned long long>() + 2);
     CK(cudaGetLastError());
   }

@@ -470,7 +470,7 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     if (n0) {
       Timed t(x, K_INGEST, static_cast<double>(n0) * (C * (8.0 + sizeof(T)) + 1.0));
       ++c.launch_count;
-      ingest_kernel<T><<<grid_for(n0, 256, 148 * 16), 256, 0, x.s>>>(
+      ingest_kernel<T><<<ingest_grid(n0), 256, 0, x.s>>>(
           d_f, d_mask, n0, C, V[0].base_b, c.counters.as<unsigned long long>() + 2);
       CK(cudaGetLastError());
     }
@@ -631,7 +631,7 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
       if (!fw.empty()) {
         Timed t(x, K_PROLONG, static_cast<double>(fw.hi - fw.lo) * F.w * (2.0 * C * sizeof(T) + 1.0));
         launch_prolong<T>(x, v.u[cur], S.w, S.h, F.w, F.h, C, fv.mask, fv.b, fv.u[0], fw.lo,
-                          fw.hi, v.st.lo, v.st.hi, fv.rows_n, v.rows_n);
+                          fw.hi, v.st.lo, v.st.hi, fv.rows_n, v.rows_n, fv.st.lo);
       }
     }
   }
