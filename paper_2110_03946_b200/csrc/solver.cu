@@ -533,7 +533,7 @@ void launch_prolong(Ctx& x, const T* coarse, int cw, int ch, int fw, int fh, int
                      sizeof(T), pro_box_w<T>(), kProCY) &&
       reinterpret_cast<uintptr_t>(coarse + static_cast<size_t>(cs_lo) * cw) % 16 == 0 &&
       (cn * sizeof(T)) % 16 == 0) {
-    // persistent CTAs, 4 per SM, each walking tiles with a 2-stage TMA ring
+    // persistent CTAs (kProTmaOcc per SM), each walking tiles with a 2-stage TMA ring
     static int sms = [] {
       int d = 0, n = 148;
       if (cudaGetDevice(&d) == cudaSuccess)
@@ -541,7 +541,7 @@ void launch_prolong(Ctx& x, const T* coarse, int cw, int ch, int fw, int fh, int
       return n;
     }();
     const int ntiles = tiles_x * tiles_y;
-    const int grid = std::min(ntiles, sms * 4);
+    const int grid = std::min(ntiles, sms * kProTmaOcc);
     // the fine mask tile by TMA too when its rows are 16-byte aligned (the
     // map covers the fine storage rows [fs_lo, fs_lo + fn / fw))
     const int fs_lo = fs_lo_arg;
