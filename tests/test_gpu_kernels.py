@@ -98,8 +98,10 @@ def test_prolongation_rejects_mismatch(solver):
             solver.prolongate(np.zeros(4), *args)
 
 
-@pytest.mark.parametrize("fw,fh", [(73, 45), (8, 8), (3, 1), (640, 361)])
+@pytest.mark.parametrize("fw,fh", [(73, 45), (8, 8), (3, 1), (640, 361), (1920, 1080), (260, 131)])
 def test_prolongation_bitwise_vs_oracle(solver, oracle, fw, fh):
+    """Even coarse widths take the persistent TMA-ring kernel, odd ones the
+    one-shot kernel; both bit-identical to the oracle (multilevel.hpp:101-128)."""
     cw, ch = (fw + 1) // 2, (fh + 1) // 2
     coarse = np.random.default_rng(fw).uniform(0, 1, (ch, cw))
     got = solver.prolongate(coarse, cw, ch, fw, fh).reshape(fh, fw)
