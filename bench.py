@@ -401,7 +401,7 @@ def main():
 
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or "WORLD_SIZE" in os.environ:  # under torchrun (even one rank: NCCL paths)
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
