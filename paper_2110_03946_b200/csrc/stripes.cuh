@@ -457,7 +457,7 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     v.u[0] = v.base_u[0] - off;
     v.u[1] = v.base_u[1] - off;
   }
-  // comm scratch: [sums C | r0 C] per rank, gathered G x 2C
+  // comm scratch: one row of NG = 2C + 4 doubles per rank (see gather below)
   c.stripe_send.ensure(sizeof(double) * (2 * C + 4));
   c.stripe_recv.ensure(sizeof(double) * (2 * C + 4) * G);
   double* d_send = c.stripe_send.as<double>();
@@ -514,7 +514,7 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
   }
   bool known_checked = false;
 
-  validate_local(o);  // checked before any sweep on every rank alike
+  bool local_checked = false;  // cg_solve's config check before the first sweep (cg.hpp:75-80)
   if (flavour == SI_FLAVOUR_ORAS)
     check_arg(std::isfinite(o.alpha), "run_schwarz_level: alpha must be finite");
   const LocalCfg lc{o.local_tolerance, o.local_max_iterations, o.local_check_interval};
@@ -591,6 +591,10 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
       }
       if (outer >= o.max_outer_iterations) break;
       NvtxRange nv_sweep("stripe sweep + halo");
+      if (!local_checked) {  // every rank takes the same decisions: all fail alike
+        validate_local(o);
+        local_checked = true;
+      }
       if (S.k1 > S.k0)
         launch_sweep<T>(x, v.mask, v.b, v.u[cur], v.u[cur ^ 1], S.w, S.h, C, S.block, S.overlap,
                         flavour, o.alpha, lc, true, d_cnt, S.k0, S.k1, v.st.lo, v.st.hi);
