@@ -534,6 +534,127 @@ inline unsigned ingest_grid(size_t N) {
   return static_cast<unsigned>((units + 256 * kIngestPairs - 1) / (256 * kIngestPairs));
 }
 
+// K5 + K3 in one pass (the whole-image device path): level-0 values
+// b0 = f at known pixels, 0 elsewhere (multilevel.hpp:84-88), AND the first
+// restriction (multilevel.hpp:33-70) from the values just made -- b0 is
+// written once and never read back.  One thread per coarse pixel (a 2x2
+// fine cell, clipped at odd edges); the accumulation order is
+// restrict_kernel's (row-major over the cell, KnownOnly or AllPixels).
+#ifndef SI_IR_CELLS
+#define SI_IR_CELLS 2  // measured: 1 -> 0.092, 2 -> 0.077, 4 -> 0.106 ms per 4K frame
+#endif
+constexpr int kIrCells = SI_IR_CELLS;  // coarse cells per thread (kIrCells x 128 per CTA row)
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(128)
+    ingest_restrict_kernel(const double* __restrict__ f, const uint8_t* __restrict__ fmask,
+                           int fw, int fh, int C, int averaging, T* __restrict__ b0,
+                           uint8_t* __restrict__ cmask, T* __restrict__ cval,
+                           unsigned long long* known_count) {
+  const int cw = (fw + 1) / 2;
+  const int cy = blockIdx.y;
+  const size_t fn = static_cast<size_t>(fw) * fh, cn = static_cast<size_t>(cw) * ((fh + 1) / 2);
+  const int fy0 = 2 * cy;
+  const bool two_y = fy0 + 1 < fh;
+  const bool all = averaging != 0;
+  unsigned cnt = 0;
+  // every cell's mask bits first (kIrCells cells, 128 apart: coalesced), then
+  // a channel's f loads for all of them, then the stores
+  unsigned kb[kIrCells];
+#pragma unroll
+  for (int q = 0; q < kIrCells; ++q) {
+    const int cx = (blockIdx.x * kIrCells + q) * blockDim.x + threadIdx.x;
+    kb[q] = 0;
+    if (cx >= cw) continue;
+    const int fx0 = 2 * cx;
+    const bool two_x = fx0 + 1 < fw;
+    const size_t r0 = static_cast<size_t>(fy0) * fw + fx0, r1 = r0 + fw;
+    if (VEC) {  // fw even: both columns exist
+      const uchar2 m0 = *reinterpret_cast<const uchar2*>(fmask + r0);
+      kb[q] |= (m0.x != 0) | (m0.y != 0) << 1;
+      if (two_y) {
+        const uchar2 m1 = *reinterpret_cast<const uchar2*>(fmask + r1);
+        kb[q] |= (m1.x != 0) << 2 | (m1.y != 0) << 3;
+      }
+    } else {
+      kb[q] |= (fmask[r0] != 0) | (two_x && fmask[r0 + 1] != 0) << 1;
+      if (two_y) kb[q] |= (fmask[r1] != 0) << 2 | (two_x && fmask[r1 + 1] != 0) << 3;
+    }
+    const int known = __popc(kb[q]);
+    cnt += known;
+    cmask[static_cast<size_t>(cy) * cw + cx] = known ? 1 : 0;
+  }
+  for (int c = 0; c < C; ++c) {
+    const double* fc = f + c * fn;
+    T* bc = b0 + c * fn;
+    Pair<T> a[kIrCells], bb[kIrCells];
+#pragma unroll
+    for (int q = 0; q < kIrCells; ++q) {  // f is read only where the cell has a known pixel
+      const int cx = (blockIdx.x * kIrCells + q) * blockDim.x + threadIdx.x;
+      a[q] = {T(0), T(0)};
+      bb[q] = {T(0), T(0)};
+      if (cx >= cw || !kb[q]) continue;
+      const int fx0 = 2 * cx;
+      const bool two_x = fx0 + 1 < fw;
+      const size_t r0 = static_cast<size_t>(fy0) * fw + fx0, r1 = r0 + fw;
+      if (VEC) {
+        const double2 v0 = __ldg(reinterpret_cast<const double2*>(fc + r0));
+        a[q] = {(kb[q] & 1) ? static_cast<T>(v0.x) : T(0), (kb[q] & 2) ? static_cast<T>(v0.y) : T(0)};
+        if (two_y) {
+          const double2 v1 = __ldg(reinterpret_cast<const double2*>(fc + r1));
+          bb[q] = {(kb[q] & 4) ? static_cast<T>(v1.x) : T(0),
+                   (kb[q] & 8) ? static_cast<T>(v1.y) : T(0)};
+        }
+      } else {
+        a[q].a = (kb[q] & 1) ? static_cast<T>(fc[r0]) : T(0);
+        if (two_x) a[q].b = (kb[q] & 2) ? static_cast<T>(fc[r0 + 1]) : T(0);
+        if (two_y) {
+          bb[q].a = (kb[q] & 4) ? static_cast<T>(fc[r1]) : T(0);
+          if (two_x) bb[q].b = (kb[q] & 8) ? static_cast<T>(fc[r1 + 1]) : T(0);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kIrCells; ++q) {
+      const int cx = (blockIdx.x * kIrCells + q) * blockDim.x + threadIdx.x;
+      if (cx >= cw) continue;
+      const int fx0 = 2 * cx;
+      const bool two_x = fx0 + 1 < fw;
+      const size_t r0 = static_cast<size_t>(fy0) * fw + fx0, r1 = r0 + fw;
+      if (VEC) {
+        if constexpr (sizeof(T) == 8) {
+          *reinterpret_cast<double2*>(bc + r0) = make_double2(a[q].a, a[q].b);
+          if (two_y) *reinterpret_cast<double2*>(bc + r1) = make_double2(bb[q].a, bb[q].b);
+        } else {
+          *reinterpret_cast<float2*>(bc + r0) = make_float2(a[q].a, a[q].b);
+          if (two_y) *reinterpret_cast<float2*>(bc + r1) = make_float2(bb[q].a, bb[q].b);
+        }
+      } else {
+        bc[r0] = a[q].a;
+        if (two_x) bc[r0 + 1] = a[q].b;
+        if (two_y) {
+          bc[r1] = bb[q].a;
+          if (two_x) bc[r1 + 1] = bb[q].b;
+        }
+      }
+      // restrict_kernel's accumulation order (row-major over the cell)
+      const int known = __popc(kb[q]);
+      const int total = (1 + two_x) * (1 + two_y);
+      T acc = T(0);
+      if (known) {
+        if (all || (kb[q] & 1)) acc += a[q].a;
+        if (two_x && (all || (kb[q] & 2))) acc += a[q].b;
+        if (two_y && (all || (kb[q] & 4))) acc += bb[q].a;
+        if (two_x && two_y && (all || (kb[q] & 8))) acc += bb[q].b;
+        acc = acc / T(all ? total : known);
+      }
+      cval[c * cn + static_cast<size_t>(cy) * cw + cx] = acc;
+    }
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(known_count, static_cast<unsigned long long>(cnt));
+  pdl_trigger();
+}
+
 // K5s: the same level-0 values from the known samples alone (the batch
 // upload, host_copy.h): vals[c*K + rank] is the rank-th known pixel's value,
 // tile_off[t] the known count before tile t (kKnownTile = 4096 pixels).

@@ -310,6 +310,12 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+// SI_NO_INGEST_FUSION=1: separate K5 ingest and K3 restriction (A/B).
+bool ingest_fusion_disabled() {
+  static const bool off = std::getenv("SI_NO_INGEST_FUSION") != nullptr;
+  return off;
+}
+
 // SI_NO_TMA=1 forces the cooperative / cp.async staging paths (A/B runs).
 bool tma_disabled() {
   static const bool off = std::getenv("SI_NO_TMA") != nullptr;
@@ -1312,6 +1318,7 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
   }
   // K5 ingest: level-0 values, known count for build_rhs's check.
   const size_t n0 = static_cast<size_t>(w) * h;
+  bool fused_restrict = false;
   if (ks) {  // K5s: only the known samples came over
     Timed t(x, K_INGEST, static_cast<double>(n0) * (C * sizeof(T) + 1.0) + ks->K * C * 8.0);
     ++x.c.launch_count;
@@ -1320,6 +1327,24 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
         d_mask, n0, C, ks->vals, ks->K, ks->tile_off, x.c.levels[0].b.as<T>(),
         x.c.counters.as<unsigned long long>() + 2);
     CK(cudaGetLastError());
+  } else if (depth > 1 && !ingest_fusion_disabled()) {
+    // K5 + K3 fused: level-0 values and level 1 in one pass
+    Timed t(x, K_INGEST, static_cast<double>(n0) * (C * (8.0 + sizeof(T)) + 1.0) +
+                             static_cast<double>(lw[1]) * lh[1] * (C * sizeof(T) + 1));
+    const dim3 grid((lw[1] + 128 * kIrCells - 1) / (128 * kIrCells), lh[1]);
+    ++x.c.launch_count;
+    if (w % 2 == 0)
+      ingest_restrict_kernel<T, true><<<grid, 128, 0, x.s>>>(
+          d_f, d_mask, w, h, C, o.averaging, x.c.levels[0].b.as<T>(),
+          x.c.levels[1].mask.as<uint8_t>(), x.c.levels[1].b.as<T>(),
+          x.c.counters.as<unsigned long long>() + 2);
+    else
+      ingest_restrict_kernel<T, false><<<grid, 128, 0, x.s>>>(
+          d_f, d_mask, w, h, C, o.averaging, x.c.levels[0].b.as<T>(),
+          x.c.levels[1].mask.as<uint8_t>(), x.c.levels[1].b.as<T>(),
+          x.c.counters.as<unsigned long long>() + 2);
+    CK(cudaGetLastError());
+    fused_restrict = true;
   } else {
     Timed t(x, K_INGEST, static_cast<double>(n0) * (C * (8.0 + sizeof(T)) + 1.0));
     ++x.c.launch_count;
@@ -1327,8 +1352,8 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
         d_f, d_mask, n0, C, x.c.levels[0].b.as<T>(), x.c.counters.as<unsigned long long>() + 2);
     CK(cudaGetLastError());
   }
-  // K3: restrict level by level.
-  for (int l = 1; l < depth; ++l) {
+  // K3: restrict level by level (level 1 already made by the fused pass).
+  for (int l = fused_restrict ? 2 : 1; l < depth; ++l) {
     const size_t cn = static_cast<size_t>(lw[l]) * lh[l];
     Timed t(x, K_RESTRICT, static_cast<double>(cn) * 4.0 * (C * sizeof(T) + 1) + cn * (C * sizeof(T) + 1));
     launch_restrict<T>(x, L[l - 1].mask, L[l - 1].b, lw[l - 1], lh[l - 1], C, o.averaging,
