@@ -8,7 +8,7 @@ outer ORAS iterations to the reference's residual tolerance (1e-3 finest,
 reference's run_method(Method::MultilevelOras) with default RunOptions.
 
   value : frames/s with inputs resident in HBM (si_run_method_device),
-          --inflight independent frames at a time (default 2: one context,
+          --inflight independent frames at a time (default 4: one context,
           stream and host thread each), CUDA events on the launching stream
           bracketing every lane's stream, max over ranks.
   e2e   : frames/s through the public host batch API (si_run_method_batch)
@@ -86,8 +86,9 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--precision", default="fp64", choices=["fp64", "fp32", "mixed"])
-    p.add_argument("--frames", type=int, default=2, help="distinct frames per rank")
-    p.add_argument("--inflight", type=int, default=2,
+    p.add_argument("--frames", type=int, default=4, help="distinct frames per rank")
+    # frames in flight (round 2, 4K fp64, frames/s): 1 -> 325, 2 -> 340, 3 -> 343, 4 -> 346
+    p.add_argument("--inflight", type=int, default=4,
                    help="frames in flight per rank (one context, stream and host thread each)")
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--no-cpu-baseline", action="store_true")
