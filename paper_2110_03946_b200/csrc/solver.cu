@@ -2972,6 +2972,7 @@ si_status si_stripe_comm_init_local(si_ctx* const* ctxs, int world, si_stripe_co
     grp->done.assign(world, nullptr);
     grp->posted.resize(world);
     grp->posted_vals.assign(world, nullptr);
+    grp->posted_sends.assign(world, nullptr);
     for (int r = 0; r < world; ++r) {
       check_arg(ctxs[r] != nullptr, "null context");
       set_device(ctxs[r]);

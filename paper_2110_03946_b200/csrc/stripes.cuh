@@ -281,6 +281,7 @@ struct LocalGroup {
   std::vector<cudaEvent_t> ready, done;
   std::vector<RowBuf> posted;
   std::vector<const double*> posted_vals;
+  std::vector<const std::vector<RowXfer>*> posted_sends;
 
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
@@ -332,10 +333,27 @@ struct LocalComm final : si_stripe_comm {
       }
     });
   }
-  void exchange(const std::vector<RowXfer>&, const std::vector<RowXfer>& recvs, const RowBuf& buf,
-                cudaStream_t s) override {
+  void exchange(const std::vector<RowXfer>& sends, const std::vector<RowXfer>& recvs,
+                const RowBuf& buf, cudaStream_t s) override {
     g->posted[rank] = buf;
+    g->posted_sends[rank] = &sends;
     round(s, [&] {
+      // the pairing NCCL relies on (NcclComm::exchange): every peer's sends
+      // to me, in order, are exactly my receives from it -- checked here on
+      // every exchange, so the local-communicator tests cover the NCCL plan
+      for (int p = 0; p < world; ++p) {
+        if (p == rank) continue;
+        size_t k = 0;
+        for (const RowXfer& x : *g->posted_sends[p]) {
+          if (x.peer != rank) continue;
+          while (k < recvs.size() && recvs[k].peer != p) ++k;
+          check_arg(k < recvs.size() && recvs[k].lo == x.lo && recvs[k].hi == x.hi,
+                    "stripes: send/receive plans of two ranks disagree");
+          ++k;
+        }
+        for (; k < recvs.size(); ++k)
+          check_arg(recvs[k].peer != p, "stripes: a receive without a matching send");
+      }
       int last = -1;
       for (const RowXfer& x : recvs) {
         if (x.peer != last) CK(cudaStreamWaitEvent(s, g->ready[x.peer], 0));
