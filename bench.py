@@ -34,6 +34,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# measured DFMA peak (scripts/fp64_peak.cu, profiles/r02_fp64_peak.json)
+FP64_PEAK_TF = 34.2
 METRIC = "4K RGB inpaint frames/s at fixed residual tol; fraction of HBM roofline"
 W4K, H4K, C4K, DENSITY, LEVELS = 3840, 2160, 3, 0.04, 3
 
@@ -507,8 +509,9 @@ def main():
     # a separate pass of the same frames: the roofline numbers below
     prof_steps = min(args.steps, 4)
     solver.set_profiling(True)
+    cg_its = []
     for j in range(prof_steps):
-        step(j)
+        cg_its.append(step(j).local_cg_iterations)
     torch.cuda.synchronize()
     solver.set_profiling(False)
     stats = solver.kernel_stats(reset=True)
@@ -586,6 +589,8 @@ def main():
 
     # ---- roofline of the dominant kernel (K2 sweep)
     sw = stats["sweep"]
+    fp64_tf = (15.0 * 1024 * float(np.sum(cg_its)) / (sw["device_ms"] / 1e3) / 1e12
+               if sw["device_ms"] else None)
     peak, peak_src = hbm_peak()
     achieved = (sw["algorithmic_bytes"] / (sw["device_ms"] / 1e3) / 1e9) if sw["device_ms"] else 0.0
     traffic, traffic_alg, fp64_pct = None, None, None
@@ -619,6 +624,15 @@ def main():
                      "frame_bytes": frame_bytes_survey,
                      "frame_bytes_formula": "SURVEY.md 8d per-frame formula with the measured k_L",
                      "sweep_share_of_step": sw["device_ms"] / max(total_dev, 1e-9),
+                     # informational: 15 FP64 flops per cell per local CG iteration
+                     # (stencil 5, two dots 4, three axpys 6) x 1,024 cells, counted
+                     # on the device (report.local_cg_iterations)
+                     "sweep_fp64_tflops": fp64_tf,
+                     "fp64_peak_tflops": FP64_PEAK_TF,
+                     "sweep_fp64_frac": fp64_tf / FP64_PEAK_TF if fp64_tf else None,
+                     "fp64_peak_source": "scripts/fp64_peak.cu on a B200 of this pool "
+                                         "(8 DFMA chains/thread, 1965 MHz): "
+                                         "profiles/r02_fp64_peak.json",
                      "onchip_bound": {"pipe": "fp64", "pct_of_peak": fp64_pct,
                                       "source": "ncu --set full, first finest-level sweep"}},
         "e2e": {"value": e2e_value, "unit": "frames/s",
