@@ -224,6 +224,15 @@ si_status si_stripe_comm_init_nccl(si_ctx* ctx, int world, int rank, const unsig
 /* comms_out[r] for r < world, rank r driven on ctxs[r] (one host thread each). */
 si_status si_stripe_comm_init_local(si_ctx* const* ctxs, int world, si_stripe_comm** comms_out);
 void si_stripe_comm_destroy(si_stripe_comm* comm);
+/* Outer iterations are decided on the device.  With speculation on (the
+ * default) a solve issues, per level, as many iterations as the last solve
+ * with the same shape and options took, without a host round trip; a level
+ * that needed more is resumed and the finer levels after it are redone
+ * (results identical).  Off: one host round trip per decision.  Every rank
+ * of a group must use the same setting. */
+si_status si_stripe_comm_set_speculation(si_stripe_comm* comm, int enabled);
+/* out[0] solves, out[1] solves that speculated, out[2] resumed levels. */
+si_status si_stripe_comm_counters(const si_stripe_comm* comm, long long* out /* 3 */);
 
 /* Rows of every level for `rank` (host only, no device): out receives
  * SI_STRIPE_PLAN_INTS ints per level (index 0 = finest): k0, k1 (block rows),

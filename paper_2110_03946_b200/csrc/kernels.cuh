@@ -94,11 +94,12 @@ __global__ void __launch_bounds__(kRedThreads)
     residual_sumsq_kernel(const uint8_t* __restrict__ mask, const T* __restrict__ u,
                           const T* __restrict__ b, int W, int H, size_t N, int mode, int row0,
                           int row1, int srow_lo, int srow_hi, double* partials, double* out,
-                          unsigned int* ticket) {
+                          unsigned int* ticket, const int* __restrict__ skip) {
   // rows [row0, row1) only (stripe mode); the stencil still sees rows
   // row0-1 and row1 as neighbours.  The buffers hold rows [srow_lo, srow_hi)
   // (pointers pre-offset, N = storage plane); whole image: 0 and H.
   __shared__ T tile[kResBand + 2][kResTileW];
+  if (skip != nullptr && *skip) return;  // stripes: the level has stopped (every CTA alike)
   const int c = blockIdx.z;
   const T* __restrict__ uc = u + c * N;
   const T* __restrict__ bc = b + c * N;
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(kResTmaThreads)
                               const __grid_constant__ CUtensorMap mmap,
                               const uint8_t* __restrict__ mask, const T* __restrict__ b, int W,
                               int H, size_t N, int row0, int row1, int srow_lo,
-                              double* partials) {
+                              double* partials, const int* __restrict__ skip) {
   __shared__ __align__(128) T tile[kResTmaBand + 2][res_tma_box_w<T>()];
   __shared__ __align__(128) uint8_t mtile[kResTmaBand][kResTmaThreads];
   __shared__ uint64_t bar;
@@ -242,6 +243,7 @@ __global__ void __launch_bounds__(kResTmaThreads)
   const bool xin = x < W;
   const size_t Wz = static_cast<size_t>(W);
   pdl_wait();  // u is the predecessor's output
+  if (skip != nullptr && *skip) return;  // stripes: the level has stopped (every CTA alike)
   if (threadIdx.x == 0) {
 #ifdef SI_TMA_DEBUG
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
@@ -549,10 +551,15 @@ __global__ void __launch_bounds__(128)
     ingest_restrict_kernel(const double* __restrict__ f, const uint8_t* __restrict__ fmask,
                            int fw, int fh, int C, int averaging, T* __restrict__ b0,
                            uint8_t* __restrict__ cmask, T* __restrict__ cval,
-                           unsigned long long* known_count) {
+                           unsigned long long* known_count, int cy0 = 0, size_t fn_s = 0,
+                           size_t cn_s = 0) {
+  // stripes: coarse rows cy0 + blockIdx.y; f / fmask / b0 / cmask / cval are
+  // pre-offset storage pointers (index with global rows) whose planes are
+  // fn_s / cn_s apart; whole image: 0, 0, 0
   const int cw = (fw + 1) / 2;
-  const int cy = blockIdx.y;
-  const size_t fn = static_cast<size_t>(fw) * fh, cn = static_cast<size_t>(cw) * ((fh + 1) / 2);
+  const int cy = cy0 + static_cast<int>(blockIdx.y);
+  const size_t fn = fn_s ? fn_s : static_cast<size_t>(fw) * fh;
+  const size_t cn = cn_s ? cn_s : static_cast<size_t>(cw) * ((fh + 1) / 2);
   const int fy0 = 2 * cy;
   const bool two_y = fy0 + 1 < fh;
   const bool all = averaging != 0;

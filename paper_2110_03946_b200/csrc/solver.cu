@@ -206,6 +206,11 @@ struct si_ctx {
   // striped solves (stripes.cuh): per-level storage rows, comm scratch
   std::vector<LevelBuf> stripe_levels;
   DevBuf stripe_send, stripe_recv, stripe_in_f, stripe_in_mask, stripe_out;
+  DevBuf stripe_state;                          // StripeState per level + counter snapshots
+  void* stripe_host = nullptr;                  // mapped mirror of the StripeStates
+  void* stripe_hdev = nullptr;                  // device alias of stripe_host
+  void* stripe_log = nullptr;                   // mapped: finest-level trace rows
+  size_t stripe_log_cap = 0;
   unsigned long long* host_state = nullptr;     // mapped: LevelState[SI_MAX_LEVELS]
   unsigned long long* dev_state = nullptr;      // device alias of host_state
   // batch pipelining: a graph-mode frame's outcome lands in frame_host[slot]
@@ -389,7 +394,8 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s,
 template <typename T>
 void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W, int H, int C,
                      int mode, double* out, bool known_invariant = true, int row0 = 0,
-                     int row1 = -1, int srow_lo = 0, int srow_hi = -1) {
+                     int row1 = -1, int srow_lo = 0, int srow_hi = -1,
+                     const int* skip = nullptr) {
   if (row1 < 0) row1 = H;
   if (srow_hi < 0) srow_hi = H;
   const int HS = srow_hi - srow_lo;
@@ -416,7 +422,8 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
       constexpr bool INV = decltype(inv)::value, MT = decltype(mt)::value;
       ++x.c.launch_count;
       launch_pdl(residual_sumsq_tma_kernel<T, INV, MT>, dim3(tx, gy, C), kResTmaThreads, x.s,
-                 map, mmap, mask, b, W, H, N, row0, row1, srow_lo, x.c.red_partials.as<double>());
+                 map, mmap, mask, b, W, H, N, row0, row1, srow_lo, x.c.red_partials.as<double>(),
+                 skip);
     };
     if (known_invariant) {
       if (mtma) launch(std::true_type{}, std::true_type{});
@@ -433,12 +440,12 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
     ++x.c.launch_count;
     residual_sumsq_kernel<T, true><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
         mask, u, b, W, H, N, mode, row0, row1, srow_lo, srow_hi, x.c.red_partials.as<double>(),
-        out, x.c.ticket.as<unsigned int>());
+        out, x.c.ticket.as<unsigned int>(), skip);
   } else {
     ++x.c.launch_count;
     residual_sumsq_kernel<T, false><<<dim3(gx, gy, C), kRedThreads, 0, x.s>>>(
         mask, u, b, W, H, N, mode, row0, row1, srow_lo, srow_hi, x.c.red_partials.as<double>(),
-        out, x.c.ticket.as<unsigned int>());
+        out, x.c.ticket.as<unsigned int>(), skip);
   }
   CK(cudaGetLastError());
 }
@@ -580,6 +587,27 @@ struct LocalCfg {
 
 template <typename T, int NW>
 void launch_sweep_nw(Ctx& x, const SweepArgs<T>& a, int nblocks, int C) {
+  if (a.skip != nullptr) {  // stripes (speculative iterations): the 2-warp sweeps only
+    if constexpr (NW == 2) {
+      ++x.c.launch_count;
+      const dim3 grid(nblocks, C);
+      const bool full = a.ax.block == kMaxBlock;
+      if constexpr (sizeof(T) == 8) {
+        if (x.c.local_fp32) {
+          if (full) oras_sweep_kernel<T, 2, true, float, true><<<grid, 64, 0, x.s>>>(a);
+          else oras_sweep_kernel<T, 2, false, float, true><<<grid, 64, 0, x.s>>>(a);
+          CK(cudaGetLastError());
+          return;
+        }
+      }
+      if (full) oras_sweep_kernel<T, 2, true, T, true><<<grid, 64, 0, x.s>>>(a);
+      else oras_sweep_kernel<T, 2, false, T, true><<<grid, 64, 0, x.s>>>(a);
+      CK(cudaGetLastError());
+      return;
+    } else {
+      fail(SI_ERR_RUNTIME, "skippable sweeps need 2 warps per CTA");
+    }
+  }
   if constexpr (sizeof(T) == 8) {
     if (x.c.local_fp32) {  // MIXED: double image / outer iteration, float local CG
       ++x.c.launch_count;
@@ -605,9 +633,10 @@ template <typename T>
 void launch_sweep(Ctx& x, const uint8_t* mask, const T* b, const T* u_old, T* u_new, int W, int H,
                   int C, int block, int overlap, int flavour, double alpha, const LocalCfg& lc,
                   bool known_invariant, unsigned long long* counters, int by0 = 0, int by1 = -1,
-                  int srow_lo = 0, int srow_hi = -1) {
+                  int srow_lo = 0, int srow_hi = -1, const int* skip = nullptr) {
   if (srow_hi < 0) srow_hi = H;
   SweepArgs<T> a{};
+  a.skip = skip;
   a.srow_lo = srow_lo;
   a.srow_hi = srow_hi;
   a.mask = mask;
@@ -2226,6 +2255,8 @@ void si_destroy(si_ctx* c) {
   for (cudaStream_t cs : c->cap_stream)
     if (cs) cudaStreamDestroy(cs);
   if (c->host_state) cudaFreeHost(c->host_state);
+  if (c->stripe_host) cudaFreeHost(c->stripe_host);
+  if (c->stripe_log) cudaFreeHost(c->stripe_log);
   for (int k = 0; k < 2; ++k) {
     if (c->frame_host[k]) cudaFreeHost(c->frame_host[k]);
     if (c->frame_done[k]) cudaEventDestroy(c->frame_done[k]);
@@ -2235,7 +2266,7 @@ void si_destroy(si_ctx* c) {
   for (auto& l : c->stripe_levels)
     for (DevBuf* b : {&l.mask, &l.b, &l.u0, &l.u1}) b->release();
   for (DevBuf* b : {&c->stripe_send, &c->stripe_recv, &c->stripe_in_f, &c->stripe_in_mask,
-                    &c->stripe_out})
+                    &c->stripe_out, &c->stripe_state})
     b->release();
   for (void* b : c->pack_buf)
     if (b) cudaFreeHost(b);
@@ -2991,6 +3022,22 @@ si_status si_stripe_comm_init_local(si_ctx* const* ctxs, int world, si_stripe_co
 }
 
 void si_stripe_comm_destroy(si_stripe_comm* comm) { delete comm; }
+
+si_status si_stripe_comm_set_speculation(si_stripe_comm* comm, int enabled) {
+  return guard([&] {
+    check_arg(comm != nullptr, "null argument");
+    comm->speculate = enabled ? 1 : 0;
+  });
+}
+
+si_status si_stripe_comm_counters(const si_stripe_comm* comm, long long* out) {
+  return guard([&] {
+    check_arg(comm && out, "null argument");
+    out[0] = comm->solves;
+    out[1] = comm->speculative;
+    out[2] = comm->resumes;
+  });
+}
 
 si_status si_run_method_striped(si_ctx* ctx, si_stripe_comm* comm, int method, const double* f,
                                 const uint8_t* mask, int w, int h, int c, const si_options* opt,

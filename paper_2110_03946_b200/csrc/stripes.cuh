@@ -171,6 +171,17 @@ struct RowBuf {
 struct si_stripe_comm {
   int world = 1, rank = 0;
   int device = 0;
+  // Level iteration counts of the last solve per (shape, options): the
+  // number of outer iterations issued without a host round trip next time.
+  // Every rank of a group makes the same calls, so every rank holds the same
+  // history and issues the same collectives.
+  struct Hist {
+    std::vector<uint64_t> key;
+    std::vector<int> iters;
+  };
+  std::vector<Hist> history;
+  int speculate = 1;                 // 0: one host round trip per decision
+  long long solves = 0, speculative = 0, resumes = 0;  // si_stripe_comm_counters
   virtual ~si_stripe_comm() = default;
   // n doubles from every rank -> recv[rank * n + i] on every rank (device)
   virtual void allgather(const double* d_send, double* d_recv, int n, cudaStream_t s) = 0;
@@ -390,18 +401,156 @@ void plan_xfers(const StripeLevel& S, int rank, const std::vector<std::vector<Sp
   }
 }
 
-__global__ void stripe_decide_copy_kernel(const double* __restrict__ src, double* dst, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+// Outcome of one level's outer iterations, decided on the device.
+struct StripeState {
+  double r0, final_rel;
+  int outer;       // sweeps executed on this level
+  int iterations;  // outer count at the last decision (report.iterations)
+  int converged;
+  int stop;        // final: the level's later sweeps and residuals skip
+  int fix_base;    // sweeps at the last parity fixup: the iterate is in u[(swept - fix_base) & 1]
+  int known_ok;    // build_rhs: some known pixel (every decision carries the count)
+};
+
+// One stop decision from the gathered G x NG rows [sums C | r0 C | known |
+// failures | CG iterations | -], in the host path's arithmetic: per-channel
+// sums in rank order from 0.0, joint_norm, rel = joint / r0 (schwarz.hpp:
+// 288-320).  first: also r0 (from the sums at r0_off: C, or 0 when u0 = b
+// bitwise) and a fresh level.  A stopped level keeps its
+// outcome (the speculative iterations after it are no-ops).  The gathered
+// rows and the state are mirrored into mapped host memory; on the finest
+// level each decision is also a trace row (log, mapped, indexed by outer).
+struct StripeTraceRow {
+  unsigned long long t;  // %globaltimer (ns) at the decision
+  double rel;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
-// known pixels among n mask bytes -> *out (a double; exact below 2^53)
-__global__ void count_known_rows_kernel(const uint8_t* __restrict__ mask, size_t n, double* out) {
-  unsigned long long cnt = 0;
+__global__ void stripe_clock_kernel(unsigned long long* out) {
+  if (threadIdx.x == 0) *out = global_ns();
+}
+
+__global__ void stripe_decide_kernel(const double* __restrict__ g, int G, int C, double tol,
+                                     int max_outer, StripeState* st, StripeState* mirror,
+                                     double* host_copy, int first, int r0_off,
+                                     StripeTraceRow* log, const unsigned long long* cnt) {
+  const int NG = 2 * C + 4;
+  for (int i = threadIdx.x; i < NG * G; i += blockDim.x) host_copy[i] = g[i];
+  if (threadIdx.x != 0) return;
+  if (cnt != nullptr) {  // one rank: the local counters directly (no stats pass)
+    host_copy[2 * C + 1] = static_cast<double>(cnt[0]);
+    host_copy[2 * C + 2] = static_cast<double>(cnt[1]);
+  }
+  StripeState s = *st;
+  auto joint = [&](int off) {
+    double j = 0.0;
+    for (int k = 0; k < C; ++k) {
+      double sum = 0.0;
+      for (int r = 0; r < G; ++r) sum += g[r * NG + off + k];
+      const double nrm = sqrt(sum);
+      j = fma(nrm, nrm, j);
+    }
+    return sqrt(j);
+  };
+  if (first) {
+    s.r0 = joint(r0_off);
+    s.outer = s.iterations = s.converged = s.stop = s.fix_base = 0;
+    double known = 0.0;
+    for (int r = 0; r < G; ++r) known += g[r * NG + 2 * C];
+    s.known_ok = known > 0.0;
+  }
+  if (!s.stop) {
+    const double rel = s.r0 > 0.0 ? joint(0) / s.r0 : 0.0;
+    s.iterations = s.outer;
+    s.final_rel = rel;
+    if (log != nullptr) log[s.outer] = {global_ns(), rel};  // finest level: the trace row
+    if (rel <= tol) {
+      s.converged = 1;
+      s.stop = 1;
+    } else if (s.outer >= max_outer) {
+      s.stop = 1;
+    } else {
+      s.outer += 1;  // the next sweep runs
+    }
+  }
+  *st = s;
+  *mirror = s;
+}
+
+// Sweeps a level has executed: a live level's `outer` already counts the
+// next one (the decision to continue increments it).
+__device__ __forceinline__ int stripe_swept(const StripeState* st) {
+  return st->stop ? st->outer : st->outer - 1;
+}
+
+// After a level: its iterate -> u0 when it sits in u1.
+template <typename T>
+__global__ void stripe_fixup_kernel(const StripeState* st, const T* __restrict__ u1,
+                                    T* __restrict__ u0, size_t n) {
+  if (((stripe_swept(st) - st->fix_base) & 1) == 0) return;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    cnt += mask[i] != 0;
-  cnt = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(cnt));
+    u0[i] = u1[i];
+}
+
+// The finest level's own rows -> the compact output, from whichever buffer
+// holds the iterate.
+template <typename T>
+__global__ void stripe_output_kernel(const StripeState* st, const T* __restrict__ u0,
+                                     const T* __restrict__ u1, double* __restrict__ out, size_t n) {
+  const T* __restrict__ src = ((stripe_swept(st) - st->fix_base) & 1) ? u1 : u0;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = static_cast<double>(src[i]);
+}
+
+// A level resumed after its fixup: the iterate is in u0 again.
+__global__ void stripe_rebase_kernel(StripeState* st) {
+  if (threadIdx.x == 0) st->fix_base = stripe_swept(st);
+}
+
+// known pixels among n mask bytes -> *out (a double; exact below 2^53):
+// 16-byte loads over the aligned body, bytes at the ends
+__global__ void count_known_rows_kernel(const uint8_t* __restrict__ mask, size_t n, double* out) {
+  const size_t lead = (16 - (reinterpret_cast<uintptr_t>(mask) & 15)) & 15;
+  const size_t head = n < lead ? n : lead;
+  const size_t body = (n - head) / 16;
+  const uint4* __restrict__ v = reinterpret_cast<const uint4*>(mask + head);
+  const size_t tid = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  auto nz = [](unsigned w) {  // nonzero bytes of a word
+    const unsigned t = ((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w;
+    return __popc(t & 0x80808080u);
+  };
+  unsigned cnt = 0;
+  for (size_t i = tid; i < body; i += stride) {
+    const uint4 q = __ldg(v + i);
+    cnt += nz(q.x) + nz(q.y) + nz(q.z) + nz(q.w);
+  }
+  const size_t tail0 = head + body * 16;
+  if (tid < head) cnt += mask[tid] != 0;
+  if (tid < n - tail0) cnt += mask[tail0 + tid] != 0;
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, static_cast<double>(cnt));
+}
+
+// K5 for rows [lo, hi) of a stripe store (pre-offset pointers, planes
+// `plane` apart): the rows the fused K5+K3 pass does not cover
+template <typename T>
+__global__ void ingest_rows_kernel(const double* __restrict__ f, const uint8_t* __restrict__ mask,
+                                   int w, int lo, int hi, int C, size_t plane, T* __restrict__ b) {
+  const size_t n = static_cast<size_t>(hi - lo) * w, base = static_cast<size_t>(lo) * w;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const bool kn = mask[base + i] != 0;
+    for (int c = 0; c < C; ++c)
+      b[c * plane + base + i] = kn ? static_cast<T>(f[c * plane + base + i]) : T(0);
+  }
 }
 
 __global__ void stripe_stats_kernel(const unsigned long long* cnt, double solves, double* out) {
@@ -482,8 +631,42 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
   double* d_recv = c.stripe_recv.as<double>();
   prepare_red(x, ((2 * C + 4) * G + 3) / 4 + 1);  // mapped slots for the G x (2C+4) gathers
 
-  // ---- K5 ingest of the store rows, K3 restriction store -> store
-  {
+  // ---- K5 ingest of the store rows, K3 restriction store -> store; K5 and
+  // the first K3 in one pass over the coarse store rows (as the direct path)
+  // plus plain K5 for fine store rows outside twice them
+  int restrict_from = 1;
+  if (depth > 1 && !ingest_fusion_disabled() && !V[1].st.empty()) {
+    const StripeLevel& F = P.L[0];
+    const Span cs = V[1].st, fs = V[0].st;
+    const Span pair{2 * cs.lo, std::min(2 * cs.hi, F.h)};
+    Timed t(x, K_INGEST, static_cast<double>(V[0].rows_n) * (C * (8.0 + sizeof(T)) + 1.0) +
+                             static_cast<double>(V[1].rows_n) * (C * sizeof(T) + 1));
+    const ptrdiff_t off0 = static_cast<ptrdiff_t>(fs.lo) * F.w;
+    const double* f_pre = d_f - off0;
+    const dim3 grid((P.L[1].w + 128 * kIrCells - 1) / (128 * kIrCells), cs.hi - cs.lo);
+    ++c.launch_count;
+    auto fused = [&](auto vec) {
+      ingest_restrict_kernel<T, decltype(vec)::value><<<grid, 128, 0, x.s>>>(
+          f_pre, V[0].mask, F.w, F.h, C, o.averaging, V[0].b, V[1].mask, V[1].b,
+          c.counters.as<unsigned long long>() + 2, cs.lo, V[0].rows_n, V[1].rows_n);
+    };
+    // the vector path moves cell pairs: even width (every offset even) and
+    // 16-byte aligned f / 2-byte aligned mask
+    if (F.w % 2 == 0 && (reinterpret_cast<uintptr_t>(d_f) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(d_mask) & 1) == 0)
+      fused(std::true_type{});
+    else fused(std::false_type{});
+    CK(cudaGetLastError());
+    std::vector<Span> rest;
+    span_minus(fs, pair, rest);
+    for (const Span& r : rest) {
+      ++c.launch_count;
+      ingest_rows_kernel<T><<<grid_for(static_cast<size_t>(r.hi - r.lo) * F.w, 256, 148 * 4), 256,
+                              0, x.s>>>(f_pre, V[0].mask, F.w, r.lo, r.hi, C, V[0].rows_n, V[0].b);
+      CK(cudaGetLastError());
+    }
+    restrict_from = 2;
+  } else {
     const size_t n0 = V[0].rows_n;
     if (n0) {
       Timed t(x, K_INGEST, static_cast<double>(n0) * (C * (8.0 + sizeof(T)) + 1.0));
@@ -493,7 +676,7 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
       CK(cudaGetLastError());
     }
   }
-  for (int l = 1; l < depth; ++l) {
+  for (int l = restrict_from; l < depth; ++l) {
     const StripeLevel& F = P.L[l - 1];
     const Span cs = V[l].st;
     if (cs.empty()) continue;
@@ -501,22 +684,64 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     launch_restrict<T>(x, V[l - 1].mask, V[l - 1].b, F.w, F.h, C, o.averaging, V[l].mask, V[l].b,
                        cs.lo, cs.hi, V[l - 1].rows_n, V[l].rows_n);
   }
-  // One all-gather per outer iteration carries everything the host needs,
-  // per rank: [sums C | r0 C | known | failures | CG iterations | solves].
+  // One all-gather per outer iteration carries every rank's
+  // [sums C | r0 C | known | failures | CG iterations | -]; the stop decision
+  // is taken on the device from it (stripe_decide_kernel), identically on
+  // every rank, so the host issues iterations without waiting for them.
   const int NG = 2 * C + 4;
-  auto gather = [&](double solves) {
+  c.stripe_state.ensure(sizeof(StripeState) * SI_MAX_LEVELS +
+                        sizeof(unsigned long long) * 2 * SI_MAX_LEVELS);
+  StripeState* d_st = c.stripe_state.as<StripeState>();
+  unsigned long long* d_snap = reinterpret_cast<unsigned long long*>(d_st + SI_MAX_LEVELS);
+  if (!c.stripe_host) {
+    CK(cudaHostAlloc(&c.stripe_host, sizeof(StripeState) * SI_MAX_LEVELS, cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(&c.stripe_hdev, c.stripe_host, 0));
+  }
+  const StripeState* h_st = static_cast<const StripeState*>(c.stripe_host);
+  StripeState* m_st = static_cast<StripeState*>(c.stripe_hdev);
+  unsigned long long* d_cnt = c.counters.as<unsigned long long>();
+  // finest-level trace rows, written by the decisions (mapped host memory):
+  // [0] = the solve's start stamp, then one row per outer iteration
+  StripeTraceRow* log_dev = nullptr;
+  const StripeTraceRow* log_host = nullptr;
+  if (tr.fn) {
+    const size_t rows = static_cast<size_t>(std::max(o.max_outer_iterations, 0)) + 2;
+    if (c.stripe_log_cap < rows) {
+      if (c.stripe_log) {
+        CK(cudaStreamSynchronize(x.s));
+        CK(cudaFreeHost(c.stripe_log));
+        c.stripe_log = nullptr;
+      }
+      CK(cudaHostAlloc(&c.stripe_log, sizeof(StripeTraceRow) * rows, cudaHostAllocMapped));
+      c.stripe_log_cap = rows;
+    }
+    void* d = nullptr;
+    CK(cudaHostGetDevicePointer(&d, c.stripe_log, 0));
+    log_dev = static_cast<StripeTraceRow*>(d);
+    log_host = static_cast<const StripeTraceRow*>(c.stripe_log);
     ++c.launch_count;
-    stripe_stats_kernel<<<1, 32, 0, x.s>>>(c.counters.as<unsigned long long>(), solves,
-                                           d_send + 2 * C + 1);
+    stripe_clock_kernel<<<1, 32, 0, x.s>>>(&log_dev[0].t);
     CK(cudaGetLastError());
-    if (G > 1) comm.allgather(d_send, d_recv, NG, x.s);  // one rank: nothing to gather
+  }
+  auto gather = [&](int level, bool first, bool r0_same = false) {
+    if (G > 1) {  // one rank: nothing to gather, the decision reads the counters
+      ++c.launch_count;
+      stripe_stats_kernel<<<1, 32, 0, x.s>>>(d_cnt, 0.0, d_send + 2 * C + 1);
+      CK(cudaGetLastError());
+      comm.allgather(d_send, d_recv, NG, x.s);
+    }
     ++c.launch_count;
-    stripe_decide_copy_kernel<<<1, 256, 0, x.s>>>(G > 1 ? d_recv : d_send, c.dev_red, NG * G);
+    stripe_decide_kernel<<<1, 128, 0, x.s>>>(G > 1 ? d_recv : d_send, G, C,
+                                             level == 0 ? o.tolerance : o.coarse_tolerance,
+                                             o.max_outer_iterations, d_st + level, m_st + level,
+                                             c.dev_red, first ? 1 : 0, r0_same ? 0 : C,
+                                             level == 0 && log_dev ? log_dev + 1 : nullptr,
+                                             G > 1 ? nullptr : d_cnt);
     CK(cudaGetLastError());
-    sync(x);
   };
   // known count of the rows this rank owns at level 0 (own rows tile the
-  // image), checked at the first gather (build_rhs, operators.hpp:83)
+  // image): every gather carries it, the first decision checks it
+  // (build_rhs, operators.hpp:83)
   CK(cudaMemsetAsync(d_send, 0, sizeof(double) * NG, x.s));
   {
     const StripeLevel& S = P.L[0];
@@ -531,22 +756,64 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     }
   }
   bool known_checked = false;
+  auto check_known = [&](const StripeState& st) {
+    if (known_checked) return;
+    check_arg(st.known_ok != 0, "build_rhs: mask has no known pixels");
+    known_checked = true;
+  };
 
   bool local_checked = false;  // cg_solve's config check before the first sweep (cg.hpp:75-80)
   if (flavour == SI_FLAVOUR_ORAS)
     check_arg(std::isfinite(o.alpha), "run_schwarz_level: alpha must be finite");
   const LocalCfg lc{o.local_tolerance, o.local_max_iterations, o.local_check_interval};
-  unsigned long long* d_cnt = c.counters.as<unsigned long long>();
   std::vector<RowXfer> sends, recvs;
   std::vector<std::vector<Span>> want(G);
+  struct Run {
+    int cur = 0;  // host view of the ping-pong (issued sweeps)
+    std::vector<RowXfer> hs, hr;  // halo plan
+  };
+  std::vector<Run> R(depth);
 
-  NvtxRange nv_solve("striped multilevel_solve");
-  for (int level = depth - 1; level >= 0; --level) {
-    NvtxRange nv_level("stripe level %d", level);
+  // Speculation: the iteration counts of the last solve with this key (same
+  // on every rank) are issued without a host round trip; a level that has
+  // not stopped by then is found at the end and resumed, and the finer
+  // levels after it are redone (results and counts identical to the
+  // synchronous loop).  No history, or local options the sweep would
+  // reject: one decision per host round trip.
+  std::vector<uint64_t> key = {static_cast<uint64_t>(P.L[0].w), static_cast<uint64_t>(P.L[0].h),
+                               static_cast<uint64_t>(C), static_cast<uint64_t>(flavour),
+                               sizeof(T), static_cast<uint64_t>(c.local_fp32),
+                               static_cast<uint64_t>(depth)};
+  {
+    auto bits = [&](double v) {
+      uint64_t u;
+      std::memcpy(&u, &v, 8);
+      key.push_back(u);
+    };
+    bits(o.tolerance);
+    bits(o.coarse_tolerance);
+    bits(o.alpha);
+    bits(o.local_tolerance);
+    for (int v : {o.block_size, o.overlap, o.averaging, o.local_max_iterations,
+                  o.local_check_interval, o.max_outer_iterations, o.normalizer})
+      key.push_back(static_cast<uint64_t>(static_cast<int64_t>(v)));
+  }
+  std::vector<int> pred(depth, -1);  // -1: synchronous
+  const bool local_ok = o.local_tolerance > 0.0 && o.local_max_iterations >= 0 &&
+                        o.local_check_interval >= 1;
+  // (the skippable sweeps are the 2-warp ones; K2g checks at run time).
+  // Trace rows come from the device log after the solve.
+  bool nw_ok = true;
+  for (int l = 0; l < depth; ++l)
+    if (P.L[l].block <= kMaxBlock) nw_ok &= (sizeof(T) == 8 ? c.sweep_nw64 : c.sweep_nw32) == 2;
+  if (local_ok && nw_ok && comm.speculate)
+    for (const auto& h : comm.history)
+      if (h.key == key && static_cast<int>(h.iters.size()) == depth) pred = h.iters;
+
+  auto begin_level = [&](int level) {
     const StripeLevel& S = P.L[level];
     View& v = V[level];
     const Span own = S.own[me];
-    int cur = 0;
     if (level == depth - 1 && v.rows_n) {
       // canonical start u0 = b (multilevel.hpp:267-273)
       ++c.launch_count;
@@ -554,116 +821,200 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
                  static_cast<const T*>(v.base_b), v.base_u[0], v.rows_n * C);
       CK(cudaGetLastError());
     }
-    const bool finest = level == 0;
-    const double tol = finest ? o.tolerance : o.coarse_tolerance;
     // halo want: window rows outside my own
     for (int g = 0; g < G; ++g) {
       want[g].clear();
       span_minus(S.win[g], S.own[g], want[g]);
     }
-    plan_xfers(S, me, want, sends, recvs);
-    const std::vector<RowXfer> halo_sends = sends, halo_recvs = recvs;
-    double r0 = 0.0;
-    bool r0_pending = true;
-    const Axis ax = Axis::make(S.w, S.block, S.overlap);
-    LevelOutcome oc;
-    for (int outer = 0;; ++outer) {
-      // residual of my own rows (+ r0 with u = b the first time)
-      if (own.empty()) {
-        CK(cudaMemsetAsync(d_send, 0, sizeof(double) * 2 * C, x.s));
-      } else if (r0_pending && o.normalizer != 1) {  // u0 and r0 in one pass
-        launch_residual_pair<T>(x, v.mask, v.u[cur], v.b, S.w, S.h, C, d_send, own.lo, own.hi,
-                                v.st.lo, v.st.hi);
-      } else {
-        launch_residual<T>(x, v.mask, v.u[cur], v.b, S.w, S.h, C, 0, d_send, true, own.lo, own.hi,
-                           v.st.lo, v.st.hi);
-        if (r0_pending)
-          launch_residual<T>(x, v.mask, v.b, v.b, S.w, S.h, C, 1, d_send + C, true, own.lo,
-                             own.hi, v.st.lo, v.st.hi);
-      }
-      gather(static_cast<double>(rep->local_solves));
-      if (!known_checked) {
-        double known = 0.0;
-        for (int g = 0; g < G; ++g) known += c.host_red[g * NG + 2 * C];
-        check_arg(known > 0.0, "build_rhs: mask has no known pixels");
-        known_checked = true;
-      }
-      // fixed rank order: identical sums (and decisions) on every rank
-      std::vector<double> sums(C, 0.0), r0s(C, 0.0);
-      for (int g = 0; g < G; ++g)
-        for (int k = 0; k < C; ++k) {
-          sums[k] += c.host_red[g * NG + k];
-          r0s[k] += c.host_red[g * NG + C + k];
-        }
-      if (r0_pending) {
-        r0 = joint_norm(r0s.data(), C);
-        r0_pending = false;
-      }
-      const double rel = r0 > 0.0 ? joint_norm(sums.data(), C) / r0 : 0.0;
-      if (finest && tr.fn) tr.fn(outer, ms_since(tr.t0), rel, std::numeric_limits<double>::quiet_NaN(), tr.user);
-      oc.iterations = outer;
-      oc.final_rel = rel;
-      if (rel <= tol) {
-        oc.converged = true;
-        break;
-      }
-      if (outer >= o.max_outer_iterations) break;
-      NvtxRange nv_sweep("stripe sweep + halo");
-      if (!local_checked) {  // every rank takes the same decisions: all fail alike
-        validate_local(o);
-        local_checked = true;
-      }
-      if (S.k1 > S.k0)
-        launch_sweep<T>(x, v.mask, v.b, v.u[cur], v.u[cur ^ 1], S.w, S.h, C, S.block, S.overlap,
-                        flavour, o.alpha, lc, true, d_cnt, S.k0, S.k1, v.st.lo, v.st.hi);
-      cur ^= 1;
-      rep->local_solves += static_cast<long long>(ax.count) * (S.k1 - S.k0) * C;
-      comm.exchange(halo_sends, halo_recvs, row_buf<T>(v.base_u[cur], S.w, v.st, C), x.s);
-    }
-    rep->level_iterations[level] = oc.iterations;
-    rep->level_final_rel[level] = oc.final_rel;
-    rep->level_converged[level] = oc.converged;
-    if (finest) {
-      rep->iterations = oc.iterations;
-      rep->final_relative_residual = oc.final_rel;
-      rep->converged = oc.converged;
-      if (!own.empty() && static_cast<const void*>(v.base_u[cur]) != static_cast<const void*>(d_out)) {
-        const size_t rows_px = static_cast<size_t>(own.hi - own.lo) * S.w;
-        Timed t(x, K_INGEST, static_cast<double>(rows_px) * C * (8.0 + sizeof(T)));
-        for (int k = 0; k < C; ++k) {  // own rows of each plane -> compact output
-          ++c.launch_count;
-          convert_kernel<T, double><<<grid_for(rows_px, 256, 148 * 16), 256, 0, x.s>>>(
-              v.u[cur] + static_cast<size_t>(k) * v.rows_n + static_cast<size_t>(own.lo) * S.w,
-              d_out + static_cast<size_t>(k) * rows_px, rows_px);
-          CK(cudaGetLastError());
-        }
-      }
+    plan_xfers(S, me, want, R[level].hs, R[level].hr);
+    R[level].cur = 0;
+    // residual of my own rows and r0 with u = b; on the coarsest level u0
+    // is a bitwise copy of b, so one pass gives both (R0Mode kR0Same)
+    const bool same = level == depth - 1 && o.normalizer != 1;
+    if (own.empty()) {
+      CK(cudaMemsetAsync(d_send, 0, sizeof(double) * 2 * C, x.s));
+    } else if (same) {
+      launch_residual<T>(x, v.mask, v.u[0], v.b, S.w, S.h, C, 0, d_send, true, own.lo, own.hi,
+                         v.st.lo, v.st.hi);
+    } else if (o.normalizer != 1) {  // u0 and r0 in one pass
+      launch_residual_pair<T>(x, v.mask, v.u[0], v.b, S.w, S.h, C, d_send, own.lo, own.hi,
+                              v.st.lo, v.st.hi);
     } else {
-      // rows my prolongation reads but my window does not hold: from owners
-      for (int g = 0; g < G; ++g) {
-        want[g].clear();
-        span_minus(S.need[g], S.win[g], want[g]);
-      }
-      plan_xfers(S, me, want, sends, recvs);
-      comm.exchange(sends, recvs, row_buf<T>(v.base_u[cur], S.w, v.st, C), x.s);
-      // K4 onto the finer level's window rows
-      const StripeLevel& F = P.L[level - 1];
-      View& fv = V[level - 1];
-      const Span fw = F.win[me];
-      if (!fw.empty()) {
-        Timed t(x, K_PROLONG, static_cast<double>(fw.hi - fw.lo) * F.w * (2.0 * C * sizeof(T) + 1.0));
-        launch_prolong<T>(x, v.u[cur], S.w, S.h, F.w, F.h, C, fv.mask, fv.b, fv.u[0], fw.lo,
-                          fw.hi, v.st.lo, v.st.hi, fv.rows_n, v.rows_n, fv.st.lo);
-      }
+      launch_residual<T>(x, v.mask, v.u[0], v.b, S.w, S.h, C, 0, d_send, true, own.lo, own.hi,
+                         v.st.lo, v.st.hi);
+      launch_residual<T>(x, v.mask, v.b, v.b, S.w, S.h, C, 1, d_send + C, true, own.lo, own.hi,
+                         v.st.lo, v.st.hi);
     }
+    gather(level, true, same);
+  };
+  // one outer iteration, skipped on the device once the level has stopped:
+  // sweep, halo exchange (an exchange after a skipped sweep copies rows
+  // equal to the ones it overwrites), residual, gather + decision
+  auto iterate = [&](int level) {
+    NvtxRange nv_sweep("stripe sweep + halo");
+    const StripeLevel& S = P.L[level];
+    View& v = V[level];
+    const Span own = S.own[me];
+    // skippable launches only while speculating (else the level is known live)
+    const int* skip = pred[level] >= 0 ? &d_st[level].stop : nullptr;
+    if (!local_checked) {  // every rank takes the same decisions: all fail alike
+      validate_local(o);
+      local_checked = true;
+    }
+    int& cur = R[level].cur;
+    if (S.k1 > S.k0)
+      launch_sweep<T>(x, v.mask, v.b, v.u[cur], v.u[cur ^ 1], S.w, S.h, C, S.block, S.overlap,
+                      flavour, o.alpha, lc, true, d_cnt, S.k0, S.k1, v.st.lo, v.st.hi, skip);
+    cur ^= 1;
+    comm.exchange(R[level].hs, R[level].hr, row_buf<T>(v.base_u[cur], S.w, v.st, C), x.s);
+    if (own.empty())
+      CK(cudaMemsetAsync(d_send, 0, sizeof(double) * 2 * C, x.s));
+    else
+      launch_residual<T>(x, v.mask, v.u[cur], v.b, S.w, S.h, C, 0, d_send, true, own.lo, own.hi,
+                         v.st.lo, v.st.hi, skip);
+    gather(level, false);
+  };
+  auto end_level = [&](int level, bool snapshot) {
+    const StripeLevel& S = P.L[level];
+    View& v = V[level];
+    const Span own = S.own[me];
+    if (level == 0) {
+      if (own.empty()) return;
+      if (static_cast<const void*>(v.base_u[0]) == static_cast<const void*>(d_out)) {
+        ++c.launch_count;
+        stripe_fixup_kernel<T><<<grid_for(v.rows_n * C, 256, 148 * 8), 256, 0, x.s>>>(
+            d_st, v.base_u[1], v.base_u[0], v.rows_n * C);
+        CK(cudaGetLastError());
+        return;
+      }
+      const size_t rows_px = static_cast<size_t>(own.hi - own.lo) * S.w;
+      Timed t(x, K_INGEST, static_cast<double>(rows_px) * C * (8.0 + sizeof(T)));
+      for (int k = 0; k < C; ++k) {  // own rows of each plane -> compact output
+        const size_t off = static_cast<size_t>(k) * v.rows_n + static_cast<size_t>(own.lo) * S.w;
+        ++c.launch_count;
+        stripe_output_kernel<T><<<grid_for(rows_px, 256, 148 * 16), 256, 0, x.s>>>(
+            d_st, v.u[0] + off, v.u[1] + off, d_out + static_cast<size_t>(k) * rows_px, rows_px);
+        CK(cudaGetLastError());
+      }
+      return;
+    }
+    if (v.rows_n) {
+      ++c.launch_count;
+      stripe_fixup_kernel<T><<<grid_for(v.rows_n * C, 256, 148 * 8), 256, 0, x.s>>>(
+          d_st + level, v.base_u[1], v.base_u[0], v.rows_n * C);
+      CK(cudaGetLastError());
+    }
+    if (snapshot)  // the counters as of this level's end: restored if a finer level is redone
+      CK(cudaMemcpyAsync(d_snap + 2 * level, d_cnt, 2 * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToDevice, x.s));
+    // rows my prolongation reads but my window does not hold: from owners
+    for (int g = 0; g < G; ++g) {
+      want[g].clear();
+      span_minus(S.need[g], S.win[g], want[g]);
+    }
+    plan_xfers(S, me, want, sends, recvs);
+    comm.exchange(sends, recvs, row_buf<T>(v.base_u[0], S.w, v.st, C), x.s);
+    // K4 onto the finer level's window rows
+    const StripeLevel& F = P.L[level - 1];
+    View& fv = V[level - 1];
+    const Span fw = F.win[me];
+    if (!fw.empty()) {
+      Timed t(x, K_PROLONG, static_cast<double>(fw.hi - fw.lo) * F.w * (2.0 * C * sizeof(T) + 1.0));
+      launch_prolong<T>(x, v.u[0], S.w, S.h, F.w, F.h, C, fv.mask, fv.b, fv.u[0], fw.lo, fw.hi,
+                        v.st.lo, v.st.hi, fv.rows_n, v.rows_n, fv.st.lo);
+    }
+  };
+  // synchronous: one host round trip per decision
+  auto run_sync = [&](int level) {
+    for (;;) {
+      sync(x);
+      const StripeState st = h_st[level];
+      check_known(st);
+      if (st.stop) return;
+      iterate(level);
+    }
+  };
+  auto run_level = [&](int level) {
+    NvtxRange nv_level("stripe level %d", level);
+    begin_level(level);
+    if (pred[level] < 0) {
+      run_sync(level);
+    } else {
+      for (int k = 0; k < pred[level] && k < o.max_outer_iterations; ++k) iterate(level);
+    }
+    end_level(level, pred[level] >= 0);
+  };
+
+  NvtxRange nv_solve("striped multilevel_solve");
+  ++comm.solves;
+  if (pred[0] >= 0) ++comm.speculative;
+  for (int level = depth - 1; level >= 0; --level) run_level(level);
+  sync(x);
+  check_known(h_st[depth - 1]);
+  for (;;) {  // levels that needed more iterations than were issued
+    int bad = -1;
+    for (int l = depth - 1; l >= 0 && bad < 0; --l)
+      if (!h_st[l].stop) bad = l;
+    if (bad < 0) break;
+    ++comm.resumes;
+    if (bad > 0)
+      CK(cudaMemcpyAsync(d_cnt, d_snap + 2 * bad, 2 * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToDevice, x.s));
+    if (bad == 0 && V[0].rows_n) {  // the finest level's end wrote the output only
+      ++c.launch_count;
+      stripe_fixup_kernel<T><<<grid_for(V[0].rows_n * C, 256, 148 * 8), 256, 0, x.s>>>(
+          d_st, V[0].base_u[1], V[0].base_u[0], V[0].rows_n * C);
+      CK(cudaGetLastError());
+    }
+    ++c.launch_count;
+    stripe_rebase_kernel<<<1, 32, 0, x.s>>>(d_st + bad);
+    CK(cudaGetLastError());
+    R[bad].cur = 0;
+    pred[bad] = -1;
+    {
+      NvtxRange nv_level("stripe level %d (resumed)", bad);
+      iterate(bad);
+      run_sync(bad);
+      end_level(bad, true);
+    }
+    for (int level = bad - 1; level >= 0; --level) run_level(level);
+    sync(x);
   }
-  // local statistics summed over ranks (the finest level's last gather came
-  // after the last sweep): failures, CG iterations, solves
+
   rep->local_failures = rep->local_cg_iterations = rep->local_solves = 0;
+  for (int l = 0; l < depth; ++l) {
+    const StripeState& st = h_st[l];
+    rep->level_iterations[l] = st.iterations;
+    rep->level_final_rel[l] = st.final_rel;
+    rep->level_converged[l] = st.converged;
+    const StripeLevel& S = P.L[l];
+    const Axis ax = Axis::make(S.w, S.block, S.overlap), ay = Axis::make(S.h, S.block, S.overlap);
+    rep->local_solves += static_cast<long long>(st.outer) * ax.count * ay.count * C;
+  }
+  if (tr.fn)  // trace rows (multilevel.hpp:252-261), stamped on the device
+    for (int i = 0; i <= h_st[0].iterations; ++i)
+      tr.fn(i, static_cast<double>(log_host[1 + i].t - log_host[0].t) * 1e-6, log_host[1 + i].rel,
+            std::numeric_limits<double>::quiet_NaN(), tr.user);
+  rep->iterations = h_st[0].iterations;
+  rep->final_relative_residual = h_st[0].final_rel;
+  rep->converged = h_st[0].converged;
+  // local statistics summed over ranks (the last gather came after the last
+  // sweep): failures, CG iterations
   for (int g = 0; g < G; ++g) {
     rep->local_failures += static_cast<long long>(c.host_red[g * NG + 2 * C + 1]);
     rep->local_cg_iterations += static_cast<long long>(c.host_red[g * NG + 2 * C + 2]);
-    rep->local_solves += static_cast<long long>(c.host_red[g * NG + 2 * C + 3]);
+  }
+  {  // remember this solve's counts for the next one with the same key
+    std::vector<int> it(depth);
+    for (int l = 0; l < depth; ++l) it[l] = h_st[l].iterations;
+    auto hit = std::find_if(comm.history.begin(), comm.history.end(),
+                            [&](const si_stripe_comm::Hist& h) { return h.key == key; });
+    if (hit != comm.history.end()) {
+      hit->iters = it;
+    } else {
+      if (comm.history.size() >= 16) comm.history.erase(comm.history.begin());
+      comm.history.push_back({key, it});
+    }
   }
   write_diagnostic(rep, depth, -1);
 }

@@ -83,6 +83,7 @@ struct SweepArgs {
   // there.  Whole-image solves: 0 and H.
   int srow_lo, srow_hi;
   T* scratch;          // K2g (blocks > 32): per-CTA CG vectors in global memory
+  const int* skip;     // stripes: nonzero = the level has stopped, the sweep does nothing
 };
 
 template <typename T>
@@ -417,7 +418,10 @@ constexpr int kSweepMinBlocks = kTmemQ<L, NW, FULL> ? SI_OCC64_QT : SweepOcc<L, 
 // compile-time positions.
 // L: the local CG's type (T, or float under double storage: the outer
 // iteration, residuals and the image stay in T).
-template <typename T, int NW, bool FULL, typename L = T>
+// SKIP (stripes): a.skip nonzero = the level has stopped, the CTA exits at
+// once.  A separate instantiation: the early exit costs the hot variant its
+// zero-spill allocation.
+template <typename T, int NW, bool FULL, typename L = T, bool SKIP = false>
 __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
     oras_sweep_kernel(const __grid_constant__ SweepArgs<T> a) {
   constexpr int R = 32 / NW;  // rows per thread
@@ -433,6 +437,9 @@ __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
   constexpr bool XT = kTmemX<L, NW, FULL>;
   constexpr bool QT = kTmemQ<L, NW, FULL>;
   constexpr uint32_t kCols = QT ? 64 : 32;
+  if constexpr (SKIP) {
+    if (*a.skip) return;  // uniform: before any barrier or TMEM
+  }
   const int bx = blockIdx.x % a.ax.count;
   const int by = a.by0 + static_cast<int>(blockIdx.x) / a.ax.count;
   const int ch = blockIdx.y;

@@ -31,6 +31,7 @@ template <typename T>
 __global__ void __launch_bounds__(kGenThreads) oras_sweep_generic_kernel(SweepArgs<T> a) {
   __shared__ T red[kGenThreads / 32];
   __shared__ int any_unk;
+  if (a.skip != nullptr && *a.skip) return;
   const int nb = a.ax.count;
   const int bx = blockIdx.x % nb, by = a.by0 + static_cast<int>(blockIdx.x) / nb;
   const int ch = blockIdx.y;

@@ -72,6 +72,19 @@ class StripeComm:
         self.rank = rank
         self.kind = kind
 
+    def set_speculation(self, enabled: bool) -> None:
+        """Issue each level's outer iterations without host round trips, as
+        many as the last solve of the same shape and options took (default
+        on; every rank of a group must agree)."""
+        _check(L.load().si_stripe_comm_set_speculation(self.handle, 1 if enabled else 0))
+
+    def counters(self) -> dict:
+        """Solves run on this communicator, how many speculated, and how many
+        levels had to be resumed."""
+        out = (C.c_longlong * 3)()
+        _check(L.load().si_stripe_comm_counters(self.handle, out))
+        return {"solves": out[0], "speculative": out[1], "resumes": out[2]}
+
     def close(self):
         if self.handle:
             L.load().si_stripe_comm_destroy(self.handle)

@@ -29,6 +29,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--forced", action="store_true")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--ranks", default="1,2,4")
+ap.add_argument("--sync", action="store_true", help="speculation off: one host round trip "
+                "per outer-iteration decision")
 a = ap.parse_args()
 W, H, C = 7680, 4320, 3
 f = si.synthetic_test_image(W, H, C, 7)
@@ -60,7 +62,8 @@ def timed(run_once, streams):
     return statistics.median(ts)
 
 
-out = {"workload": "7680x4320 RGB 2% 3 levels" + (" forced 2 sweeps" if a.forced else "")}
+out = {"workload": "7680x4320 RGB 2% 3 levels" + (" forced 2 sweeps" if a.forced else ""),
+       "speculation": not a.sync}
 solver = si.Solver(0)
 df = torch.from_numpy(f.data).cuda()
 dm = torch.from_numpy(m.known).cuda()
@@ -80,6 +83,8 @@ ref = do.cpu().numpy()
 for G in (int(g) for g in a.ranks.split(",")):
     solvers = [solver] + [si.Solver(0) for _ in range(G - 1)]
     comms = S.local_comms(solvers)
+    for cm in comms:
+        cm.set_speculation(not a.sync)
     streams = [torch.cuda.Stream() for _ in range(G)]
     plans = [S.level_plan(si.Method.MultilevelOras, W, H, C, o, G, r)[0] for r in range(G)]
     ins = [(torch.from_numpy(np.ascontiguousarray(f.data[:, p.store_lo:p.store_hi])).cuda(),
@@ -104,7 +109,8 @@ for G in (int(g) for g in a.ranks.split(",")):
     same = all(np.array_equal(ins[r][2].cpu().numpy(), ref[:, p.own_lo:p.own_hi])
                for r, p in enumerate(plans))
     out[f"G{G}"] = {"ms": ms, "ratio_to_direct": ms / out["direct_ms"], "bit_identical": same,
-                    "store_rows": [[p.store_lo, p.store_hi] for p in plans]}
+                    "store_rows": [[p.store_lo, p.store_hi] for p in plans],
+                    "comm": comms[0].counters()}
     for cm in comms:
         cm.close()
 print(json.dumps(out))

@@ -173,3 +173,139 @@ def test_empty_mask_fails_on_every_rank(solver):
     m = si.InpaintingMask(64, 64, 0)
     with pytest.raises(si.InvalidArgument, match="no known pixels"):
         S.run_method_striped_group(solvers(2), si.Method.MultilevelOras, f, m, si.RunOptions())
+
+
+# ---- device-decided iterations: speculation and its recovery -------------------
+
+def _group_persistent(solvers_, comms, method, f, m, o):
+    """One collective solve over persistent communicators (threads)."""
+    import threading
+    G = len(solvers_)
+    out = si.ImageBuffer(data=np.zeros_like(f.data))
+    res = [None] * G
+    err = [None] * G
+
+    def rank(r):
+        try:
+            res[r] = S.run_method_striped(solvers_[r], comms[r], method, f, m, o, out=out)
+        except Exception as e:  # noqa: BLE001
+            err[r] = e
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out, res
+
+
+SPEC_CASES = [
+    # w, h, c, method, options, G
+    (640, 480, 3, si.Method.MultilevelOras, dict(levels=3), 2),
+    (777, 333, 3, si.Method.MultilevelOras, dict(tolerance=1e-6), 3),
+    (512, 700, 1, si.Method.Oras, dict(tolerance=1e-5), 2),
+    (260, 190, 3, si.Method.MultilevelOras, dict(block_size=64, overlap=10), 2),  # K2g
+    (640, 360, 3, si.Method.MultilevelOras, dict(precision=si.Precision.MIXED), 4),
+    (640, 360, 3, si.Method.MultilevelOras, dict(precision=si.Precision.FP32), 2),
+    (96, 70, 2, si.Method.MultilevelOras, dict(levels=3), 8),  # ranks without rows
+]
+
+
+@pytest.mark.parametrize("case", range(len(SPEC_CASES)))
+def test_speculative_repeat_matches_single_gpu(solver, case):
+    """The second solve of the same shape/options issues every level's
+    iterations without host round trips: same image, counts and trace."""
+    w, h, c, method, kw, G = SPEC_CASES[case]
+    f = si.synthetic_test_image(w, h, c, 300 + case)
+    m = si.random_mask(w, h, 0.04, 400 + case)
+    o = si.RunOptions(**kw)
+    single = solver.run_method(method, f, m, o)
+    sv = solvers(G)
+    comms = S.local_comms(sv)
+    try:
+        for k in range(3):
+            img, res = _group_persistent(sv, comms, method, f, m, o)
+            check_same(single, img, [r.report for r in res], G)
+            for r in res:
+                assert len(r.trace.rows) == single.report.iterations + 1
+                for a, b in zip(r.trace.rows, single.trace.rows):
+                    assert a.iteration == b.iteration
+                    assert abs(a.rel_residual - b.rel_residual) <= \
+                        1e-12 * abs(b.rel_residual) + 1e-18
+                ts = [row.time_ms for row in r.trace.rows]
+                assert ts[0] >= 0 and all(b >= a for a, b in zip(ts, ts[1:]))
+        for cm in comms:
+            cnt = cm.counters()
+            assert cnt["solves"] == 3 and cnt["speculative"] == 2 and cnt["resumes"] == 0, cnt
+    finally:
+        for cm in comms:
+            cm.close()
+
+
+def test_misspeculation_resumes_and_redoes_finer_levels(solver):
+    """Frames of one shape whose level counts differ: a level that needs more
+    iterations than the previous frame took is resumed and the finer levels
+    are redone; every frame equals its single-GPU solve."""
+    w, h, c = 640, 480, 3
+    o = si.RunOptions(levels=3, tolerance=1e-4)
+    frames = [(si.synthetic_test_image(w, h, c, 500 + k), si.random_mask(w, h, d, 600 + k))
+              for k, d in enumerate([0.30, 0.02, 0.30, 0.05, 0.02])]
+    singles = [solver.run_method(si.Method.MultilevelOras, f, m, o) for f, m in frames]
+    counts = [list(s.report.level_iterations) for s in singles]
+    assert any(any(b > a for a, b in zip(counts[k], counts[k + 1]))
+               for k in range(len(counts) - 1)), counts  # some level is under-predicted
+    sv = solvers(2)
+    comms = S.local_comms(sv)
+    try:
+        for (f, m), single in zip(frames, singles):
+            img, res = _group_persistent(sv, comms, si.Method.MultilevelOras, f, m, o)
+            check_same(single, img, [r.report for r in res], 2)
+        cnt = comms[0].counters()
+        assert cnt["speculative"] == len(frames) - 1 and cnt["resumes"] >= 1, cnt
+        assert comms[1].counters() == cnt
+    finally:
+        for cm in comms:
+            cm.close()
+
+
+def test_speculation_off_matches(solver):
+    f = si.synthetic_test_image(640, 480, 3, 9)
+    m = si.random_mask(640, 480, 0.05, 10)
+    o = si.RunOptions(levels=3, tolerance=1e-5)
+    single = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    sv = solvers(2)
+    comms = S.local_comms(sv)
+    try:
+        for cm in comms:
+            cm.set_speculation(False)
+        for _ in range(2):
+            img, res = _group_persistent(sv, comms, si.Method.MultilevelOras, f, m, o)
+            check_same(single, img, [r.report for r in res], 2)
+        assert comms[0].counters()["speculative"] == 0
+    finally:
+        for cm in comms:
+            cm.close()
+
+
+@pytest.mark.parametrize("forced", [False, True])
+def test_c5_speculative_repeat(solver, forced):
+    """configs[4] (and its forced-sweep variant) solved twice over the same
+    two-rank group: the second solve speculates and stays bit-identical."""
+    f = si.synthetic_test_image(7680, 4320, 3, 7)
+    m = si.random_mask(7680, 4320, 0.02, 11)
+    o = (si.RunOptions(levels=3, tolerance=1e-12, max_outer_iterations=2) if forced
+         else si.RunOptions(levels=3))
+    single = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    sv = solvers(2)
+    comms = S.local_comms(sv)
+    try:
+        for _ in range(2):
+            img, res = _group_persistent(sv, comms, si.Method.MultilevelOras, f, m, o)
+            check_same(single, img, [r.report for r in res], 2)
+        assert comms[0].counters()["speculative"] == 1
+    finally:
+        for cm in comms:
+            cm.close()
