@@ -91,7 +91,11 @@ struct DevBuf {
     if (want <= bytes) return false;
     release();
     CK(cudaMalloc(&ptr, want));
+    // cudaMemset runs on the legacy stream, which does not order against the
+    // non-blocking solve streams: finish it before any of them can write here
+    // (else a late zero-fill can overwrite an upload or a kernel's output)
     CK(cudaMemset(ptr, 0, want));
+    CK(cudaStreamSynchronize(cudaStreamLegacy));
     bytes = want;
     return true;
   }

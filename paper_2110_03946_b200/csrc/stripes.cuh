@@ -498,15 +498,27 @@ __global__ void stripe_fixup_kernel(const StripeState* st, const T* __restrict__
     u0[i] = u1[i];
 }
 
-// The finest level's own rows -> the compact output, from whichever buffer
-// holds the iterate.
-template <typename T>
+// The finest level's own rows of every channel -> the compact output, from
+// whichever buffer holds the iterate: plane c's own rows start `skip`
+// elements into its `plane`-long storage plane.  VEC: 16-byte moves (the
+// offsets are even and the buffers 16-byte aligned).
+template <typename T, bool VEC>
 __global__ void stripe_output_kernel(const StripeState* st, const T* __restrict__ u0,
-                                     const T* __restrict__ u1, double* __restrict__ out, size_t n) {
+                                     const T* __restrict__ u1, size_t plane, size_t skip,
+                                     double* __restrict__ out, size_t n, int C) {
   const T* __restrict__ src = ((stripe_swept(st) - st->fix_base) & 1) ? u1 : u0;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
-  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = static_cast<double>(src[i]);
+  const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int c = 0; c < C; ++c) {
+    const T* __restrict__ s = src + c * plane + skip;
+    double* __restrict__ d = out + c * n;
+    if constexpr (VEC && sizeof(T) == 8) {
+      for (size_t i = t0; i < n / 2; i += stride)
+        reinterpret_cast<double2*>(d)[i] = __ldg(reinterpret_cast<const double2*>(s) + i);
+    } else {
+      for (size_t i = t0; i < n; i += stride) d[i] = static_cast<double>(s[i]);
+    }
+  }
 }
 
 // A level resumed after its fixup: the iterate is in u0 again.
@@ -888,14 +900,20 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
         return;
       }
       const size_t rows_px = static_cast<size_t>(own.hi - own.lo) * S.w;
+      const size_t skip = static_cast<size_t>(own.lo - v.st.lo) * S.w;
       Timed t(x, K_INGEST, static_cast<double>(rows_px) * C * (8.0 + sizeof(T)));
-      for (int k = 0; k < C; ++k) {  // own rows of each plane -> compact output
-        const size_t off = static_cast<size_t>(k) * v.rows_n + static_cast<size_t>(own.lo) * S.w;
-        ++c.launch_count;
-        stripe_output_kernel<T><<<grid_for(rows_px, 256, 148 * 16), 256, 0, x.s>>>(
-            d_st, v.u[0] + off, v.u[1] + off, d_out + static_cast<size_t>(k) * rows_px, rows_px);
-        CK(cudaGetLastError());
-      }
+      ++c.launch_count;
+      const bool vec = sizeof(T) == 8 && rows_px % 2 == 0 && skip % 2 == 0 && v.rows_n % 2 == 0 &&
+                       ((reinterpret_cast<uintptr_t>(d_out) | reinterpret_cast<uintptr_t>(v.base_u[0]) |
+                         reinterpret_cast<uintptr_t>(v.base_u[1])) & 15) == 0;
+      const unsigned grid = 148 * 4;
+      if (vec)
+        stripe_output_kernel<T, true><<<grid, 256, 0, x.s>>>(d_st, v.base_u[0], v.base_u[1],
+                                                             v.rows_n, skip, d_out, rows_px, C);
+      else
+        stripe_output_kernel<T, false><<<grid, 256, 0, x.s>>>(d_st, v.base_u[0], v.base_u[1],
+                                                              v.rows_n, skip, d_out, rows_px, C);
+      CK(cudaGetLastError());
       return;
     }
     if (v.rows_n) {

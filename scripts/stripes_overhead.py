@@ -99,6 +99,9 @@ for G in (int(g) for g in a.ranks.split(",")):
             S.run_method_striped_device(solvers[r], comms[r], si.Method.MultilevelOras,
                                         fi.data_ptr(), mi.data_ptr(), W, H, C, oi.data_ptr(), o,
                                         stream=streams[r].cuda_stream)
+        if G == 1:  # one rank: no thread to start
+            rank(0)
+            return
         th = [threading.Thread(target=rank, args=(r,)) for r in range(G)]
         for t in th:
             t.start()
