@@ -231,6 +231,12 @@ void si_stripe_comm_destroy(si_stripe_comm* comm);
  * (results identical).  Off: one host round trip per decision.  Every rank
  * of a group must use the same setting. */
 si_status si_stripe_comm_set_speculation(si_stripe_comm* comm, int enabled);
+/* The finest own rows of the last striped solve on ctx that ran without an
+ * output buffer: channel k's rows start at *rows + k * *plane_stride
+ * (doubles), *n_rows rows of w; device memory owned by ctx, valid until its
+ * next call.  *rows is NULL when the rank owns no rows. */
+si_status si_stripe_result_rows(si_ctx* ctx, const double** rows, size_t* plane_stride,
+                                int* n_rows);
 /* out[0] solves, out[1] solves that speculated, out[2] resumed levels. */
 si_status si_stripe_comm_counters(const si_stripe_comm* comm, long long* out /* 3 */);
 
@@ -251,7 +257,9 @@ si_status si_run_method_striped(si_ctx* ctx, si_stripe_comm* comm, int method, c
                                 const uint8_t* mask, int w, int h, int c, const si_options* opt,
                                 double* out, si_report* report, si_trace_fn trace, void* user);
 /* Device-resident: d_f_rows / d_mask_rows hold level-0 rows [store_lo,
- * store_hi) (compact planar), d_out_rows receives rows [own_lo, own_hi). */
+ * store_hi) (compact planar), d_out_rows receives rows [own_lo, own_hi).
+ * d_out_rows may be NULL (FP64 / MIXED): the rows are then left where the
+ * solve put them, see si_stripe_result_rows (no device output pass). */
 si_status si_run_method_striped_device(si_ctx* ctx, si_stripe_comm* comm, int method,
                                        const double* d_f_rows, const uint8_t* d_mask_rows, int w,
                                        int h, int c, const si_options* opt, double* d_out_rows,

@@ -125,6 +125,7 @@ SIGNATURES = {
     "si_stripe_comm_init_local": (_i, [C.POINTER(_vp), _i, C.POINTER(_vp)]),
     "si_stripe_comm_destroy": (None, [_vp]),
     "si_stripe_comm_set_speculation": (_i, [_vp, _i]),
+    "si_stripe_result_rows": (_i, [_vp, C.POINTER(_vp), C.POINTER(C.c_size_t), _ip]),
     "si_stripe_comm_counters": (_i, [_vp, _llp]),
     "si_stripe_level_plan": (_i, [_i, _i, _i, _i, C.POINTER(si_options), _i, _i, _ip, _ip]),
     "si_run_method_striped": (_i, [_vp, _vp, _i, _vp, _vp, _i, _i, _i, C.POINTER(si_options),

@@ -552,10 +552,11 @@ __global__ void __launch_bounds__(128)
                            int fw, int fh, int C, int averaging, T* __restrict__ b0,
                            uint8_t* __restrict__ cmask, T* __restrict__ cval,
                            unsigned long long* known_count, int cy0 = 0, size_t fn_s = 0,
-                           size_t cn_s = 0) {
+                           size_t cn_s = 0, int klo = 0, int khi = 0x7fffffff) {
   // stripes: coarse rows cy0 + blockIdx.y; f / fmask / b0 / cmask / cval are
   // pre-offset storage pointers (index with global rows) whose planes are
-  // fn_s / cn_s apart; whole image: 0, 0, 0
+  // fn_s / cn_s apart, and only fine rows [klo, khi) are counted as known
+  // pixels (the rank's own rows); whole image: 0, 0, 0, all rows
   const int cw = (fw + 1) / 2;
   const int cy = cy0 + static_cast<int>(blockIdx.y);
   const size_t fn = fn_s ? fn_s : static_cast<size_t>(fw) * fh;
@@ -587,7 +588,9 @@ __global__ void __launch_bounds__(128)
       if (two_y) kb[q] |= (fmask[r1] != 0) << 2 | (two_x && fmask[r1 + 1] != 0) << 3;
     }
     const int known = __popc(kb[q]);
-    cnt += known;
+    const unsigned rows = (fy0 >= klo && fy0 < khi ? 3u : 0u) |
+                          (fy0 + 1 >= klo && fy0 + 1 < khi ? 12u : 0u);
+    cnt += __popc(kb[q] & rows);
     cmask[static_cast<size_t>(cy) * cw + cx] = known ? 1 : 0;
   }
   for (int c = 0; c < C; ++c) {

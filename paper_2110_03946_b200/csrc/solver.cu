@@ -213,6 +213,9 @@ struct si_ctx {
   DevBuf stripe_state;                          // StripeState per level + counter snapshots
   void* stripe_host = nullptr;                  // mapped mirror of the StripeStates
   void* stripe_hdev = nullptr;                  // device alias of stripe_host
+  const void* stripe_result = nullptr;          // finest own rows of the last striped solve
+  size_t stripe_result_stride = 0;              // elements between channel planes
+  int stripe_result_rows = 0, stripe_result_f64 = 0;
   void* stripe_log = nullptr;                   // mapped: finest-level trace rows
   size_t stripe_log_cap = 0;
   unsigned long long* host_state = nullptr;     // mapped: LevelState[SI_MAX_LEVELS]
@@ -2913,6 +2916,10 @@ void run_striped_device(si_ctx* ctx, si_stripe_comm* comm, int method, const dou
   begin_counters(x);
   Trace tr{trace, user, Clock::now()};
   const int flavour = flavour_for(method);
+  ctx->stripe_result = nullptr;
+  ctx->stripe_result_rows = 0;
+  check_arg(d_out != nullptr || o.precision != SI_PRECISION_FP32,
+            "stripes: an FP32 solve needs an output buffer (its rows are float in place)");
   if (o.precision == SI_PRECISION_FP32)
     stripe_solve_device<float>(x, *comm, P, flavour, d_f, d_mask, c, o, d_out, rep, tr);
   else
@@ -2932,18 +2939,24 @@ void run_striped_host(si_ctx* ctx, si_stripe_comm* comm, int method, const doubl
   Ctx x{*ctx, ctx->own_stream};
   ctx->stripe_in_f.ensure(std::max<size_t>(1, rows * W * c) * sizeof(double));
   ctx->stripe_in_mask.ensure(std::max<size_t>(1, rows * W));
-  ctx->stripe_out.ensure(std::max<size_t>(1, orows * W * c) * sizeof(double));
+  // double storage: the own rows are copied to the host straight from the
+  // level storage (no device output pass)
+  const bool in_place = o.precision != SI_PRECISION_FP32;
+  if (!in_place) ctx->stripe_out.ensure(std::max<size_t>(1, orows * W * c) * sizeof(double));
   const auto t0 = Clock::now();
   for (int k = 0; k < c && rows; ++k)
     h2d(x, ctx->stripe_in_f.as<double>() + k * rows * W, f + k * N + st.lo * W,
         rows * W * sizeof(double));
   if (rows) h2d(x, ctx->stripe_in_mask.ptr, mask + st.lo * W, rows * W);
   run_striped_device(ctx, comm, method, ctx->stripe_in_f.as<double>(),
-                     ctx->stripe_in_mask.as<uint8_t>(), w, h, c, o, ctx->stripe_out.as<double>(),
-                     rep, trace, user, ctx->own_stream);
+                     ctx->stripe_in_mask.as<uint8_t>(), w, h, c, o,
+                     in_place ? nullptr : ctx->stripe_out.as<double>(), rep, trace, user,
+                     ctx->own_stream);
+  const double* res = in_place ? static_cast<const double*>(ctx->stripe_result)
+                               : ctx->stripe_out.as<double>();
+  const size_t stride = in_place ? ctx->stripe_result_stride : orows * W;
   for (int k = 0; k < c && orows; ++k)
-    d2h(x, out + k * N + own.lo * W, ctx->stripe_out.as<double>() + k * orows * W,
-        orows * W * sizeof(double));
+    d2h(x, out + k * N + own.lo * W, res + k * stride, orows * W * sizeof(double));
   rep->h2d_bytes = static_cast<long long>(rows * W * (c * sizeof(double) + 1));
   rep->d2h_bytes = static_cast<long long>(orows * W * c * sizeof(double));
   rep->elapsed_ms = ms_since(t0);
@@ -3027,6 +3040,18 @@ si_status si_stripe_comm_init_local(si_ctx* const* ctxs, int world, si_stripe_co
 
 void si_stripe_comm_destroy(si_stripe_comm* comm) { delete comm; }
 
+si_status si_stripe_result_rows(si_ctx* ctx, const double** rows, size_t* plane_stride,
+                                int* n_rows) {
+  return guard([&] {
+    check_arg(ctx && rows && plane_stride && n_rows, "null argument");
+    check_arg(ctx->stripe_result == nullptr || ctx->stripe_result_f64,
+              "stripes: the last solve kept float rows");
+    *rows = static_cast<const double*>(ctx->stripe_result);
+    *plane_stride = ctx->stripe_result_stride;
+    *n_rows = ctx->stripe_result_rows;
+  });
+}
+
 si_status si_stripe_comm_set_speculation(si_stripe_comm* comm, int enabled) {
   return guard([&] {
     check_arg(comm != nullptr, "null argument");
@@ -3067,7 +3092,7 @@ si_status si_run_method_striped_device(si_ctx* ctx, si_stripe_comm* comm, int me
   si_report* rep = report ? report : &scratch;
   clear_report(rep);
   const si_status st = guard([&] {
-    check_arg(ctx && comm && d_f_rows && d_mask_rows && d_out_rows, "null argument");
+    check_arg(ctx && comm && d_f_rows && d_mask_rows, "null argument");
     set_device(ctx);
     const auto t0 = Clock::now();
     run_striped_device(ctx, comm, method, d_f_rows, d_mask_rows, w, h, c, opts_or_default(opt),

@@ -443,6 +443,7 @@ __global__ void stripe_decide_kernel(const double* __restrict__ g, int G, int C,
   for (int i = threadIdx.x; i < NG * G; i += blockDim.x) host_copy[i] = g[i];
   if (threadIdx.x != 0) return;
   if (cnt != nullptr) {  // one rank: the local counters directly (no stats pass)
+    host_copy[2 * C] = static_cast<double>(cnt[2]);
     host_copy[2 * C + 1] = static_cast<double>(cnt[0]);
     host_copy[2 * C + 2] = static_cast<double>(cnt[1]);
   }
@@ -461,7 +462,9 @@ __global__ void stripe_decide_kernel(const double* __restrict__ g, int G, int C,
     s.r0 = joint(r0_off);
     s.outer = s.iterations = s.converged = s.stop = s.fix_base = 0;
     double known = 0.0;
-    for (int r = 0; r < G; ++r) known += g[r * NG + 2 * C];
+    if (cnt != nullptr) known = static_cast<double>(cnt[2]);
+    else
+      for (int r = 0; r < G; ++r) known += g[r * NG + 2 * C];
     s.known_ok = known > 0.0;
   }
   if (!s.stop) {
@@ -513,8 +516,19 @@ __global__ void stripe_output_kernel(const StripeState* st, const T* __restrict_
     const T* __restrict__ s = src + c * plane + skip;
     double* __restrict__ d = out + c * n;
     if constexpr (VEC && sizeof(T) == 8) {
-      for (size_t i = t0; i < n / 2; i += stride)
-        reinterpret_cast<double2*>(d)[i] = __ldg(reinterpret_cast<const double2*>(s) + i);
+      // four 16-byte loads in flight per thread
+      const size_t m = n / 2;
+      const double2* __restrict__ s2 = reinterpret_cast<const double2*>(s);
+      double2* __restrict__ d2 = reinterpret_cast<double2*>(d);
+      size_t i = t0;
+      for (; i + 3 * stride < m; i += 4 * stride) {
+        double2 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __ldg(s2 + i + k * stride);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) d2[i + k * stride] = v[k];
+      }
+      for (; i < m; i += stride) d2[i] = __ldg(s2 + i);
     } else {
       for (size_t i = t0; i < n; i += stride) d[i] = static_cast<double>(s[i]);
     }
@@ -526,9 +540,10 @@ __global__ void stripe_rebase_kernel(StripeState* st) {
   if (threadIdx.x == 0) st->fix_base = stripe_swept(st);
 }
 
-// known pixels among n mask bytes -> *out (a double; exact below 2^53):
-// 16-byte loads over the aligned body, bytes at the ends
-__global__ void count_known_rows_kernel(const uint8_t* __restrict__ mask, size_t n, double* out) {
+// known pixels among n mask bytes -> *out: 16-byte loads over the aligned
+// body, bytes at the ends
+__global__ void count_known_rows_kernel(const uint8_t* __restrict__ mask, size_t n,
+                                        unsigned long long* out) {
   const size_t lead = (16 - (reinterpret_cast<uintptr_t>(mask) & 15)) & 15;
   const size_t head = n < lead ? n : lead;
   const size_t body = (n - head) / 16;
@@ -548,7 +563,7 @@ __global__ void count_known_rows_kernel(const uint8_t* __restrict__ mask, size_t
   if (tid < head) cnt += mask[tid] != 0;
   if (tid < n - tail0) cnt += mask[tail0 + tid] != 0;
   cnt = __reduce_add_sync(0xffffffffu, cnt);
-  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, static_cast<double>(cnt));
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, static_cast<unsigned long long>(cnt));
 }
 
 // K5 for rows [lo, hi) of a stripe store (pre-offset pointers, planes
@@ -565,11 +580,13 @@ __global__ void ingest_rows_kernel(const double* __restrict__ f, const uint8_t* 
   }
 }
 
-__global__ void stripe_stats_kernel(const unsigned long long* cnt, double solves, double* out) {
+// counters [failures, CG iterations, known pixels of my own rows] -> the
+// gather row's [known | failures | CG iterations] (exact below 2^53)
+__global__ void stripe_stats_kernel(const unsigned long long* cnt, double* out) {
   if (threadIdx.x == 0) {
-    out[0] = static_cast<double>(cnt[0]);
-    out[1] = static_cast<double>(cnt[1]);
-    out[2] = solves;
+    out[0] = static_cast<double>(cnt[2]);
+    out[1] = static_cast<double>(cnt[0]);
+    out[2] = static_cast<double>(cnt[1]);
   }
 }
 
@@ -586,7 +603,8 @@ RowBuf row_buf(T* storage, int w, Span store, int C) {
 
 // The striped multilevel solve of one rank.  d_f / d_mask hold the level-0
 // store rows (compact [C][rows][w] / [rows][w]); d_out receives the finest
-// own rows (compact).  Everything is issued on x.s.
+// own rows (compact), or is null: the rows stay in the level storage
+// (c.stripe_result, si_stripe_result_rows).  Everything is issued on x.s.
 template <typename T>
 void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, int flavour,
                          const double* d_f, const uint8_t* d_mask, int C, const si_options& o,
@@ -647,6 +665,7 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
   // the first K3 in one pass over the coarse store rows (as the direct path)
   // plus plain K5 for fine store rows outside twice them
   int restrict_from = 1;
+  bool known_counted = false;  // counters[2] = known pixels of my own level-0 rows
   if (depth > 1 && !ingest_fusion_disabled() && !V[1].st.empty()) {
     const StripeLevel& F = P.L[0];
     const Span cs = V[1].st, fs = V[0].st;
@@ -655,12 +674,15 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
                              static_cast<double>(V[1].rows_n) * (C * sizeof(T) + 1));
     const ptrdiff_t off0 = static_cast<ptrdiff_t>(fs.lo) * F.w;
     const double* f_pre = d_f - off0;
+    const Span own0 = F.own[me];
+    known_counted = own0.empty() || (pair.lo <= own0.lo && own0.hi <= pair.hi);
     const dim3 grid((P.L[1].w + 128 * kIrCells - 1) / (128 * kIrCells), cs.hi - cs.lo);
     ++c.launch_count;
     auto fused = [&](auto vec) {
       ingest_restrict_kernel<T, decltype(vec)::value><<<grid, 128, 0, x.s>>>(
           f_pre, V[0].mask, F.w, F.h, C, o.averaging, V[0].b, V[1].mask, V[1].b,
-          c.counters.as<unsigned long long>() + 2, cs.lo, V[0].rows_n, V[1].rows_n);
+          c.counters.as<unsigned long long>() + (known_counted ? 2 : 3), cs.lo, V[0].rows_n,
+          V[1].rows_n, own0.empty() ? 0 : own0.lo, own0.empty() ? 0 : own0.hi);
     };
     // the vector path moves cell pairs: even width (every offset even) and
     // 16-byte aligned f / 2-byte aligned mask
@@ -683,8 +705,8 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     if (n0) {
       Timed t(x, K_INGEST, static_cast<double>(n0) * (C * (8.0 + sizeof(T)) + 1.0));
       ++c.launch_count;
-      ingest_kernel<T><<<ingest_grid(n0), 256, 0, x.s>>>(
-          d_f, d_mask, n0, C, V[0].base_b, c.counters.as<unsigned long long>() + 2);
+      ingest_kernel<T><<<ingest_grid(n0), 256, 0, x.s>>>(  // counts halo rows too: sink
+          d_f, d_mask, n0, C, V[0].base_b, c.counters.as<unsigned long long>() + 3);
       CK(cudaGetLastError());
     }
   }
@@ -738,7 +760,7 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
   auto gather = [&](int level, bool first, bool r0_same = false) {
     if (G > 1) {  // one rank: nothing to gather, the decision reads the counters
       ++c.launch_count;
-      stripe_stats_kernel<<<1, 32, 0, x.s>>>(d_cnt, 0.0, d_send + 2 * C + 1);
+      stripe_stats_kernel<<<1, 32, 0, x.s>>>(d_cnt, d_send + 2 * C);
       CK(cudaGetLastError());
       comm.allgather(d_send, d_recv, NG, x.s);
     }
@@ -752,18 +774,19 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     CK(cudaGetLastError());
   };
   // known count of the rows this rank owns at level 0 (own rows tile the
-  // image): every gather carries it, the first decision checks it
-  // (build_rhs, operators.hpp:83)
+  // image; counted by the fused K5+K3 pass, else here): every gather
+  // carries it, the first decision checks it (build_rhs, operators.hpp:83)
   CK(cudaMemsetAsync(d_send, 0, sizeof(double) * NG, x.s));
-  {
+  if (!known_counted) {
     const StripeLevel& S = P.L[0];
     const Span own = S.own[me];
     if (!own.empty()) {
       ++c.launch_count;
-      count_known_rows_kernel<<<grid_for(static_cast<size_t>(own.hi - own.lo) * S.w, 256, 148 * 8),
+      count_known_rows_kernel<<<grid_for(static_cast<size_t>(own.hi - own.lo) * S.w / 16, 256,
+                                         148 * 8),
                                 256, 0, x.s>>>(V[0].mask + static_cast<size_t>(own.lo) * S.w,
                                                static_cast<size_t>(own.hi - own.lo) * S.w,
-                                               d_send + 2 * C);
+                                               d_cnt + 2);
       CK(cudaGetLastError());
     }
   }
@@ -891,7 +914,7 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     View& v = V[level];
     const Span own = S.own[me];
     if (level == 0) {
-      if (own.empty()) return;
+      if (own.empty() || d_out == nullptr) return;  // no output: the rows stay in place
       if (static_cast<const void*>(v.base_u[0]) == static_cast<const void*>(d_out)) {
         ++c.launch_count;
         stripe_fixup_kernel<T><<<grid_for(v.rows_n * C, 256, 148 * 8), 256, 0, x.s>>>(
@@ -1013,6 +1036,16 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     for (int i = 0; i <= h_st[0].iterations; ++i)
       tr.fn(i, static_cast<double>(log_host[1 + i].t - log_host[0].t) * 1e-6, log_host[1 + i].rel,
             std::numeric_limits<double>::quiet_NaN(), tr.user);
+  {  // where my finest own rows ended (si_stripe_result_rows)
+    const StripeState& st = h_st[0];
+    const int par = ((st.stop ? st.outer : st.outer - 1) - st.fix_base) & 1;
+    const Span own = P.L[0].own[me];
+    c.stripe_result = own.empty() ? nullptr
+                                  : V[0].base_u[par] + static_cast<size_t>(own.lo - V[0].st.lo) * P.L[0].w;
+    c.stripe_result_stride = V[0].rows_n;
+    c.stripe_result_rows = own.empty() ? 0 : own.hi - own.lo;
+    c.stripe_result_f64 = sizeof(T) == 8;
+  }
   rep->iterations = h_st[0].iterations;
   rep->final_relative_residual = h_st[0].final_rel;
   rep->converged = h_st[0].converged;

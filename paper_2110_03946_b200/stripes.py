@@ -150,10 +150,13 @@ def run_method_striped(solver: Solver, comm: StripeComm, method: Method, f: Imag
 
 
 def run_method_striped_device(solver: Solver, comm: StripeComm, method: Method, f_rows_ptr: int,
-                              mask_rows_ptr: int, w: int, h: int, c: int, out_rows_ptr: int,
-                              options: Optional[RunOptions] = None, stream=None):
+                              mask_rows_ptr: int, w: int, h: int, c: int,
+                              out_rows_ptr: Optional[int], options: Optional[RunOptions] = None,
+                              stream=None):
     """Device-resident: rows [store_lo, store_hi) of f / mask in, rows
-    [own_lo, own_hi) of the result out (level_plan(...)[0])."""
+    [own_lo, own_hi) of the result out (level_plan(...)[0]).  out_rows_ptr
+    None (FP64 / MIXED): the rows stay in the solver's storage, see
+    result_rows()."""
     options = options or RunOptions()
     rep = L.si_report()
     o = options.to_c()
@@ -161,6 +164,31 @@ def run_method_striped_device(solver: Solver, comm: StripeComm, method: Method, 
                                                  f_rows_ptr, mask_rows_ptr, w, h, c, C.byref(o),
                                                  out_rows_ptr, C.byref(rep), stream))
     return _report(rep)
+
+
+def result_rows(solver: Solver):
+    """(device pointer, plane stride in doubles, rows) of this rank's finest
+    own rows after a striped solve without an output buffer (valid until the
+    solver's next call); pointer 0 when the rank owns no rows."""
+    p = C.c_void_p()
+    stride = C.c_size_t()
+    rows = C.c_int()
+    _check(L.load().si_stripe_result_rows(solver.handle, C.byref(p), C.byref(stride),
+                                          C.byref(rows)))
+    return (p.value or 0), stride.value, rows.value
+
+
+def result_rows_tensor(solver: Solver, c: int, w: int):
+    """result_rows() as a torch view [c, rows, w] (float64, no copy)."""
+    import torch
+    ptr, stride, rows = result_rows(solver)
+    if not ptr:
+        return torch.empty((c, 0, w), dtype=torch.float64, device=f"cuda:{solver.device}")
+
+    class _Rows:
+        __cuda_array_interface__ = {"shape": (c, rows, w), "typestr": "<f8", "data": (ptr, False),
+                                    "version": 2, "strides": (8 * stride, 8 * w, 8)}
+    return torch.as_tensor(_Rows(), device=f"cuda:{solver.device}")
 
 
 def run_method_striped_group(solvers: Sequence[Solver], method: Method, f: ImageBuffer,

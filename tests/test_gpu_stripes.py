@@ -309,3 +309,59 @@ def test_c5_speculative_repeat(solver, forced):
     finally:
         for cm in comms:
             cm.close()
+
+
+@pytest.mark.parametrize("G", [1, 2, 3])
+def test_result_rows_in_place(solver, G):
+    """A device solve without an output buffer leaves each rank's rows in
+    its storage (si_stripe_result_rows): same rows as the single-GPU image,
+    including after a speculative repeat with an odd finest sweep count."""
+    import threading
+    import torch
+    w, h, c = 640, 480, 3
+    f = si.synthetic_test_image(w, h, c, 41)
+    m = si.random_mask(w, h, 0.05, 42)
+    o = si.RunOptions(levels=3, tolerance=1e-5)
+    single = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    sv = solvers(G)
+    comms = S.local_comms(sv)
+    plans = [S.level_plan(si.Method.MultilevelOras, w, h, c, o, G, r)[0] for r in range(G)]
+    ins = [(torch.from_numpy(np.ascontiguousarray(f.data[:, p.store_lo:p.store_hi])).cuda(),
+            torch.from_numpy(np.ascontiguousarray(m.known[p.store_lo:p.store_hi])).cuda())
+           for p in plans]
+    torch.cuda.synchronize()
+    reps = [None] * G
+    try:
+        for _ in range(2):
+            def rank(r):
+                reps[r] = S.run_method_striped_device(sv[r], comms[r], si.Method.MultilevelOras,
+                                                      ins[r][0].data_ptr(), ins[r][1].data_ptr(),
+                                                      w, h, c, None, o)
+            th = [threading.Thread(target=rank, args=(r,)) for r in range(G)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+            out = np.zeros_like(f.data)
+            for r, p in enumerate(plans):
+                out[:, p.own_lo:p.own_hi] = S.result_rows_tensor(sv[r], c, w).cpu().numpy()
+            check_same(single, si.ImageBuffer(data=out), reps, G)
+    finally:
+        for cm in comms:
+            cm.close()
+
+
+def test_fp32_needs_an_output_buffer(solver):
+    import torch
+    f = si.synthetic_test_image(64, 48, 1, 1)
+    m = si.random_mask(64, 48, 0.1, 2)
+    comm = S.local_comms([solver])[0]
+    try:
+        df = torch.from_numpy(f.data).cuda()
+        dm = torch.from_numpy(m.known).cuda()
+        with pytest.raises(si.InvalidArgument, match="FP32"):
+            S.run_method_striped_device(solver, comm, si.Method.MultilevelOras, df.data_ptr(),
+                                        dm.data_ptr(), 64, 48, 1, None,
+                                        si.RunOptions(precision=si.Precision.FP32))
+    finally:
+        comm.close()
