@@ -264,6 +264,19 @@ si_status si_run_method_striped_device(si_ctx* ctx, si_stripe_comm* comm, int me
                                        const double* d_f_rows, const uint8_t* d_mask_rows, int w,
                                        int h, int c, const si_options* opt, double* d_out_rows,
                                        si_report* report, void* stream);
+/* Every rank of a local group (si_stripe_comm_init_local) in one call, on
+ * device rows as si_run_method_striped_device: rank r on ctxs[r] and
+ * comms[r] with d_f_rows[r] / d_mask_rows[r] -> d_out_rows[r] (d_out_rows or
+ * an entry may be NULL: rows in place) on streams[r] (NULL: the context's).
+ * Ranks 1..world-1 run on the group's persistent host threads, rank 0 on the
+ * caller's.  One group call at a time per group. */
+si_status si_run_method_striped_local_device(si_stripe_comm* const* comms, si_ctx* const* ctxs,
+                                             int world, int method,
+                                             const double* const* d_f_rows,
+                                             const uint8_t* const* d_mask_rows, int w, int h,
+                                             int c, const si_options* opt,
+                                             double* const* d_out_rows, si_report* reports,
+                                             void* const* streams);
 /* Convenience: `world` ranks as threads of this process on ctxs[] over a
  * local communicator; out receives the whole image; reports: NULL or world. */
 si_status si_run_method_striped_group(si_ctx* const* ctxs, int world, int method, const double* f,

@@ -132,6 +132,10 @@ SIGNATURES = {
                                    _vp, C.POINTER(si_report), TRACE_FN, _vp]),
     "si_run_method_striped_device": (_i, [_vp, _vp, _i, _vp, _vp, _i, _i, _i,
                                           C.POINTER(si_options), _vp, C.POINTER(si_report), _vp]),
+    "si_run_method_striped_local_device": (_i, [C.POINTER(_vp), C.POINTER(_vp), _i, _i,
+                                                C.POINTER(_vp), C.POINTER(_vp), _i, _i, _i,
+                                                C.POINTER(si_options), C.POINTER(_vp),
+                                                C.POINTER(si_report), C.POINTER(_vp)]),
     "si_run_method_striped_group": (_i, [C.POINTER(_vp), _i, _i, _vp, _vp, _i, _i, _i,
                                          C.POINTER(si_options), _vp, C.POINTER(si_report)]),
     "si_partition_domain": (_i, [_i, _i, _i, _i, _ip, _ip, _ip, _i]),

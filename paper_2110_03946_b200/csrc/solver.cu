@@ -3104,6 +3104,45 @@ si_status si_run_method_striped_device(si_ctx* ctx, si_stripe_comm* comm, int me
   return st;
 }
 
+si_status si_run_method_striped_local_device(si_stripe_comm* const* comms, si_ctx* const* ctxs,
+                                             int world, int method,
+                                             const double* const* d_f_rows,
+                                             const uint8_t* const* d_mask_rows, int w, int h,
+                                             int c, const si_options* opt,
+                                             double* const* d_out_rows, si_report* reports,
+                                             void* const* streams) {
+  std::vector<si_status> sts(std::max(world, 1), SI_OK);
+  std::vector<std::string> errs(std::max(world, 1));
+  const si_status st = guard([&] {
+    check_arg(comms && ctxs && d_f_rows && d_mask_rows && world >= 1, "null argument");
+    auto* l0 = dynamic_cast<LocalComm*>(comms[0]);
+    check_arg(l0 != nullptr && l0->world == world,
+              "stripes: a group call needs the world's local communicators");
+    for (int r = 0; r < world; ++r) {
+      auto* lr = dynamic_cast<LocalComm*>(comms[r]);
+      check_arg(lr && lr->g == l0->g && lr->rank == r,
+                "stripes: communicators of one local group, in rank order");
+    }
+    l0->g->run_all([&](int r) {
+      sts[r] = si_run_method_striped_device(ctxs[r], comms[r], method, d_f_rows[r],
+                                            d_mask_rows[r], w, h, c, opt,
+                                            d_out_rows ? d_out_rows[r] : nullptr,
+                                            reports ? &reports[r] : nullptr,
+                                            streams ? streams[r] : nullptr);
+      if (sts[r] != SI_OK) errs[r] = g_last_error;
+    });
+  });
+  if (st != SI_OK) return st;
+  for (int pass = 0; pass < 2; ++pass)  // a failing rank first, then aborted peers
+    for (int r = 0; r < world; ++r)
+      if (sts[r] != SI_OK &&
+          (pass == 1 || errs[r].find("aborted by another rank") == std::string::npos)) {
+        g_last_error = errs[r];
+        return sts[r];
+      }
+  return SI_OK;
+}
+
 si_status si_run_method_striped_group(si_ctx* const* ctxs, int world, int method, const double* f,
                                       const uint8_t* mask, int w, int h, int c,
                                       const si_options* opt, double* out, si_report* reports) {

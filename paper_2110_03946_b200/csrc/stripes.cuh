@@ -312,7 +312,52 @@ struct LocalGroup {
     aborted = true;
     cv.notify_all();
   }
+
+  // Persistent host threads for ranks 1..world-1 of a one-call group solve
+  // (si_run_method_striped_local_device); rank 0 runs on the caller's
+  // thread.  Started on first use; one group call at a time.
+  std::vector<std::thread> workers;
+  std::mutex wm;
+  std::condition_variable wcv, wdone;
+  std::function<void(int)> job;
+  long long job_gen = 0;
+  int job_left = 0;
+  bool quit = false;
+  void run_all(const std::function<void(int)>& f) {
+    if (world > 1 && workers.empty())
+      for (int r = 1; r < world; ++r) workers.emplace_back([this, r] { worker(r); });
+    {
+      std::lock_guard<std::mutex> lk(wm);
+      job = f;
+      job_left = world - 1;
+      ++job_gen;
+    }
+    wcv.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> lk(wm);
+    wdone.wait(lk, [&] { return job_left == 0; });
+  }
+  void worker(int r) {
+    long long seen = 0;
+    std::unique_lock<std::mutex> lk(wm);
+    for (;;) {
+      wcv.wait(lk, [&] { return quit || job_gen != seen; });
+      if (quit) return;
+      seen = job_gen;
+      const std::function<void(int)> f = job;
+      lk.unlock();
+      f(r);
+      lk.lock();
+      if (--job_left == 0) wdone.notify_all();
+    }
+  }
   ~LocalGroup() {
+    {
+      std::lock_guard<std::mutex> lk(wm);
+      quit = true;
+    }
+    wcv.notify_all();
+    for (auto& t : workers) t.join();
     for (auto e : ready) if (e) cudaEventDestroy(e);
     for (auto e : done) if (e) cudaEventDestroy(e);
   }

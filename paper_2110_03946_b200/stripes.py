@@ -166,6 +166,29 @@ def run_method_striped_device(solver: Solver, comm: StripeComm, method: Method, 
     return _report(rep)
 
 
+def run_method_striped_local_device(solvers: Sequence[Solver], comms: Sequence[StripeComm],
+                                    method: Method, f_rows_ptrs, mask_rows_ptrs, w: int, h: int,
+                                    c: int, out_rows_ptrs=None,
+                                    options: Optional[RunOptions] = None, streams=None):
+    """Every rank of a local group in one call (ranks 1.. on the group's
+    persistent host threads): per-rank device rows as in
+    run_method_striped_device; out_rows_ptrs None = rows in place.  Returns
+    every rank's report."""
+    options = options or RunOptions()
+    G = len(solvers)
+    if len(comms) != G:
+        raise InvalidArgument("run_method_striped_local_device: one communicator per solver")
+    vp = C.c_void_p * G
+    rep = (L.si_report * G)()
+    o = options.to_c()
+    outs = None if out_rows_ptrs is None else vp(*out_rows_ptrs)
+    sts = None if streams is None else vp(*streams)
+    _check(L.load().si_run_method_striped_local_device(
+        vp(*[cm.handle for cm in comms]), vp(*[s.handle for s in solvers]), G, int(method),
+        vp(*f_rows_ptrs), vp(*mask_rows_ptrs), w, h, c, C.byref(o), outs, rep, sts))
+    return [_report(rep[r]) for r in range(G)]
+
+
 def result_rows(solver: Solver):
     """(device pointer, plane stride in doubles, rows) of this rank's finest
     own rows after a striped solve without an output buffer (valid until the

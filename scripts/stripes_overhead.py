@@ -1,7 +1,9 @@
 """Cost of the stripe decomposition on ONE B200 (BASELINE configs[4] shape):
 the 8K RGB frame solved directly (run_method_device) and as G virtual ranks
-(G host threads, one context and stream each, local communicator: device
-copies ordered by events, no kernel waits on another rank's kernel).  All
+(G host threads -- the local group's persistent C++ workers, or Python
+threads with --py-threads -- one context and stream each, local
+communicator: device copies ordered by events, no kernel waits on another
+rank's kernel).  All
 ranks share the one GPU, so this measures the decomposition's overhead
 (extra launches, halo copies, per-iteration all-gathers and host
 decisions), not multi-GPU scaling.  Device time: every rank's stream waits
@@ -31,6 +33,8 @@ ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--ranks", default="1,2,4")
 ap.add_argument("--copy-out", action="store_true", help="each rank copies its rows to an "
                 "output buffer (else they stay in place: si_stripe_result_rows)")
+ap.add_argument("--py-threads", action="store_true", help="one Python thread per rank "
+                "calling si_run_method_striped_device (else si_run_method_striped_local_device)")
 ap.add_argument("--sync", action="store_true", help="speculation off: one host round trip "
                 "per outer-iteration decision")
 a = ap.parse_args()
@@ -65,7 +69,8 @@ def timed(run_once, streams):
 
 
 out = {"workload": "7680x4320 RGB 2% 3 levels" + (" forced 2 sweeps" if a.forced else ""),
-       "speculation": not a.sync, "output": "copied" if a.copy_out else "in place"}
+       "speculation": not a.sync, "output": "copied" if a.copy_out else "in place",
+       "ranks_driven_by": "python threads" if a.py_threads else "si_run_method_striped_local_device"}
 solver = si.Solver(0)
 df = torch.from_numpy(f.data).cuda()
 dm = torch.from_numpy(m.known).cuda()
@@ -96,6 +101,14 @@ for G in (int(g) for g in a.ranks.split(",")):
     torch.cuda.synchronize()
 
     def group():
+        if not a.py_threads:  # one call: ranks 1.. on the group's persistent C++ threads
+            S.run_method_striped_local_device(
+                solvers, comms, si.Method.MultilevelOras, [i[0].data_ptr() for i in ins],
+                [i[1].data_ptr() for i in ins], W, H, C,
+                [i[2].data_ptr() for i in ins] if a.copy_out else None, o,
+                streams=[st.cuda_stream for st in streams])
+            return
+
         def rank(r):
             fi, mi, oi = ins[r]
             S.run_method_striped_device(solvers[r], comms[r], si.Method.MultilevelOras,

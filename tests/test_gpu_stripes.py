@@ -365,3 +365,60 @@ def test_fp32_needs_an_output_buffer(solver):
                                         si.RunOptions(precision=si.Precision.FP32))
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_local_device_group_call(solver, G):
+    """si_run_method_striped_local_device: the whole group in one call (the
+    group's persistent threads), repeated (speculative), rows in place and
+    copied out."""
+    import torch
+    w, h, c = 777, 333, 3
+    f = si.synthetic_test_image(w, h, c, 51)
+    m = si.random_mask(w, h, 0.04, 52)
+    o = si.RunOptions(levels=3, tolerance=1e-5)
+    single = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    sv = solvers(G)
+    comms = S.local_comms(sv)
+    plans = [S.level_plan(si.Method.MultilevelOras, w, h, c, o, G, r)[0] for r in range(G)]
+    ins = [(torch.from_numpy(np.ascontiguousarray(f.data[:, p.store_lo:p.store_hi])).cuda(),
+            torch.from_numpy(np.ascontiguousarray(m.known[p.store_lo:p.store_hi])).cuda(),
+            torch.empty((c, p.own_hi - p.own_lo, w), dtype=torch.float64, device="cuda"))
+           for p in plans]
+    torch.cuda.synchronize()
+    try:
+        for k in range(3):
+            copy = k == 1
+            reps = S.run_method_striped_local_device(
+                sv, comms, si.Method.MultilevelOras, [i[0].data_ptr() for i in ins],
+                [i[1].data_ptr() for i in ins], w, h, c,
+                [i[2].data_ptr() for i in ins] if copy else None, o)
+            out = np.zeros_like(f.data)
+            for r, p in enumerate(plans):
+                rows = ins[r][2] if copy else S.result_rows_tensor(sv[r], c, w)
+                out[:, p.own_lo:p.own_hi] = rows.cpu().numpy()
+            check_same(single, si.ImageBuffer(data=out), reps, G)
+        assert comms[0].counters()["speculative"] == 2
+    finally:
+        for cm in comms:
+            cm.close()
+
+
+def test_local_device_group_error_reaches_caller(solver):
+    import torch
+    f = si.synthetic_test_image(64, 64, 1, 1)
+    m = si.InpaintingMask(64, 64, 0)
+    sv = solvers(2)
+    comms = S.local_comms(sv)
+    plans = [S.level_plan(si.Method.MultilevelOras, 64, 64, 1, None, 2, r)[0] for r in range(2)]
+    ins = [(torch.from_numpy(np.ascontiguousarray(f.data[:, p.store_lo:p.store_hi])).cuda(),
+            torch.from_numpy(np.ascontiguousarray(m.known[p.store_lo:p.store_hi])).cuda())
+           for p in plans]
+    try:
+        with pytest.raises(si.InvalidArgument, match="no known pixels"):
+            S.run_method_striped_local_device(sv, comms, si.Method.MultilevelOras,
+                                              [i[0].data_ptr() for i in ins],
+                                              [i[1].data_ptr() for i in ins], 64, 64, 1)
+    finally:
+        for cm in comms:
+            cm.close()
