@@ -1,9 +1,9 @@
 """ncu launch list of one direct C5 solve and one G=1 / G=2 stripe solve
 (profiler range only around the measured solves):
   ncu --profile-from-start off --metrics gpu__time_duration.sum --csv \
-      python scripts/dev/stripes_launches.py"""
+      python scripts/stripes_launches.py"""
 import os, sys, threading
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_2110_03946_b200 as si
