@@ -30,6 +30,7 @@ from paper_2110_03946_b200 import stripes as S  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--forced", action="store_true")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--config", choices=["c5", "c3"], default="c5")
 ap.add_argument("--ranks", default="1,2,4")
 ap.add_argument("--copy-out", action="store_true", help="each rank copies its rows to an "
                 "output buffer (else they stay in place: si_stripe_result_rows)")
@@ -38,9 +39,12 @@ ap.add_argument("--py-threads", action="store_true", help="one Python thread per
 ap.add_argument("--sync", action="store_true", help="speculation off: one host round trip "
                 "per outer-iteration decision")
 a = ap.parse_args()
-W, H, C = 7680, 4320, 3
+if a.config == "c3":  # configs[2]: 4K RGB, 4%
+    W, H, C, dens = 3840, 2160, 3, 0.04
+else:               # configs[4]: 8K RGB, 2%
+    W, H, C, dens = 7680, 4320, 3, 0.02
 f = si.synthetic_test_image(W, H, C, 7)
-m = si.random_mask(W, H, 0.02, 11)
+m = si.random_mask(W, H, dens, 11)
 o = (si.RunOptions(levels=3, tolerance=1e-12, max_outer_iterations=2) if a.forced
      else si.RunOptions(levels=3))
 main = torch.cuda.current_stream()
@@ -68,7 +72,7 @@ def timed(run_once, streams):
     return statistics.median(ts)
 
 
-out = {"workload": "7680x4320 RGB 2% 3 levels" + (" forced 2 sweeps" if a.forced else ""),
+out = {"workload": f"{W}x{H} RGB {dens:.0%} 3 levels" + (" forced 2 sweeps" if a.forced else ""),
        "speculation": not a.sync, "output": "copied" if a.copy_out else "in place",
        "ranks_driven_by": "python threads" if a.py_threads else "si_run_method_striped_local_device"}
 solver = si.Solver(0)
