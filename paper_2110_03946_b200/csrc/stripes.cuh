@@ -457,14 +457,7 @@ struct StripeState {
   int known_ok;    // build_rhs: some known pixel (every decision carries the count)
 };
 
-// One stop decision from the gathered G x NG rows [sums C | r0 C | known |
-// failures | CG iterations | -], in the host path's arithmetic: per-channel
-// sums in rank order from 0.0, joint_norm, rel = joint / r0 (schwarz.hpp:
-// 288-320).  first: also r0 (from the sums at r0_off: C, or 0 when u0 = b
-// bitwise) and a fresh level.  A stopped level keeps its
-// outcome (the speculative iterations after it are no-ops).  The gathered
-// rows and the state are mirrored into mapped host memory; on the finest
-// level each decision is also a trace row (log, mapped, indexed by outer).
+// A finest-level trace row, written by the decision itself.
 struct StripeTraceRow {
   unsigned long long t;  // %globaltimer (ns) at the decision
   double rel;
@@ -480,12 +473,22 @@ __global__ void stripe_clock_kernel(unsigned long long* out) {
   if (threadIdx.x == 0) *out = global_ns();
 }
 
+// One stop decision from the gathered G x NG rows [sums C | r0 C | known |
+// failures | CG iterations | -], in the host path's arithmetic: per-channel
+// sums in rank order from 0.0, joint_norm, rel = joint / r0 (schwarz.hpp:
+// 288-320).  first: also r0 (from the sums at r0_off: C, or 0 when u0 = b
+// bitwise) and a fresh level.  A stopped level keeps its outcome (the
+// speculative iterations after it are no-ops).  The gathered rows and the
+// state are mirrored into mapped host memory; on the finest level each
+// decision is also a trace row (log, mapped, indexed by outer).  cnt (one
+// rank): the counters are read directly instead of through the gather.
 __global__ void stripe_decide_kernel(const double* __restrict__ g, int G, int C, double tol,
                                      int max_outer, StripeState* st, StripeState* mirror,
                                      double* host_copy, int first, int r0_off,
                                      StripeTraceRow* log, const unsigned long long* cnt) {
   const int NG = 2 * C + 4;
   for (int i = threadIdx.x; i < NG * G; i += blockDim.x) host_copy[i] = g[i];
+  __syncthreads();  // the copy lands before thread 0 overwrites the counter slots
   if (threadIdx.x != 0) return;
   if (cnt != nullptr) {  // one rank: the local counters directly (no stats pass)
     host_copy[2 * C] = static_cast<double>(cnt[2]);
