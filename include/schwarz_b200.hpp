@@ -20,6 +20,7 @@
 // returns std::span like image.hpp:44-52).  Link with libschwarz_b200.so.
 #pragma once
 
+#include <array>
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
@@ -391,6 +392,79 @@ inline std::vector<SolveResult> run_batch(
                                            f0.width, f0.height, f0.channels, &o, op.data(),
                                            reps.data()));
   for (size_t k = 0; k < frames.size(); ++k) res[k].report = detail::to_report(reps[k]);
+  return res;
+}
+
+// ---- one image over G ranks in horizontal stripes (configs[4]) ----
+// A communicator of the ranks: NCCL (one process per GPU; rank 0 makes the id
+// and the caller broadcasts it) or local (G ranks as threads of one process).
+class StripeComm {
+ public:
+  using NcclId = std::array<unsigned char, SI_NCCL_ID_BYTES>;
+  static NcclId nccl_unique_id() {
+    NcclId id{};
+    detail::throw_status(si_nccl_unique_id(id.data()));
+    return id;
+  }
+  static StripeComm nccl(Context& ctx, int world, int rank, const NcclId& id) {
+    si_stripe_comm* h = nullptr;
+    detail::throw_status(si_stripe_comm_init_nccl(ctx.get(), world, rank, id.data(), &h));
+    return StripeComm(h, world, rank);
+  }
+  // comms[r] for rank r, driven on contexts[r]
+  static std::vector<StripeComm> local(const std::vector<Context*>& contexts) {
+    const int world = static_cast<int>(contexts.size());
+    std::vector<si_ctx*> ctxs;
+    for (Context* c : contexts) ctxs.push_back(c->get());
+    std::vector<si_stripe_comm*> hs(contexts.size(), nullptr);
+    detail::throw_status(si_stripe_comm_init_local(ctxs.data(), world, hs.data()));
+    std::vector<StripeComm> out;
+    for (int r = 0; r < world; ++r) out.push_back(StripeComm(hs[r], world, r));
+    return out;
+  }
+  StripeComm(StripeComm&& o) noexcept : h_(o.h_), world_(o.world_), rank_(o.rank_) {
+    o.h_ = nullptr;
+  }
+  StripeComm& operator=(StripeComm&& o) noexcept {
+    std::swap(h_, o.h_);
+    world_ = o.world_;
+    rank_ = o.rank_;
+    return *this;
+  }
+  StripeComm(const StripeComm&) = delete;
+  StripeComm& operator=(const StripeComm&) = delete;
+  ~StripeComm() {
+    if (h_) si_stripe_comm_destroy(h_);
+  }
+  // repeated solves issue their outer iterations without host round trips
+  // (default on; every rank must agree)
+  void set_speculation(bool on) { detail::throw_status(si_stripe_comm_set_speculation(h_, on)); }
+  si_stripe_comm* get() const { return h_; }
+  int world() const { return world_; }
+  int rank() const { return rank_; }
+
+ private:
+  StripeComm(si_stripe_comm* h, int world, int rank) : h_(h), world_(world), rank_(rank) {}
+  si_stripe_comm* h_ = nullptr;
+  int world_ = 1, rank_ = 0;
+};
+
+// run_method over the ranks of `comm` (collective: every rank calls it with
+// the full image).  The result image holds this rank's own finest rows
+// (zeros elsewhere); the report and trace are the global ones.
+inline SolveResult run_method_striped(Method method, const ImageBuffer& f,
+                                      const InpaintingMask& mask, const RunOptions& options,
+                                      StripeComm& comm, Context& ctx) {
+  require_same_grid(f, mask);
+  SolveResult res;
+  res.image = ImageBuffer(f.width, f.height, f.channels);
+  si_report rep;
+  const si_options o = options.to_c();
+  detail::throw_status(si_run_method_striped(ctx.get(), comm.get(), static_cast<int>(method),
+                                             f.data.data(), mask.known.data(), f.width, f.height,
+                                             f.channels, &o, res.image.data.data(), &rep,
+                                             &detail::trace_sink, &res.trace));
+  res.report = detail::to_report(rep);
   return res;
 }
 

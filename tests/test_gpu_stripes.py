@@ -424,3 +424,55 @@ def test_local_device_group_error_reaches_caller(solver):
     finally:
         for cm in comms:
             cm.close()
+
+
+def test_cpp_dropin_striped_two_threads(tmp_path, solver):
+    """include/schwarz_b200.hpp: StripeComm::local + run_method_striped from
+    two C++ threads (two contexts on one GPU), solved twice (the second
+    speculates); the assembled image equals the single-GPU run_method."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "t.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include <thread>
+#include "schwarz_b200.hpp"
+namespace sb = schwarz_b200;
+int main() {
+  auto f = sb::synthetic_test_image(640, 480, 3, 9);
+  auto m = sb::random_mask(640, 480, 0.05, 10);
+  sb::RunOptions o; o.tolerance = 1e-5;
+  auto single = sb::run_method(sb::Method::MultilevelOras, f, m, o);
+  sb::Context c0(0), c1(0);
+  auto comms = sb::StripeComm::local({&c0, &c1});
+  int ok = 1;
+  for (int rep = 0; rep < 2; ++rep) {
+    sb::SolveResult r[2];
+    std::thread t([&] { r[1] = sb::run_method_striped(sb::Method::MultilevelOras, f, m, o, comms[1], c1); });
+    r[0] = sb::run_method_striped(sb::Method::MultilevelOras, f, m, o, comms[0], c0);
+    t.join();
+    for (size_t i = 0; i < f.data.size(); ++i) {
+      const double v = r[0].image.data[i] + r[1].image.data[i];  // own rows are disjoint
+      if (v != single.image.data[i]) ok = 0;
+    }
+    for (auto& x : r)
+      if (x.report.level_iterations != single.report.level_iterations ||
+          x.report.local_cg_iterations != single.report.local_cg_iterations ||
+          x.trace.rows.size() != single.trace.rows.size()) ok = 0;
+  }
+  long long cnt[3];
+  si_stripe_comm_counters(comms[0].get(), cnt);
+  std::printf("%d %lld %lld\n", ok, cnt[0], cnt[1]);
+  return 0;
+}
+''')
+    lib_dir = os.path.join(root, "paper_2110_03946_b200")
+    exe = str(tmp_path / "t")
+    cc = subprocess.run(["g++", "-std=c++17", "-O2", "-pthread", "-I", os.path.join(root, "include"),
+                         str(src), os.path.join(lib_dir, "libschwarz_b200.so"),
+                         f"-Wl,-rpath,{lib_dir}", "-o", exe], capture_output=True, text=True)
+    assert cc.returncode == 0, cc.stderr
+    run = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert run.returncode == 0, run.stderr
+    assert run.stdout.split() == ["1", "2", "1"], run.stdout
