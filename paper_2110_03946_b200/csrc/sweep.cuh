@@ -426,13 +426,6 @@ __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
     oras_sweep_kernel(const __grid_constant__ SweepArgs<T> a) {
   constexpr int R = 32 / NW;  // rows per thread
   __shared__ SweepSmem<T, NW, L> S;
-#ifdef SI_PROBE
-  const long long pr_k0 = clock64();
-  long long pr_k1 = pr_k0, pr_k2 = pr_k0;
-#endif
-#ifdef SI_PROBE_SETUP
-  long long pr_s0 = 0, pr_s1 = 0, pr_s2 = 0;
-#endif
 
   constexpr bool XT = kTmemX<L, NW, FULL>;
   constexpr bool QT = kTmemQ<L, NW, FULL>;
@@ -492,14 +485,7 @@ __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
       stage_u_tile<T, NW>(S.ut, c.u, c.x0, c.y0, B, c.W, a.srow_lo, a.srow_hi);
       __syncthreads();
     }
-#ifdef SI_PROBE_SETUP
-    pr_s0 = clock64();
-#endif
     unk = local_rhs<T, R, INV, L>(c, S.ut, r, kb, bv);
-#ifdef SI_PROBE_SETUP
-    if (unk == 0xdeadbeefu) a.u_new[0] = r[0];  // forces r complete before the stamp
-    pr_s1 = clock64();
-#endif
   };
   if (a.known_invariant)
     setup(std::true_type{});
@@ -530,9 +516,6 @@ __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
     }
   }
   const int any_unknown = __syncthreads_or(unk != 0);
-#ifdef SI_PROBE_SETUP
-  pr_s2 = clock64();
-#endif
 
   // Robin diagonals of my column: interior rows, block row 0, block row B-1.
   L dI = L(0), dT = L(0), dB = L(0);
@@ -556,21 +539,6 @@ __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
 
   int iters = 0;
   bool converged = true;
-#ifdef SI_PROBE
-  // cycles per CG-iteration segment (CTA thread 0): [0] apply + pAp reduction,
-  // [1] division + update + rr reduction, [2] beta + p update + staging
-  long long pr_t = 0, pr_seg[3] = {0, 0, 0};
-#define SI_PROBE_MARK(k)                                  \
-  do {                                                    \
-    const long long now_ = clock64();                     \
-    if ((k) >= 0) pr_seg[(k) < 0 ? 0 : (k)] += now_ - pr_t; \
-    pr_t = now_;                                          \
-  } while (0)
-#else
-#define SI_PROBE_MARK(k) \
-  do {                   \
-  } while (0)
-#endif
 
   if (any_unknown) {
 #pragma unroll
@@ -694,10 +662,6 @@ __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
       converged = true;
     } else {
       int until_check = a.lcheck;  // iter % lcheck == 0  <=>  countdown hits 0
-      SI_PROBE_MARK(-1);
-#ifdef SI_PROBE
-      pr_k1 = pr_t;
-#endif
       for (int iter = 1; iter <= a.lmax; ++iter) {
         L part_pq;
         if constexpr (QT) {
@@ -711,7 +675,6 @@ __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
           iters = iter - 1;
           break;
         }
-        SI_PROBE_MARK(0);
         // alpha = rr / pAp through the correctly rounded reciprocal and one
         // Markstein step (== the IEEE quotient, si_selftest 0): 2.81 -> 2.78 ms
         // per frame's sweeps; SI_ALPHA_DIV=1 keeps the division (A/B)
@@ -754,7 +717,6 @@ __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
         const bool cadence = until_check == a.lcheck || iter == a.lmax;
         bool maybe_done = rr_new < thr2_lo;
         if (rr_new >= thr2_lo && rr_new <= thr2_hi) maybe_done = band_sqrt_le(rr_new, thr);
-        SI_PROBE_MARK(1);
         if (cadence || maybe_done) {
           // True residual b - A x, then confirm or replace (cg.hpp:131-146).
           // the neighbours' boundary rows of x were published before the rr
@@ -802,15 +764,10 @@ __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
         rr = rr_new;
         rr_rcp = recip_rn(rr);
         if (iter == a.lmax) iters = a.lmax;
-        SI_PROBE_MARK(2);
       }
     }
   }
 
-#ifdef SI_PROBE
-  pr_k2 = clock64();
-  if (pr_k1 == pr_k0) pr_k1 = pr_k2;
-#endif
   // ---- accumulate_owned: u_new = u_old + v on the owned rectangle ----------
   // v = CG solution at unknown cells, the residual b - u at known cells.
   const int ox0 = a.ax.owned_begin(bx), ox1 = a.ax.owned_end(bx);
@@ -854,18 +811,6 @@ __global__ void __launch_bounds__(NW * 32, (kSweepMinBlocks<L, NW, FULL>))
   if (tid == 0 && a.counters && any_unknown) {
     if (!converged) atomicAdd(&a.counters[0], 1ull);
     atomicAdd(&a.counters[1], static_cast<unsigned long long>(iters));
-#ifdef SI_PROBE
-    const long long pr_k3 = clock64();
-#ifdef SI_PROBE_SETUP
-    pr_seg[0] = pr_s0 - pr_k0;
-    pr_seg[1] = pr_s1 - pr_s0;
-    pr_seg[2] = pr_k1 - pr_s1;
-#endif
-    for (int k = 0; k < 3; ++k)
-      atomicAdd(&a.counters[3 + k], static_cast<unsigned long long>(pr_seg[k]));
-    atomicAdd(&a.counters[6], static_cast<unsigned long long>(pr_k1 - pr_k0));
-    atomicAdd(&a.counters[7], static_cast<unsigned long long>(pr_k3 - pr_k2));
-#endif
   }
 }
 
