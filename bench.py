@@ -357,7 +357,62 @@ def c5_leg(args, world, rank, local, dist, solver):
                      / world / (ms / 1e3) / 1e9 / hbm_peak()[0]}
         del df, dm
     comm.close()
+    if world == 1:
+        out["virtual_g2"] = c5_virtual_g2(args, solver, f, m, w, h, c, out["tol"]["ms_per_frame"])
     return out
+
+
+def c5_virtual_g2(args, solver, f, m, w, h, c, ms_one):
+    """The stripe decomposition's overhead on one GPU: the configs[4] frame as
+    TWO ranks of a local group sharing this GPU (si_run_method_striped_local_device,
+    rows in place), CUDA events on both rank streams; not a scaling number."""
+    import torch
+    import paper_2110_03946_b200 as si
+    from paper_2110_03946_b200 import stripes as S
+    o = si.RunOptions(levels=LEVELS)
+    sv = [solver, si.Solver(solver.device)]
+    comms = S.local_comms(sv)
+    streams = [torch.cuda.Stream() for _ in sv]
+    plans = [S.level_plan(si.Method.MultilevelOras, w, h, c, o, 2, r)[0] for r in range(2)]
+    ins = [(torch.from_numpy(np.ascontiguousarray(f.data[:, p.store_lo:p.store_hi])).cuda(),
+            torch.from_numpy(np.ascontiguousarray(m.known[p.store_lo:p.store_hi])).cuda())
+           for p in plans]
+    main = torch.cuda.current_stream()
+
+    def run():
+        return S.run_method_striped_local_device(
+            sv, comms, si.Method.MultilevelOras, [i[0].data_ptr() for i in ins],
+            [i[1].data_ptr() for i in ins], w, h, c, None, o,
+            streams=[st.cuda_stream for st in streams])
+    for _ in range(max(args.warmup, 3)):
+        run()
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, 20))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(main)
+    for st in streams:
+        st.wait_event(e0)
+    for _ in range(steps):
+        reps = run()
+    for st in streams:
+        ev = torch.cuda.Event()
+        ev.record(st)
+        main.wait_event(ev)
+    e1.record(main)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    img = np.zeros_like(f.data)
+    for r, p in enumerate(plans):
+        img[:, p.own_lo:p.own_hi] = S.result_rows_tensor(sv[r], c, w).cpu().numpy()
+    ref = solver.run_method(si.Method.MultilevelOras, f, m, o)
+    res = {"ms_per_frame": ms, "ratio_to_one_rank": ms / ms_one, "steps": steps,
+           "bit_identical_to_1gpu": bool(np.array_equal(img, ref.image.data)) and
+           list(reps[0].level_iterations) == list(ref.report.level_iterations),
+           "speculative_solves": comms[0].counters()["speculative"],
+           "note": "two ranks on ONE GPU (local communicator): decomposition overhead"}
+    for cm in comms:
+        cm.close()
+    return res
 
 
 def spawn_ranks(n):
