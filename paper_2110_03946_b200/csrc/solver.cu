@@ -2359,10 +2359,6 @@ si_status si_run_method(si_ctx* ctx, int method, const double* f, const uint8_t*
     ctx->in_f.ensure(n * c * sizeof(double));
     ctx->in_mask.ensure(n);
     ctx->out_img.ensure(n * c * sizeof(double));
-    static const bool run_trace = [] {
-      const char* e = std::getenv("SI_RUN_TRACE");
-      return e && e[0] == '1';
-    }();
     KnownSamples ks{};
     const bool sparse = upload_known(x, f, mask, n, c, &ks);
     if (!sparse) h2d(x, ctx->in_f.ptr, f, n * c * sizeof(double));
@@ -2399,13 +2395,8 @@ si_status si_run_method(si_ctx* ctx, int method, const double* f, const uint8_t*
       if (prefault.valid()) prefault.wait();
       throw;
     }
-    const double t_solved = ms_since(t0);
     if (prefault.valid()) prefault.get();
-    const double t_faulted = ms_since(t0);
     d2h(x, out, ctx->out_img.ptr, out_bytes);
-    if (run_trace)
-      std::fprintf(stderr, "run_method: solved %.2f prefaulted %.2f copied-out %.2f ms\n",
-                   t_solved, t_faulted, ms_since(t0));
     rep->h2d_bytes = up;
     rep->d2h_bytes = static_cast<long long>(n * c * sizeof(double));
   });
