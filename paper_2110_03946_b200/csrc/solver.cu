@@ -3018,6 +3018,24 @@ si_status si_stripe_comm_init_local(si_ctx* const* ctxs, int world, si_stripe_co
       CK(cudaEventCreateWithFlags(&grp->ready[r], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&grp->done[r], cudaEventDisableTiming));
     }
+    // ranks on different GPUs of the process pull each other's rows over
+    // NVLink: peer access both ways where the devices support it (the
+    // caller's current device is restored)
+    int caller_dev = 0;
+    CK(cudaGetDevice(&caller_dev));
+    for (int r = 0; r < world; ++r)
+      for (int q = 0; q < world; ++q) {
+        const int a = ctxs[r]->device, b = ctxs[q]->device;
+        if (a == b) continue;
+        int can = 0;
+        CK(cudaDeviceCanAccessPeer(&can, a, b));
+        if (!can) continue;
+        CK(cudaSetDevice(a));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+        else CK(e);
+      }
+    CK(cudaSetDevice(caller_dev));
     for (int r = 0; r < world; ++r) {
       auto comm = new LocalComm();
       comm->world = world;
