@@ -3005,6 +3005,8 @@ si_status si_stripe_comm_init_nccl(si_ctx* ctx, int world, int rank, const unsig
 si_status si_stripe_comm_init_local(si_ctx* const* ctxs, int world, si_stripe_comm** out) {
   return guard([&] {
     check_arg(ctxs && out && world >= 1, "null argument");
+    int caller_dev = 0;
+    CK(cudaGetDevice(&caller_dev));
     auto grp = std::make_shared<LocalGroup>();
     grp->world = world;
     grp->ready.assign(world, nullptr);
@@ -3021,8 +3023,6 @@ si_status si_stripe_comm_init_local(si_ctx* const* ctxs, int world, si_stripe_co
     // ranks on different GPUs of the process pull each other's rows over
     // NVLink: peer access both ways where the devices support it (the
     // caller's current device is restored)
-    int caller_dev = 0;
-    CK(cudaGetDevice(&caller_dev));
     for (int r = 0; r < world; ++r)
       for (int q = 0; q < world; ++q) {
         const int a = ctxs[r]->device, b = ctxs[q]->device;
