@@ -7,21 +7,23 @@ level's own partition (partition_domain, partition.hpp:46-106); each rank
 allocates, ingests, restricts, sweeps and prolongs only its rows (plus
 halos).  Per outer iteration (run_schwarz_level, schwarz.hpp:288-320) the
 G x C partial residual sums are all-gathered, every rank takes the same stop
-decision (fixed rank order), sweeps its block rows and exchanges halo rows
-with the owners.  The image equals the single-GPU solve bit for bit whenever
-the stop decisions agree.
+decision on the device (fixed rank order), sweeps its block rows and
+exchanges halo rows with the owners; repeated solves of one shape issue
+their iterations without host round trips (speculation, resumed when a
+level needs more).  The image equals the single-GPU solve bit for bit
+whenever the stop decisions agree.
 
 Communicators:
   * `nccl_comm(solver, dist)`: one process per GPU; rank 0 makes the NCCL
     id, torch.distributed broadcasts it, the library drives NCCL
     (ncclAllGather + grouped ncclSend/ncclRecv on the solve stream);
   * `local_comms(solvers)`: G ranks as host threads of this process (any
-    devices, including G ranks on one GPU); device copies ordered by events.
+    devices, including G ranks on one GPU); device copies ordered by events;
+    `run_method_striped_local_device` drives the whole group in one call.
 """
 from __future__ import annotations
 
 import ctypes as C
-import threading
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
