@@ -213,6 +213,9 @@ SPEC_CASES = [
     (640, 360, 3, si.Method.MultilevelOras, dict(precision=si.Precision.MIXED), 4),
     (640, 360, 3, si.Method.MultilevelOras, dict(precision=si.Precision.FP32), 2),
     (96, 70, 2, si.Method.MultilevelOras, dict(levels=3), 8),  # ranks without rows
+    (300, 200, 3, si.Method.MultilevelOras,
+     dict(averaging=si.CoarseAveraging.AllPixels, normalizer=si.ResidualNormalizer.RhsNorm), 3),
+    (400, 300, 2, si.Method.Ras, dict(tolerance=1e-5), 2),
 ]
 
 
@@ -476,3 +479,23 @@ int main() {
     run = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert run.returncode == 0, run.stderr
     assert run.stdout.split() == ["1", "2", "1"], run.stdout
+
+
+def test_invalid_local_options_fail_like_the_reference(solver):
+    """Invalid local CG options are rejected when the first sweep is about to
+    run (cg_solve's check, cg.hpp:75-80), on every rank (the stripe engine
+    never speculates with options the sweep would reject)."""
+    f = si.synthetic_test_image(320, 240, 3, 61)
+    m = si.random_mask(320, 240, 0.05, 62)
+    o = si.RunOptions(levels=2)
+    o.local.tolerance = 0.0
+    with pytest.raises(si.InvalidArgument, match="tolerance must be positive"):
+        solver.run_method(si.Method.MultilevelOras, f, m, o)
+    sv = solvers(2)
+    comms = S.local_comms(sv)
+    try:
+        with pytest.raises(si.InvalidArgument, match="tolerance must be positive"):
+            _group_persistent(sv, comms, si.Method.MultilevelOras, f, m, o)
+    finally:
+        for cm in comms:
+            cm.close()
