@@ -211,7 +211,11 @@ inline bool host_is_pinned(const void* p) {
 // owner passes (it throws).
 class Stager {
  public:
-  static constexpr size_t kChunk = size_t(32) << 20;
+  // a ring of kBufs pinned chunks: the DMA of the next chunks overlaps the
+  // host copy of this one, and small chunks keep the unoverlapped first DMA
+  // and last host copy short (was 2 x 32 MB)
+  static constexpr size_t kChunk = size_t(8) << 20;
+  static constexpr int kBufs = 4;
 
   explicit Stager(std::function<void(cudaError_t, const char*)> check) : check_(std::move(check)) {}
   ~Stager() { release(); }
@@ -219,7 +223,7 @@ class Stager {
   Stager& operator=(const Stager&) = delete;
 
   void release() {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kBufs; ++b) {
       if (ev_[b]) cudaEventDestroy(ev_[b]);
       if (buf_[b]) cudaFreeHost(buf_[b]);
       ev_[b] = nullptr;
@@ -228,15 +232,16 @@ class Stager {
   }
 
   // dst (device) <- src (host).  Returns once the caller's buffer has been
-  // read; the last chunk's DMA may still be in flight on stream s.
+  // read; the last chunks' DMA may still be in flight on stream s.
   void h2d(void* dst, const void* src, size_t n, cudaStream_t s) {
     if (n < (size_t(1) << 20) || host_is_pinned(src)) {
       check_(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync H2D");
       return;
     }
     ensure();
-    int b = 0;
-    for (size_t off = 0; off < n; off += kChunk, b ^= 1) {
+    size_t k = 0;
+    for (size_t off = 0; off < n; off += kChunk, ++k) {
+      const int b = static_cast<int>(k % kBufs);
       const size_t len = std::min(kChunk, n - off);
       check_(cudaEventSynchronize(ev_[b]), "cudaEventSynchronize");  // chunk free again
       pool_.memcpy(buf_[b], static_cast<const char*>(src) + off, len);
@@ -259,17 +264,17 @@ class Stager {
     const size_t chunks = (n + kChunk - 1) / kChunk;
     auto issue = [&](size_t k) {
       const size_t off = k * kChunk, len = std::min(kChunk, n - off);
-      const int b = static_cast<int>(k & 1);
+      const int b = static_cast<int>(k % kBufs);
       check_(cudaMemcpyAsync(buf_[b], static_cast<const char*>(src) + off, len,
                              cudaMemcpyDeviceToHost, s),
              "cudaMemcpyAsync D2H");
       check_(cudaEventRecord(ev_[b], s), "cudaEventRecord");
     };
-    issue(0);
+    for (size_t k = 0; k < std::min<size_t>(kBufs - 1, chunks); ++k) issue(k);
     for (size_t k = 0; k < chunks; ++k) {
-      const int b = static_cast<int>(k & 1);
+      const int b = static_cast<int>(k % kBufs);
       check_(cudaEventSynchronize(ev_[b]), "cudaEventSynchronize");
-      if (k + 1 < chunks) issue(k + 1);  // next chunk's DMA overlaps this copy-out
+      if (k + kBufs - 1 < chunks) issue(k + kBufs - 1);  // keep kBufs - 1 DMAs ahead
       const size_t off = k * kChunk, len = std::min(kChunk, n - off);
       pool_.memcpy(static_cast<char*>(dst) + off, buf_[b], len);
     }
@@ -277,7 +282,7 @@ class Stager {
 
  private:
   void ensure() {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kBufs; ++b) {
       if (!buf_[b]) check_(cudaMallocHost(&buf_[b], kChunk), "cudaMallocHost");
       if (!ev_[b]) {
         check_(cudaEventCreateWithFlags(&ev_[b], cudaEventDisableTiming), "cudaEventCreate");
@@ -287,8 +292,8 @@ class Stager {
 
   std::function<void(cudaError_t, const char*)> check_;
   CopyPool pool_;
-  void* buf_[2] = {nullptr, nullptr};
-  cudaEvent_t ev_[2] = {nullptr, nullptr};
+  void* buf_[kBufs] = {};
+  cudaEvent_t ev_[kBufs] = {};
 };
 
 }  // namespace sib
