@@ -414,6 +414,87 @@ __global__ void __launch_bounds__(kResTmaThreads)
   pdl_trigger();
 }
 
+// K1p with b derived from u: after prolongation + snap the level's start
+// iterate equals b at known pixels and b is 0 elsewhere (the multilevel
+// invariant), so b = (mask ? u : 0) pixel for pixel and the pair needs one
+// TMA tile (u) plus the mask with a one-pixel halo (a 2-D box of
+// (128 + 32) x (band + 2) bytes starting 16 columns left: TMA wants 16-byte
+// aligned starts) instead of the u and b tiles: half the DRAM reads.  The
+// per-pixel terms are residual_pair_tma_kernel's bit for bit.
+template <typename T>
+__global__ void __launch_bounds__(kResTmaThreads)
+    residual_pair_derived_kernel(const __grid_constant__ CUtensorMap umap,
+                                 const __grid_constant__ CUtensorMap mmap, int W, int H,
+                                 int row0, int row1, int srow_lo, double* partials) {
+  __shared__ __align__(128) T tile[kResPairBand + 2][res_tma_box_w<T>()];
+  __shared__ __align__(128) uint8_t mt[kResPairBand + 2][kResTmaThreads + 32];
+  __shared__ uint64_t bar;
+  const int c = blockIdx.z;
+  const int x0 = blockIdx.x * kResTmaThreads;
+  const int x = x0 + threadIdx.x;
+  const int y0 = row0 + static_cast<int>(blockIdx.y) * kResPairBand;
+  const int ny = min(kResPairBand, row1 - y0);
+  const bool xin = x < W;
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, sizeof(tile) + sizeof(mt));
+    tma_load_3d(&tile[0][0], &umap, x0 - res_tma_lead<T>(), y0 - 1 - srow_lo, c, &bar);
+    tma_load_2d(&mt[0][0], &mmap, x0 - 16, y0 - 1 - srow_lo, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const int t = threadIdx.x + res_tma_lead<T>();  // tile column of x
+  const int m = threadIdx.x + 16;                  // mask column of x
+  const int deg_x = (x > 0) + (x + 1 < W);
+  const T deg_in = T(deg_x + 2);
+  double acc_u = 0.0, acc_b = 0.0;
+  T up = tile[0][t], ctr = tile[1][t];
+  bool mup = mt[0][m] != 0, mctr = mt[1][m] != 0;
+#pragma unroll
+  for (int k = 0; k < kResPairBand; ++k) {
+    const int y = y0 + k;
+    const T dn = tile[k + 2][t];
+    const bool mdn = mt[k + 2][m] != 0;
+    const T w = tile[k + 1][t - 1], e = tile[k + 1][t + 1];
+    const T deg = (y > 0 && y + 1 < H) ? deg_in : T(deg_x + (y > 0) + (y + 1 < H));
+    const bool in = xin && k < ny;
+    // u0
+    const T sum = ((w + e) + up) + dn;
+    const T au = fma(deg, ctr, -sum);
+    const double ru = (in && !mctr) ? static_cast<double>(au) : 0.0;
+    acc_u = fma(ru, ru, acc_u);
+    // b = (mask ? u : 0)
+    const T bw = mt[k + 1][m - 1] ? w : T(0), be = mt[k + 1][m + 1] ? e : T(0);
+    const T bn = mup ? up : T(0), bs = mdn ? dn : T(0);
+    const T sumb = ((bw + be) + bn) + bs;
+    const T ab = fma(deg, mctr ? ctr : T(0), -sumb);
+    const double rb = (in && !mctr) ? static_cast<double>(ab) : 0.0;
+    acc_b = fma(rb, rb, acc_b);
+    up = ctr;
+    ctr = dn;
+    mup = mctr;
+    mctr = mdn;
+  }
+  __shared__ double wsum[2][kResTmaThreads / 32];
+  acc_u = warp_sum(acc_u);
+  acc_b = warp_sum(acc_b);
+  if ((threadIdx.x & 31) == 0) {
+    wsum[0][threadIdx.x >> 5] = acc_u;
+    wsum[1][threadIdx.x >> 5] = acc_b;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kResTmaThreads / 32; ++w) s += wsum[threadIdx.x][w];
+    const size_t nblk = static_cast<size_t>(gridDim.x) * gridDim.y;
+    partials[(threadIdx.x * gridDim.z + blockIdx.z) * nblk + blockIdx.y * gridDim.x +
+             blockIdx.x] = s;
+  }
+  pdl_trigger();
+}
+
 // Fixed-order sum of nblk partials per channel (grid: one CTA per channel).
 __global__ void __launch_bounds__(kRedThreads)
     finish_partials_kernel(const double* __restrict__ partials, int nblk, double* out) {

@@ -328,6 +328,12 @@ bool ingest_fusion_disabled() {
   return off;
 }
 
+// SI_NO_PAIR_DERIVE=1: the pair pass reads b instead of deriving it (A/B).
+bool pair_derive_disabled() {
+  static const bool off = std::getenv("SI_NO_PAIR_DERIVE") != nullptr;
+  return off;
+}
+
 // SI_NO_TMA=1 forces the cooperative / cp.async staging paths (A/B runs).
 bool tma_disabled() {
   static const bool off = std::getenv("SI_NO_TMA") != nullptr;
@@ -469,6 +475,26 @@ void launch_residual_pair(Ctx& x, const uint8_t* mask, const T* u, const T* b, i
   const int HS = srow_hi - srow_lo;
   const size_t off = static_cast<size_t>(srow_lo) * W;
   CUtensorMap umap, bmap, mmap{};
+  // b derived from u (every caller runs the pair on a level's start iterate
+  // after prolongation + snap: u = b at known pixels, b = 0 elsewhere)
+  if (!pair_derive_disabled() && !tma_disabled() &&
+      make_plane_map(&umap, u + off, W, HS, C, sizeof(T), res_tma_box_w<T>(), kResPairBand + 2) &&
+      make_mask_map(&mmap, mask + off, W, HS, kResTmaThreads + 32, kResPairBand + 2)) {
+    const int rows = std::max(1, row1 - row0);
+    const int tx = (W + kResTmaThreads - 1) / kResTmaThreads;
+    const int gy = (rows + kResPairBand - 1) / kResPairBand;
+    x.c.red_partials.ensure(sizeof(double) * static_cast<size_t>(tx) * gy * 2 * C);
+    Timed t(x, K_RESIDUAL, static_cast<double>(W) * std::max(0, row1 - row0) * (C * sizeof(T) + 1));
+    ++x.c.launch_count;
+    launch_pdl(residual_pair_derived_kernel<T>, dim3(tx, gy, C), kResTmaThreads, x.s, umap, mmap,
+               W, H, row0, row1, srow_lo, x.c.red_partials.as<double>());
+    CK(cudaGetLastError());
+    ++x.c.launch_count;
+    launch_pdl(finish_partials_kernel, dim3(2 * C), kRedThreads, x.s,
+               static_cast<const double*>(x.c.red_partials.as<double>()), tx * gy, out);
+    CK(cudaGetLastError());
+    return;
+  }
   if (!tma_disabled() &&
       make_plane_map(&umap, u + off, W, HS, C, sizeof(T), res_tma_box_w<T>(), kResPairBand + 2) &&
       make_plane_map(&bmap, b + off, W, HS, C, sizeof(T), res_tma_box_w<T>(), kResPairBand + 2)) {
