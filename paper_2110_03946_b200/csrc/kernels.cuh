@@ -637,7 +637,8 @@ __global__ void __launch_bounds__(128)
   // stripes: coarse rows cy0 + blockIdx.y; f / fmask / b0 / cmask / cval are
   // pre-offset storage pointers (index with global rows) whose planes are
   // fn_s / cn_s apart, and only fine rows [klo, khi) are counted as known
-  // pixels (the rank's own rows); whole image: 0, 0, 0, all rows
+  // pixels (the rank's own rows); whole image: 0, 0, 0, all rows.  b0 null:
+  // the level-0 values are not written.
   const int cw = (fw + 1) / 2;
   const int cy = cy0 + static_cast<int>(blockIdx.y);
   const size_t fn = fn_s ? fn_s : static_cast<size_t>(fw) * fh;
@@ -711,7 +712,9 @@ __global__ void __launch_bounds__(128)
       const int fx0 = 2 * cx;
       const bool two_x = fx0 + 1 < fw;
       const size_t r0 = static_cast<size_t>(fy0) * fw + fx0, r1 = r0 + fw;
-      if (VEC) {
+      if (b0 == nullptr) {
+        // level-0 values not kept (their only reader, the snap, takes f)
+      } else if (VEC) {
         if constexpr (sizeof(T) == 8) {
           *reinterpret_cast<double2*>(bc + r0) = make_double2(a[q].a, a[q].b);
           if (two_y) *reinterpret_cast<double2*>(bc + r1) = make_double2(bb[q].a, bb[q].b);

@@ -463,6 +463,15 @@ void launch_residual(Ctx& x, const uint8_t* mask, const T* u, const T* b, int W,
   CK(cudaGetLastError());
 }
 
+// launch_residual_pair derives b from u on these buffers (whole level).
+template <typename T>
+bool pair_derivable(const uint8_t* mask, const T* u, int W, int H, int C) {
+  CUtensorMap umap, mmap;
+  return !pair_derive_disabled() && !tma_disabled() &&
+         make_plane_map(&umap, u, W, H, C, sizeof(T), res_tma_box_w<T>(), kResPairBand + 2) &&
+         make_mask_map(&mmap, mask, W, H, kResTmaThreads + 32, kResPairBand + 2);
+}
+
 // The start of a level: sums of u0 -> out[0..C) and canonical_r0's sums of
 // u = b -> out[C..2C) (normalizer InitialGuess, multilevel invariant), in one
 // K1 pass when TMA can address the buffers, else as two K1 launches.
@@ -1381,6 +1390,7 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
   // K5 ingest: level-0 values, known count for build_rhs's check.
   const size_t n0 = static_cast<size_t>(w) * h;
   bool fused_restrict = false;
+  bool skip_b0 = false;  // level-0 b not materialised (the snap reads d_f)
   if (ks) {  // K5s: only the known samples came over
     Timed t(x, K_INGEST, static_cast<double>(n0) * (C * sizeof(T) + 1.0) + ks->K * C * 8.0);
     ++x.c.launch_count;
@@ -1390,21 +1400,25 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
         x.c.counters.as<unsigned long long>() + 2);
     CK(cudaGetLastError());
   } else if (depth > 1 && !ingest_fusion_disabled()) {
-    // K5 + K3 fused: level-0 values and level 1 in one pass
-    Timed t(x, K_INGEST, static_cast<double>(n0) * (C * (8.0 + sizeof(T)) + 1.0) +
+    // K5 + K3 fused: level-0 values and level 1 in one pass.  fp64 Schwarz
+    // levels with the InitialGuess normaliser read level-0 b only where the
+    // prolongation snaps (f itself there) once the pair pass derives b from
+    // u0: then b0 is not written at all (199 MB per 4K RGB frame).
+    skip_b0 = std::is_same<T, double>::value && flavour != kFlavourCg && o.normalizer != 1 &&
+              pair_derivable(L[0].mask, L[0].u[0], w, h, C);
+    Timed t(x, K_INGEST, static_cast<double>(n0) * (C * ((skip_b0 ? 0.0 : 8.0) + sizeof(T)) + 1.0) +
                              static_cast<double>(lw[1]) * lh[1] * (C * sizeof(T) + 1));
     const dim3 grid((lw[1] + 128 * kIrCells - 1) / (128 * kIrCells), lh[1]);
+    T* b0 = skip_b0 ? nullptr : x.c.levels[0].b.as<T>();
     ++x.c.launch_count;
     if (w % 2 == 0)
       ingest_restrict_kernel<T, true><<<grid, 128, 0, x.s>>>(
-          d_f, d_mask, w, h, C, o.averaging, x.c.levels[0].b.as<T>(),
-          x.c.levels[1].mask.as<uint8_t>(), x.c.levels[1].b.as<T>(),
-          x.c.counters.as<unsigned long long>() + 2);
+          d_f, d_mask, w, h, C, o.averaging, b0, x.c.levels[1].mask.as<uint8_t>(),
+          x.c.levels[1].b.as<T>(), x.c.counters.as<unsigned long long>() + 2);
     else
       ingest_restrict_kernel<T, false><<<grid, 128, 0, x.s>>>(
-          d_f, d_mask, w, h, C, o.averaging, x.c.levels[0].b.as<T>(),
-          x.c.levels[1].mask.as<uint8_t>(), x.c.levels[1].b.as<T>(),
-          x.c.counters.as<unsigned long long>() + 2);
+          d_f, d_mask, w, h, C, o.averaging, b0, x.c.levels[1].mask.as<uint8_t>(),
+          x.c.levels[1].b.as<T>(), x.c.counters.as<unsigned long long>() + 2);
     CK(cudaGetLastError());
     fused_restrict = true;
   } else {
@@ -1506,7 +1520,12 @@ void multilevel_device(Ctx& x, int levels_req, int flavour, const double* d_f,
       LevelView<T>& F = L[level - 1];
       const size_t fn = static_cast<size_t>(F.w) * F.h;
       Timed t(x, K_PROLONG, static_cast<double>(fn) * (2.0 * C * sizeof(T) + 1.0) + n * C * sizeof(T));
-      launch_prolong<T>(x, V.u[V.cur], V.w, V.h, F.w, F.h, C, F.mask, F.b, F.u[0]);
+      // the snap's values: f itself when level-0 b was not kept (fp64: b0 == f
+      // at known pixels bit for bit)
+      const T* snap = F.b;
+      if constexpr (std::is_same<T, double>::value)
+        if (level == 1 && skip_b0) snap = d_f;
+      launch_prolong<T>(x, V.u[V.cur], V.w, V.h, F.w, F.h, C, F.mask, snap, F.u[0]);
       CK(cudaGetLastError());
       F.cur = 0;
     }
