@@ -714,21 +714,25 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
   // plus plain K5 for fine store rows outside twice them
   int restrict_from = 1;
   bool known_counted = false;  // counters[2] = known pixels of my own level-0 rows
+  bool skip_b0 = false;        // level-0 b not written: the snap reads f (as the direct path)
   if (depth > 1 && !ingest_fusion_disabled() && !V[1].st.empty()) {
     const StripeLevel& F = P.L[0];
     const Span cs = V[1].st, fs = V[0].st;
     const Span pair{2 * cs.lo, std::min(2 * cs.hi, F.h)};
-    Timed t(x, K_INGEST, static_cast<double>(V[0].rows_n) * (C * (8.0 + sizeof(T)) + 1.0) +
+    Timed t(x, K_INGEST, static_cast<double>(V[0].rows_n) * (C * 8.0 + 1.0) +
                              static_cast<double>(V[1].rows_n) * (C * sizeof(T) + 1));
     const ptrdiff_t off0 = static_cast<ptrdiff_t>(fs.lo) * F.w;
     const double* f_pre = d_f - off0;
     const Span own0 = F.own[me];
     known_counted = own0.empty() || (pair.lo <= own0.lo && own0.hi <= pair.hi);
     const dim3 grid((P.L[1].w + 128 * kIrCells - 1) / (128 * kIrCells), cs.hi - cs.lo);
+    skip_b0 = std::is_same<T, double>::value && o.normalizer != 1 &&
+              pair_derivable(V[0].base_mask, V[0].base_u[0], F.w, fs.hi - fs.lo, C);
+    T* b0 = skip_b0 ? nullptr : V[0].b;
     ++c.launch_count;
     auto fused = [&](auto vec) {
       ingest_restrict_kernel<T, decltype(vec)::value><<<grid, 128, 0, x.s>>>(
-          f_pre, V[0].mask, F.w, F.h, C, o.averaging, V[0].b, V[1].mask, V[1].b,
+          f_pre, V[0].mask, F.w, F.h, C, o.averaging, b0, V[1].mask, V[1].b,
           c.counters.as<unsigned long long>() + (known_counted ? 2 : 3), cs.lo, V[0].rows_n,
           V[1].rows_n, own0.empty() ? 0 : own0.lo, own0.empty() ? 0 : own0.hi);
     };
@@ -740,7 +744,7 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     else fused(std::false_type{});
     CK(cudaGetLastError());
     std::vector<Span> rest;
-    span_minus(fs, pair, rest);
+    if (!skip_b0) span_minus(fs, pair, rest);
     for (const Span& r : rest) {
       ++c.launch_count;
       ingest_rows_kernel<T><<<grid_for(static_cast<size_t>(r.hi - r.lo) * F.w, 256, 148 * 4), 256,
@@ -1009,7 +1013,10 @@ void stripe_solve_device(Ctx& x, si_stripe_comm& comm, const StripeLayout& P, in
     const Span fw = F.win[me];
     if (!fw.empty()) {
       Timed t(x, K_PROLONG, static_cast<double>(fw.hi - fw.lo) * F.w * (2.0 * C * sizeof(T) + 1.0));
-      launch_prolong<T>(x, v.u[0], S.w, S.h, F.w, F.h, C, fv.mask, fv.b, fv.u[0], fw.lo, fw.hi,
+      const T* snap = fv.b;  // the snap's values (f itself when b0 was not kept)
+      if constexpr (std::is_same<T, double>::value)
+        if (level == 1 && skip_b0) snap = d_f - static_cast<ptrdiff_t>(fv.st.lo) * F.w;
+      launch_prolong<T>(x, v.u[0], S.w, S.h, F.w, F.h, C, fv.mask, snap, fv.u[0], fw.lo, fw.hi,
                         v.st.lo, v.st.hi, fv.rows_n, v.rows_n, fv.st.lo);
     }
   };
