@@ -245,11 +245,6 @@ __global__ void __launch_bounds__(kResTmaThreads)
   pdl_wait();  // u is the predecessor's output
   if (skip != nullptr && *skip) return;  // stripes: the level has stopped (every CTA alike)
   if (threadIdx.x == 0) {
-#ifdef SI_TMA_DEBUG
-    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0)
-      printf("tile smem %u (mod128 %u) bar %u bytes %u\n", smem_addr(&tile[0][0]),
-             smem_addr(&tile[0][0]) % 128, smem_addr(&bar), (unsigned)sizeof(tile));
-#endif
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, sizeof(tile) + (MTMA ? sizeof(mtile) : 0));
     // the maps cover the storage rows (stripe mode: [srow_lo, ...)): rows
