@@ -841,3 +841,39 @@ def test_repeated_headline_solves_are_bit_identical(solver):
         assert [x.psnr for x in r.trace.rows] == [x.psnr for x in base.trace.rows]
         assert r.report.local_cg_iterations == base.report.local_cg_iterations
         assert r.report.local_failures == base.report.local_failures
+
+
+@pytest.mark.parametrize("size", [(3840, 2160, 3, 0.04), (640, 480, 3, 0.05)])
+def test_data_movement_switches_are_bit_identical(size):
+    """The pair pass deriving b from u0 and the unwritten level-0 b change
+    only data movement: with SI_NO_PAIR_DERIVE / SI_NO_INGEST_FUSION (b0
+    written and read back) the device path's image and report are the same
+    bits."""
+    import hashlib
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    w, h, c, d = size
+    code = (
+        "import sys, json, hashlib; sys.path.insert(0, %r)\n"
+        "import torch\n"
+        "import paper_2110_03946_b200 as si\n"
+        "f = si.synthetic_test_image(%d, %d, %d, 7); m = si.random_mask(%d, %d, %r, 11)\n"
+        "df = torch.from_numpy(f.data).cuda(); dm = torch.from_numpy(m.known).cuda()\n"
+        "do = torch.empty_like(df)\n"
+        "r = si.Solver(0).run_method_device(si.Method.MultilevelOras, df.data_ptr(),\n"
+        "    dm.data_ptr(), %d, %d, %d, do.data_ptr(), si.RunOptions())\n"
+        "torch.cuda.synchronize()\n"
+        "print(json.dumps({'img': hashlib.sha256(do.cpu().numpy().tobytes()).hexdigest(),\n"
+        "  'levels': list(r.level_iterations), 'rel': r.final_relative_residual.hex(),\n"
+        "  'cg': r.local_cg_iterations, 'fails': r.local_failures}))\n"
+    ) % (root, w, h, c, w, h, d, w, h, c)
+    outs = []
+    for env in ({}, {"SI_NO_PAIR_DERIVE": "1"}, {"SI_NO_INGEST_FUSION": "1"}):
+        run = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                             timeout=300, env={**os.environ, **env})
+        assert run.returncode == 0, run.stderr[-2000:]
+        outs.append(json.loads(run.stdout.strip().splitlines()[-1]))
+    assert outs[1] == outs[0]
+    assert outs[2] == outs[0]
